@@ -1,0 +1,435 @@
+"""bench.py -- batched energy-prediction throughput on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload c2|c5s] [--kernels N_KERNELS]
+
+Workload (default "c2"): BASELINE.json configs[1] -- 10k synthetic kernels x the
+64-config launch grid on the tesla_k20 profile (640k points per GPU) -- run
+through the FULL energy pipeline (static features K1 -> cycle estimator +
+features K2/K3 -> 500-tree depth-16 ensemble K4 -> energy K6), because the
+metric is energy-prediction points/s.  "c5s" is one GPU's slice of configs[4]
+(256 configs x 3 archs, one ensemble per arch) with the kernel count chosen by
+--kernels.  A step = one sweep over the GPU's points with inputs resident in
+HBM.  Multi-GPU (torchrun): every rank sweeps its own kernel shard (weak
+scaling, no data-path collective); time = max over ranks.
+
+One JSON line on rank 0.  See DESIGN.md §Measurement for the byte accounting.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path[:0] = [str(ROOT), str(ROOT / "oracle")]
+
+PEAKS = ROOT / "MEASURED_PEAKS.json"
+FALLBACK_HBM = 6650.0
+
+
+def hbm_peak():
+    try:
+        return float(json.loads(PEAKS.read_text())["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows: list = []
+        self.proc = None
+        self.thread = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[4:8]) if v == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# --------------------------------------------------------------- workload
+
+
+def build_workload(args, rank: int):
+    from paper_2305_01886_b200 import corpus as CG
+    from paper_2305_01886_b200 import pack, workloads
+    from paper_2305_01886_b200.profiles import resolve_profile
+
+    if args.workload == "c2":
+        n_k = args.kernels or 10000
+        cfgs = CG.config2_grid()
+        archs = ["tesla_k20"]
+    elif args.workload == "c5s":
+        n_k = args.kernels or 2000
+        cfgs = CG.config5_grid()
+        archs = ["tesla_k20", "tesla_m60", "gtx1050"]
+    else:
+        raise SystemExit(f"unknown workload {args.workload}")
+    t0 = time.time()
+    c = workloads.synth_packed(n_k, seed=1000 + rank)
+    profs = [resolve_profile(a) for a in archs]
+    sel = pack.manifest_indices(pack.SELECTED_FEATURES)
+    return {"corpus": c, "profiles": profs, "configs": cfgs, "archs": archs, "sel": sel,
+            "n_k": n_k, "build_s": time.time() - t0}
+
+
+def make_ensembles(W, dc, dg, rt, n_trees, depth):
+    """Declared synthetic ensembles: n_trees random trees of
+    depth `depth` (~109k nodes each at depth 16), scaling bounds = min/max of the
+    workload's own features (what MinMaxScaler would fit)."""
+    import torch
+
+    from paper_2305_01886_b200 import pack
+    from paper_2305_01886_b200.ensemble import random_forest_flat
+
+    out = rt.schedule_features(dc, dg, si=False, sf=False, feat=False, sel_idx=W["sel"])
+    X = out["sel"]
+    ok = out["status"] == 0
+    Xo = X[ok]
+    lo = torch.nan_to_num(Xo.min(dim=0).values).cpu().numpy()
+    hi = torch.nan_to_num(Xo.max(dim=0).values).cpu().numpy()
+    flats = [random_forest_flat(n_trees, depth, pack.SELECTED_FEATURES, lo, hi, seed=7 + a)
+             for a in range(len(W["profiles"]))]
+    return flats
+
+
+# ----------------------------------------------------------------- ours
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2305_01886_b200 import runtime as rt
+
+    torch.cuda.set_device(local_rank)
+    W = build_workload(args, rank)
+    c = W["corpus"]
+    dc = rt.DeviceCorpus.upload(c)
+    dg = rt.DeviceGrid.build(dc, W["profiles"], W["configs"])
+    n_pts = dg.n_points
+    flats = make_ensembles(W, dc, dg, rt, args.trees, args.depth)
+    ens = [rt.DeviceEnsemble.upload(f) for f in flats]
+    sweep = rt.Sweep(dc, dg, ens, W["sel"])
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+
+    for _ in range(args.warmup):
+        sweep.run()
+    torch.cuda.synchronize()
+
+    # ---- timed: K steps, device events per step, L2 flushed (untimed) between steps
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        for k in range(args.steps):
+            flush.zero_()
+            evs[k][0].record(stream)
+            sweep.run()
+            evs[k][1].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    total_ms = float(sum(step_ms))
+
+    # ---- per-kernel split (same stream, events between launches)
+    split = per_kernel_split(rt, dc, dg, sweep, W, flush, args.steps)
+
+    # ---- e2e: host buffers in, results out, through the C-ABI per step
+    e2e = run_e2e(rt, W, c, dg, sweep, args.steps, flush)
+
+    # ---- reductions across ranks (max time, sum of points)
+    t = torch.tensor([total_ms, e2e["ms"]], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms, e2e_ms = float(t[0]), float(t[1])
+    st = sweep.status.cpu().numpy()
+    return {"W": W, "n_pts": n_pts, "total_ms": total_ms, "step_ms": step_ms, "split": split,
+            "e2e_ms": e2e_ms, "e2e": e2e, "clk": clk.summary(), "flats": flats,
+            "infeasible": int((st != 0).sum()), "dc_bytes": dc.nbytes}
+
+
+def per_kernel_split(rt, dc, dg, sweep, W, flush, steps):
+    """Average device time of each stage, CUDA events on the launching stream."""
+    import torch
+
+    stream = torch.cuda.current_stream()
+    ks, ls = rt.static_features(dc, dg)
+    names = ["k1_static", "k23_schedule", "k4_rf_predict"]
+    acc = {n: 0.0 for n in names}
+    n = max(steps, 1)
+    out = None
+    for _ in range(n):
+        flush.zero_()
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        e[0].record(stream)
+        ks, ls = rt.static_features(dc, dg)
+        e[1].record(stream)
+        out = rt.schedule_features(dc, dg, si=False, sf=True, feat=False, sel_idx=W["sel"])
+        e[2].record(stream)
+        rt.rf_predict(sweep.ens[0], out["sel"], status=out["status"], time_us=out["sf"][:, 7])
+        e[3].record(stream)
+        torch.cuda.synchronize()
+        for i, nm in enumerate(names):
+            acc[nm] += e[i].elapsed_time(e[i + 1])
+    return {k: v / n for k, v in acc.items()}
+
+
+def run_e2e(rt, W, c, dg, sweep, steps, flush):
+    """Reference-facing call with HOST buffers: pinned host corpus -> H2D ->
+    sweep -> D2H of (status, time, power, energy), all inside the timing."""
+    import torch
+
+    host = {k: torch.from_numpy(np.ascontiguousarray(getattr(c, k)).view(np.uint8)
+                                if getattr(c, k).dtype.fields else np.ascontiguousarray(getattr(c, k))).pin_memory()
+            for k in ("tok", "preds", "blk", "fpreds", "topo", "ker")}
+    dev = {k: sweep.dc.bufs[k] for k in host}
+    n = dg.n_points
+    outs = {k: torch.empty(n, dtype=dt).pin_memory() for k, dt in
+            (("status", torch.uint8), ("time", torch.float64), ("power", torch.float64),
+             ("energy", torch.float64))}
+    h2d = sum(v.numel() * v.element_size() for v in host.values())
+    d2h = n * (1 + 8 * 3)
+    stream = torch.cuda.current_stream()
+    ms = 0.0
+    for _ in range(steps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for k in host:
+            dev[k].copy_(host[k], non_blocking=True)
+        st, tu, pw, en = sweep.run()
+        outs["status"].copy_(st, non_blocking=True)
+        outs["time"].copy_(tu, non_blocking=True)
+        outs["power"].copy_(pw, non_blocking=True)
+        outs["energy"].copy_(en, non_blocking=True)
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms += a.elapsed_time(b)
+    return {"ms": ms, "h2d": h2d, "d2h": d2h}
+
+
+# ------------------------------------------------------------ CPU legs
+
+
+def cpu_sample(args, W, flats, n_kernels: int, threads: int):
+    """Oracle (CPU restatement, `kind: port`) over the first n_kernels kernels of
+    the workload: schedule + features + ensemble + energy.  Returns (points, s)."""
+    import oracle as O
+
+    c = W["corpus"]
+    hg = O.HostGrid(c, W["profiles"], W["configs"], kernel_ids=np.arange(n_kernels))
+    t0 = time.perf_counter()
+    out = O.schedule_features(hg, sel_idx=W["sel"], threads=threads)
+    n_cfg, n_arch = len(W["configs"]), len(W["profiles"])
+    arch_of = (np.arange(hg.n_points) // n_cfg) % n_arch
+    for a in range(n_arch):
+        m = arch_of == a
+        O.rf_predict(flats[a], out["sel"][m], status=out["status"][m],
+                     time_us=np.nan_to_num(out["sf"][m, 7]), threads=threads)
+    return hg.n_points, time.perf_counter() - t0
+
+
+def cpu_flats(args, W):
+    """Ensembles for CPU-only runs (no device): bounds from oracle features."""
+    import oracle as O
+
+    from paper_2305_01886_b200 import pack
+    from paper_2305_01886_b200.ensemble import random_forest_flat
+
+    hg = O.HostGrid(W["corpus"], W["profiles"], W["configs"],
+                    kernel_ids=np.arange(min(200, W["n_k"])))
+    out = O.schedule_features(hg, sel_idx=W["sel"])
+    X = out["sel"][out["status"] == 0]
+    lo, hi = np.nanmin(X, axis=0), np.nanmax(X, axis=0)
+    return [random_forest_flat(args.trees, args.depth, pack.SELECTED_FEATURES, lo, hi, seed=7 + a)
+            for a in range(len(W["profiles"]))]
+
+
+def sample_kernels(W, target_s: float, threads: int, flats) -> int:
+    pts, dt = cpu_sample(None, W, flats, 2, threads)
+    per_kernel = dt / 2
+    return int(max(2, min(W["n_k"], target_s / max(per_kernel, 1e-6))))
+
+
+# ------------------------------------------------------------------ main
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c2", choices=["c2", "c5s"])
+    ap.add_argument("--kernels", type=int, default=0)
+    ap.add_argument("--trees", type=int, default=500)
+    ap.add_argument("--depth", type=int, default=16)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    threads = os.cpu_count() or 1
+    metric = "energy-prediction points/sec"
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        W = build_workload(args, 0)
+        flats = cpu_flats(args, W)
+        nk = sample_kernels(W, args.cpu_seconds / max(args.steps + args.warmup, 1), threads, flats)
+        for _ in range(1):
+            cpu_sample(args, W, flats, min(nk, 2), threads)
+        pts = sec = 0.0
+        for _ in range(args.steps):
+            p, s = cpu_sample(args, W, flats, nk, threads)
+            pts += p
+            sec += s
+        v = pts / sec
+        sample = (f"first {nk} kernels x {len(W['configs'])} configs x {len(W['archs'])} arch "
+                  f"per step ({int(pts / args.steps)} points), oracle port, {threads} threads")
+        print(json.dumps({
+            "impl": "reference", "metric": metric, "value": v, "unit": "points/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": sec / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_name(args), "kernels": W["n_k"],
+                       "configs": len(W["configs"]), "archs": W["archs"],
+                       "ensemble": f"{args.trees} trees depth {args.depth} (declared random)"},
+            "cpu_baseline": {"value": v, "unit": "points/s", "cores": threads, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": v, "unit": "points/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}))
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    R = run_ours(args, rank, world, local_rank)
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    W = R["W"]
+    n_total = R["n_pts"] * world
+    value = n_total * args.steps / (R["total_ms"] / 1e3)
+    e2e_value = n_total * args.steps / (R["e2e_ms"] / 1e3)
+    # roofline of the dominant kernel
+    split = R["split"]
+    dom = max(split, key=split.get)
+    n_pts = R["n_pts"]
+    flat = R["flats"][0]
+    ens_bytes = int(flat.nodes.nbytes)
+    nsel = len(W["sel"])
+    alg = {
+        # tokens + preds + blocks + kernels read once, config + outputs per point
+        "k1_static": R["dc_bytes"] + W["n_k"] * (64 + 24),
+        "k23_schedule": R["dc_bytes"] + W["n_k"] * (64 + 24) + n_pts * (1 + 8 * 9 + 8 * nsel),
+        "k4_rf_predict": ens_bytes * len(R["flats"]) + n_pts * (8 * nsel + 1 + 8 + 16),
+    }
+    peak, peak_kind = hbm_peak()
+    achieved = alg[dom] / (split[dom] / 1e3) / 1e9
+    # CPU baseline on rank 0 (bounded sample)
+    nk = sample_kernels(W, args.cpu_seconds, threads, R["flats"])
+    cp, cs = cpu_sample(args, W, R["flats"], nk, threads)
+    line = {
+        "metric": metric, "value": value, "unit": "points/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": R["total_ms"] / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload_name(args), "kernels_per_gpu": W["n_k"],
+                   "configs": len(W["configs"]), "archs": W["archs"],
+                   "points_per_gpu": n_pts, "tokens_per_gpu": W["corpus"].n_tok,
+                   "ensemble": f"{args.trees} trees depth {args.depth} "
+                               f"({flat.nodes.shape[0] // max(flat.n_trees, 1)} nodes/tree, "
+                               "declared random)",
+                   "l2": "256 MB flush between timed steps (untimed); ensemble > L2",
+                   "infeasible_points": R["infeasible"], "parallelism": f"dp{world} (kernel shards)"},
+        "e2e": {"value": e2e_value, "unit": "points/s", "h2d_bytes_per_step": R["e2e"]["h2d"],
+                "d2h_bytes_per_step": R["e2e"]["d2h"]},
+        "gpu_launches": 3 * args.steps,
+        "kernel_ms": split,
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                     "algorithmic_bytes": alg[dom], "traffic": None},
+        "cpu_baseline": {"value": cp / cs, "unit": "points/s", "cores": threads, "kind": "port",
+                         "sample": f"first {nk} kernels of the workload ({cp} points), oracle "
+                                   f"schedule+features+ensemble+energy"},
+        "clocks": R["clk"],
+        "setup_s": round(W["build_s"], 2),
+    }
+    print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def workload_name(args) -> str:
+    if args.workload == "c2":
+        return ("BASELINE configs[1]: 10k kernels x 64 launch configs, tesla_k20, full energy "
+                "pipeline (K1+K2/K3+K4+K6)")
+    return "BASELINE configs[4] per-GPU slice: kernels x 256 configs x 3 archs"
+
+
+if __name__ == "__main__":
+    main()

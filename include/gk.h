@@ -1,0 +1,216 @@
+/*
+ * gk.h -- C-ABI of libgk (sm_100a) for the batched energy-prediction hot path of
+ * arXiv 2305.01886 (reference package `gpukalc` / `gpukalc-trainer`).
+ *
+ * The reference has no FFI: its boundary is the Python API.  Each entry point
+ * below replaces the per-point Python call named in its comment; the Python
+ * host package (paper_2305_01886_b200) binds these through ctypes and keeps the
+ * reference's names, argument meaning and exceptions.
+ *
+ * Conventions
+ *   - all pointers are DEVICE pointers unless the name ends in `_host`; the
+ *     caller owns every buffer, the library only borrows them;
+ *   - `stream` is a cudaStream_t passed as void*; calls are asynchronous and
+ *     never synchronise unless documented;
+ *   - return 0 on success, <0 on argument / CUDA error; gk_last_error() gives
+ *     the message (thread-local);
+ *   - per-point failures do not abort a batch: they are written to a status
+ *     byte (GK_OK, GK_INFEASIBLE_LAUNCH, GK_INFEASIBLE_OCCUPANCY).
+ */
+#ifndef GK_H
+#define GK_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GK_ABI_VERSION 1
+
+/* resource / class codes (reference ptx/types.py:12-24) */
+enum { GK_SP = 0, GK_SFU = 1, GK_DPU = 2, GK_LSU = 3, GK_WS = 4, GK_NRES = 5 };
+enum { GK_COMPUTE = 0, GK_GLOBAL = 1, GK_SHARED = 2, GK_MISC = 3, GK_NCLASS = 4 };
+/* token flag bits (in gk_token.cls above the 2 class bits) */
+#define GK_F_BRANCH 0x04u /* is_branch (classify.py:102-104)            */
+#define GK_F_GLOAD  0x08u /* GLOBAL and root in {ld, ldu} (features.py:168-170) */
+#define GK_F_GSTORE 0x10u /* GLOBAL and root == st       (features.py:171-172) */
+
+/* per-point status */
+enum { GK_OK = 0, GK_INFEASIBLE_LAUNCH = 1, GK_INFEASIBLE_OCCUPANCY = 2 };
+
+#define GK_MAX_BP 8   /* piecewise global-latency breakpoints per arch */
+#define GK_NFEAT 32   /* FEATURE_ORDER length (features.py:21-54)      */
+
+/* One PTX instruction, program order (8 B).  The DFG predecessors of token i
+ * are preds[tok[i].pred0 .. tok[i+1].pred0) (block-local producer indices);
+ * the token array carries one sentinel entry at the end. */
+typedef struct {
+    uint8_t  res;    /* GK_SP..GK_WS                                  */
+    uint8_t  cls;    /* class code (bits 0-1) | GK_F_* flags           */
+    uint16_t sig;    /* latency signature id -> gk_arch-major lat table */
+    uint32_t pred0;  /* offset into preds[]                            */
+} gk_token;
+
+/* One basic block (40 B). */
+typedef struct {
+    int64_t  mult;          /* loop multiplier (types.py:109-124)                */
+    uint32_t tok0;          /* first token (global index)                        */
+    uint32_t n;             /* instructions                                      */
+    uint32_t fpred0;        /* forward CFG predecessors: fpreds[fpred0 .. +n_fpred] */
+    uint16_t n_fpred;
+    uint16_t n_glob;        /* GLOBAL-class instructions in the block            */
+    uint16_t res_cnt[GK_NRES]; /* instructions per resource                      */
+    uint8_t  is_exit;       /* no forward out-edge (types.py:79-82)              */
+    uint8_t  pad_;
+} gk_block;
+
+/* One kernel (32 B).  Blocks are contiguous in the block table and their tokens
+ * contiguous in the token table. */
+typedef struct {
+    uint32_t blk0, n_blk;   /* block range                                        */
+    uint32_t topo0;         /* topo[topo0 .. +n_blk]: Kahn order (types.py:87-107) */
+    uint32_t max_n;         /* largest block (instructions)                       */
+    uint32_t tok0, n_tok;   /* token range                                        */
+    uint32_t pad_[2];
+} gk_kernel;
+
+/* A packed corpus: every array lives on the device (or host for the oracle). */
+typedef struct {
+    const gk_token  *tok;    /* n_tok + 1 (sentinel)     */
+    const uint16_t  *preds;  /* DFG producer lists       */
+    const gk_block  *blk;    /* n_blk                    */
+    const uint32_t  *fpreds; /* forward CFG preds (kernel-local block ids) */
+    const uint32_t  *topo;   /* kernel-local block ids   */
+    const gk_kernel *ker;    /* n_ker                    */
+    uint32_t n_tok, n_blk, n_ker, n_sig;
+    uint32_t max_n;          /* largest block over all kernels (instructions) */
+    uint32_t max_blk;        /* most blocks in one kernel                     */
+} gk_corpus;
+
+/* Launch configuration (scheduler.py:31-50). */
+typedef struct { int32_t n_blocks, tpb, regs, shmem; } gk_config;
+
+/* Architecture record (profiles.py:104-135), one per arch. */
+typedef struct {
+    int64_t units[GK_NRES];
+    double  gap[GK_NRES];
+    double  pipeline;
+    int64_t nSM, L2_sz, nTh_sm_max, reg_b_max, shm_b_max, nB_max, wSM_max, Sz_w;
+    int64_t access_sz, access_gm_sz, access_shm_sz, nWS, nDU;
+    double  nu_gpu;
+    double  tpg_a, tpg_b, tpg_c, tps_a, tps_b, tps_c, tp_floor;
+    double  ov_slope, ov_icpt;
+    int32_t n_bp, pad_;
+    double  bp[GK_MAX_BP];
+    double  seg_slope[GK_MAX_BP + 1], seg_icpt[GK_MAX_BP + 1];
+} gk_arch;
+
+/* Static per-kernel tallies (K1; features.py:157-172, scheduler.py:255-266). */
+typedef struct {
+    int64_t cnt[GK_NCLASS];   /* sum of multipliers per class       */
+    int64_t branches, loads, stores, pad_;
+} gk_kstat;
+
+/* Indices into the int64 / f64 per-point schedule outputs (KernelSchedule,
+ * scheduler.py:105-134). */
+enum { GK_SI_THREADS_SCHED = 0, GK_SI_THREADS_PER_SM, GK_SI_BLOCKS_PER_SM, GK_SI_WAVES,
+       GK_SI_N_GLOBAL, GK_SI_N_SHARED, GK_NSI };
+enum { GK_SF_GM_LATENCY = 0, GK_SF_D_KERNEL, GK_SF_OVERHEAD, GK_SF_GM_PENALTY,
+       GK_SF_SM_PENALTY, GK_SF_CM_PENALTY, GK_SF_D_TOTAL, GK_SF_TIME_US, GK_SF_CFG_DELAY,
+       GK_NSF };
+
+/* Optional per-instruction schedule (the --trace rows, scheduler.py:74-102).
+ * Only valid for grids over ONE kernel; arrays are [n_points][n_tok_kernel]
+ * and [n_points][n_blk_kernel]. */
+typedef struct {
+    double  *start, *duration, *latency;
+    int64_t *n_batches;
+    double  *blk_delay, *blk_finish;
+} gk_trace;
+
+/* Point grid: kernels x archs x configs, point p = (ki*n_arch + ai)*n_cfg + ci. */
+typedef struct {
+    const uint32_t  *kernel_ids;  /* n_k indices into the corpus            */
+    const gk_config *cfg;         /* n_cfg                                  */
+    const gk_arch   *arch;        /* n_arch records                         */
+    const double    *lat;         /* [n_arch][n_sig] signature latencies     */
+    /* optional per-config overrides (NULL = none) for the block/CFG-level faces
+     * schedule_block / schedule_cfg (scheduler.py:137, 188), which take n_tw
+     * and gm_latency directly: n_tw_override[c] > 0 replaces cap*tpb,
+     * a non-NaN gm_override[c] replaces the piecewise global latency. */
+    const int64_t   *n_tw_override;
+    const double    *gm_override;
+    uint32_t n_k, n_cfg, n_arch, pad_;
+} gk_grid;
+
+/* Flattened tree ensemble (power.py:22-33).  Node = 16 B: for a split,
+ * {threshold, feature, left} with right = left + 1; for a leaf, {value, -1, 0}.
+ * Child indices are tree-local; trees are contiguous from tree_off[t]. */
+typedef struct { double v; int32_t feature; int32_t left; } gk_node;
+
+typedef struct {
+    const gk_node *nodes;
+    const int64_t *tree_off;    /* n_trees                        */
+    const double  *scale_lo;    /* n_feat  (power.py:128-145)     */
+    const double  *scale_hi;
+    double   base_score;
+    uint32_t n_trees, n_feat, max_depth;
+} gk_ensemble;
+
+/* ------------------------------------------------------------------------ */
+
+int         gk_abi_version(void);
+const char *gk_last_error(void);
+int         gk_device_sm_count(void);
+
+/* K1 -- static segmented counts per kernel and per (arch, kernel) sequential
+ * latency sums of the non-global classes.  Replaces the config-independent
+ * half of extract_features (features.py:155-172) and static_mem_counts
+ * (scheduler.py:255-266).  out_latsum is [n_arch][n_k][3] (Compute, Shared,
+ * Misc), out_kstat is [n_k]. */
+int gk_static_features(const gk_corpus *corpus, const gk_grid *grid,
+                       gk_kstat *out_kstat, double *out_latsum, void *stream);
+
+/* K2+K3 -- per-point schedule and features.  Replaces schedule_kernel
+ * (scheduler.py:325-363) and extract_features (features.py:149-247) per
+ * point.  Any output pointer may be NULL.
+ *   out_status  [n_points] u8
+ *   out_si      [n_points][GK_NSI] int64, out_sf [n_points][GK_NSF] f64
+ *   out_feat    [n_points][GK_NFEAT] f64 in FEATURE_ORDER
+ *   out_sel     [n_points][n_sel] f64: the features listed in sel_idx (manifest
+ *               order for a power model), raw (unscaled)
+ *   trace       per-instruction rows (single-kernel grids only), may be NULL
+ * kstat/latsum come from gk_static_features on the same grid. */
+int gk_schedule_features(const gk_corpus *corpus, const gk_grid *grid,
+                         const gk_kstat *kstat, const double *latsum,
+                         uint8_t *out_status, int64_t *out_si, double *out_sf,
+                         double *out_feat, const int32_t *sel_idx, uint32_t n_sel,
+                         double *out_sel, const gk_trace *trace, void *stream);
+
+/* K4 (+K6) -- ensemble inference over raw feature rows X[n_rows][ld] (first
+ * n_feat columns, manifest order), scaled per power.py:128-145, trees summed in
+ * file order onto base_score (power.py:148-168).  If time_us != NULL also
+ * writes energy = power * time_us (power.py:171-181, fp64 product).
+ * Rows whose status byte (optional) is nonzero get NaN. */
+int gk_rf_predict(const gk_ensemble *ens, const double *X, int64_t ld, int64_t n_rows,
+                  const uint8_t *status, const double *time_us,
+                  double *out_power, double *out_energy, void *stream);
+
+/* Fused sweep: K1 -> K2/K3 -> K4 -> K6 for a whole grid with one ensemble per
+ * arch (ens_host[n_arch], a HOST array of descriptors whose pointers are device
+ * pointers; all ensembles share the manifest sel_idx[n_sel], a device array).
+ * Writes status / time_us / power_w / energy_uj per point.  `work` must hold
+ * gk_sweep_workspace_bytes() bytes of device memory. */
+size_t gk_sweep_workspace_bytes(const gk_grid *grid, uint32_t n_sel);
+int gk_predict_energy_sweep(const gk_corpus *corpus, const gk_grid *grid,
+                            const gk_ensemble *ens_host, const int32_t *sel_idx,
+                            uint32_t n_sel, void *work, uint8_t *out_status,
+                            double *out_time_us, double *out_power, double *out_energy,
+                            void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GK_H */

@@ -1,0 +1,386 @@
+"""Drop-in predictor API: the reference's hot-path functions, same names,
+argument meaning, return types and exceptions, computed by libgk on the GPU.
+
+Scalar face (reference ``gpukalc/__init__.py:16-71``):
+    schedule_kernel(profile, graph, launch) -> KernelSchedule   (scheduler.py:325)
+    extract_features(profile, graph, launch) -> FeatureVector   (features.py:149)
+    predict_power(ensemble, features) -> float                  (power.py:148)
+    predict_energy(power_w, time_us) -> float                   (power.py:171)
+Batched face (new; what the per-launch loops of cli.py:184-197/251-254 become):
+    schedule_batch / extract_features_batch / predict_power_batch / predict_launches
+
+Scalar calls pack + upload the graph once (cached per graph object) and run
+the same kernels as the batched sweep with a one-point grid.  The scalar
+``predict_energy`` keeps the reference's decimal product (its exactness is
+part of the contract pinned by pkg/tests/test_power.py:215-217); batched
+energy is the fp64 product on the device (<= 1 ulp apart).
+"""
+
+from __future__ import annotations
+
+from collections.abc import Mapping
+from dataclasses import dataclass, fields
+from decimal import Decimal
+
+import numpy as np
+
+from . import abi
+from .ensemble import TreeEnsemble, flatten, load_ensemble
+from .errors import EnsembleError, ScheduleError
+from .ir import InstClass, Resource
+from .pack import FEATURE_ORDER, SELECTED_FEATURES, CorpusBuilder, pack_corpus
+from .profiles import ArchProfile, us_from_cycles
+
+# ------------------------------------------------------------------ types
+
+
+@dataclass(frozen=True)
+class LaunchConfig:
+    """Reference ``scheduler.py:31-50``."""
+
+    n_blocks: int
+    threads_per_block: int
+    reg_per_thread: int = 0
+    shmem_per_block: int = 0
+
+    def __post_init__(self):
+        if self.n_blocks < 1:
+            raise ScheduleError("n_blocks must be >= 1")
+        if self.threads_per_block < 1:
+            raise ScheduleError("threads_per_block must be >= 1")
+        if self.reg_per_thread < 0 or self.shmem_per_block < 0:
+            raise ScheduleError("resource footprints must be >= 0")
+
+    @property
+    def total_threads(self) -> int:
+        return self.n_blocks * self.threads_per_block
+
+
+@dataclass(frozen=True)
+class InstSchedule:
+    index: int
+    opcode: str
+    klass: InstClass
+    resource: Resource
+    start: float
+    duration: float
+    latency: float
+    n_batches: int
+
+    @property
+    def finish(self) -> float:
+        return self.start + self.duration
+
+
+@dataclass(frozen=True)
+class BlockSchedule:
+    label: str
+    rows: tuple
+    delay: float
+
+
+@dataclass(frozen=True)
+class CfgSchedule:
+    blocks: tuple
+    multipliers: tuple
+    finish: tuple
+    delay: float
+
+
+@dataclass(frozen=True)
+class KernelSchedule:
+    """Reference ``scheduler.py:105-134``."""
+
+    kernel: str
+    launch: LaunchConfig
+    threads_scheduled: int
+    threads_per_sm: int
+    blocks_per_sm: int
+    waves: int
+    gm_latency: float
+    cfg: CfgSchedule
+    d_kernel: float
+    overhead_cycles: float
+    gm_penalty: float
+    sm_penalty: float
+    cm_penalty: float
+    n_global: int
+    n_shared: int
+    _d_total: float = 0.0
+    _time_us: float = 0.0
+    _nu_gpu: float = 0.0
+
+    @property
+    def d_total(self) -> float:
+        return self._d_total
+
+    def time_us(self, profile: ArchProfile) -> float:
+        # the device already divided by the scheduling profile's clock
+        if profile is None or profile.nu_gpu == self._nu_gpu:
+            return self._time_us
+        return us_from_cycles(profile, self._d_total)
+
+
+@dataclass(frozen=True)
+class FeatureVector:
+    """32 features in FEATURE_ORDER (reference ``features.py:78-120``)."""
+
+    avg_comp_lat: float
+    avg_glob_lat: float
+    avg_misc_lat: float
+    avg_shar_lat: float
+    branch: float
+    comp_inst_kernel: float
+    comp_inst_sm: float
+    comp_lat_sm: float
+    glob_inst_kernel: float
+    glob_inst_sm: float
+    glob_lat_sm: float
+    glob_load_sm: float
+    glob_store_sm: float
+    misc_inst_kernel: float
+    misc_inst_sm: float
+    misc_lat_sm: float
+    shar_inst_kernel: float
+    shar_inst_sm: float
+    shar_lat_sm: float
+    sm_active: float
+    n_warps: float
+    waves: float
+    total_threads: float
+    inst_issue_cycles: float
+    cache_penalty: float
+    glb_penalty: float
+    sh_penalty: float
+    occupancy: float
+    reg_thread: float
+    shmem_block: float
+    block_size: float
+    grid_size: float
+
+    def as_dict(self) -> dict:
+        return {n: getattr(self, n) for n in FEATURE_ORDER}
+
+    def as_row(self) -> tuple:
+        return tuple(getattr(self, n) for n in FEATURE_ORDER)
+
+
+assert tuple(f.name for f in fields(FeatureVector)) == FEATURE_ORDER
+
+# --------------------------------------------------------------- caches
+
+_CORPUS: dict = {}
+_ARCH: dict = {}
+_ENS: dict = {}
+
+
+def _launch_tuple(launch) -> tuple:
+    if isinstance(launch, LaunchConfig) or hasattr(launch, "threads_per_block"):
+        return (launch.n_blocks, launch.threads_per_block, launch.reg_per_thread,
+                launch.shmem_per_block)
+    return tuple(launch)
+
+
+def _device_corpus(graphs):
+    from .runtime import DeviceCorpus
+
+    key = tuple(id(g) for g in graphs)
+    hit = _CORPUS.get(key)
+    if hit is None:
+        if len(_CORPUS) > 64:
+            _CORPUS.clear()
+        hit = _CORPUS[key] = (list(graphs), DeviceCorpus.upload(pack_corpus(graphs)))
+    return hit[1]
+
+
+def _infeasible_message(launch) -> str:
+    nb, tpb, regs, shm = _launch_tuple(launch)
+    return (f"block of {tpb} threads, {regs} regs/thread, {shm} B shared does not fit on one SM")
+
+
+# ------------------------------------------------------------- batched
+
+
+def schedule_batch(profiles, graphs, launches, *, features: bool = True, sel_idx=None,
+                   trace: bool = False, to_host: bool = True) -> dict:
+    """All (graph, profile, launch) points of a grid on the device.
+
+    Point p = (graph_i * n_profiles + profile_j) * n_launches + launch_k.
+    Returns numpy arrays (or device tensors with to_host=False): status u8,
+    si [n,6] int64 (abi.SI_NAMES), sf [n,9] f64 (abi.SF_NAMES), feat [n,32] f64.
+    """
+    from .runtime import DeviceGrid, schedule_features
+
+    if isinstance(profiles, ArchProfile) or not isinstance(profiles, (list, tuple)):
+        profiles = [profiles]
+    graphs = list(graphs)
+    dc = _device_corpus(graphs)
+    dg = DeviceGrid.build(dc, profiles, [_launch_tuple(L) for L in launches])
+    out = schedule_features(dc, dg, feat=features, sel_idx=sel_idx, trace=trace)
+    if not to_host:
+        return out
+    return {k: (v.cpu().numpy() if hasattr(v, "cpu") else v) for k, v in out.items()}
+
+
+def extract_features_batch(profiles, graphs, launches, *, selected=None) -> np.ndarray:
+    """[n_points, 32] (or [n, len(selected)]) features; infeasible rows are NaN."""
+    out = schedule_batch(profiles, graphs, launches, features=True)
+    feat = out["feat"]
+    if selected is not None:
+        feat = feat[:, [FEATURE_ORDER.index(n) for n in selected]]
+    return feat
+
+
+# --------------------------------------------------------------- scalar
+
+
+def schedule_kernel(profile: ArchProfile, graph, launch: LaunchConfig) -> KernelSchedule:
+    """Reference ``scheduler.py:325-363`` (per-instruction rows included)."""
+    out = schedule_batch([profile], [graph], [launch], features=False, trace=True)
+    if out["status"][0] == abi.STATUS_INFEASIBLE_LAUNCH:
+        raise ScheduleError(_infeasible_message(launch))
+    si, sf = out["si"][0], out["sf"][0]
+    blocks = []
+    t = 0
+    mult = graph.loop_multipliers()
+    for b, blk in enumerate(graph.blocks):
+        rows = []
+        for i, ins in enumerate(blk.instructions):
+            rows.append(InstSchedule(index=i, opcode=ins.opcode, klass=ins.klass,
+                                     resource=ins.resource, start=float(out["tr_start"][0, t]),
+                                     duration=float(out["tr_duration"][0, t]),
+                                     latency=float(out["tr_latency"][0, t]),
+                                     n_batches=int(out["tr_n_batches"][0, t])))
+            t += 1
+        blocks.append(BlockSchedule(label=blk.label, rows=tuple(rows),
+                                    delay=float(out["tr_blk_delay"][0, b])))
+    cfg = CfgSchedule(blocks=tuple(blocks), multipliers=tuple(mult),
+                      finish=tuple(float(v) for v in out["tr_blk_finish"][0]),
+                      delay=float(sf[abi.SF_NAMES.index("cfg_delay")]))
+    L = launch if isinstance(launch, LaunchConfig) else LaunchConfig(*_launch_tuple(launch))
+    return KernelSchedule(
+        kernel=graph.name, launch=L, threads_scheduled=int(si[0]), threads_per_sm=int(si[1]),
+        blocks_per_sm=int(si[2]), waves=int(si[3]), gm_latency=float(sf[0]), cfg=cfg,
+        d_kernel=float(sf[1]), overhead_cycles=float(sf[2]), gm_penalty=float(sf[3]),
+        sm_penalty=float(sf[4]), cm_penalty=float(sf[5]), n_global=int(si[4]),
+        n_shared=int(si[5]), _d_total=float(sf[6]), _time_us=float(sf[7]),
+        _nu_gpu=profile.nu_gpu)
+
+
+def extract_features(profile: ArchProfile, graph, launch: LaunchConfig) -> FeatureVector:
+    """Reference ``features.py:149-247``."""
+    out = schedule_batch([profile], [graph], [launch], features=True)
+    st = out["status"][0]
+    if st == abi.STATUS_INFEASIBLE_LAUNCH:
+        raise ScheduleError(_infeasible_message(launch))
+    if st == abi.STATUS_INFEASIBLE_OCCUPANCY:
+        raise ScheduleError(f"block of {_launch_tuple(launch)[1]} threads does not fit on one SM")
+    return FeatureVector(*[float(v) for v in out["feat"][0]])
+
+
+def _rows_for(ensemble: TreeEnsemble, features) -> list:
+    if isinstance(features, Mapping):
+        missing = [n for n in ensemble.feature_manifest if n not in features]
+        if missing:
+            raise EnsembleError(f"features missing from input: {', '.join(missing)}")
+        return [float(features[n]) for n in ensemble.feature_manifest]
+    raw = [float(v) for v in features]
+    if len(raw) != ensemble.n_features:
+        raise EnsembleError(f"expected {ensemble.n_features} feature values, got {len(raw)}")
+    return raw
+
+
+def _device_ensemble(ensemble: TreeEnsemble):
+    from .runtime import DeviceEnsemble
+
+    key = id(ensemble)
+    hit = _ENS.get(key)
+    if hit is None or hit[0] is not ensemble:
+        if len(_ENS) > 16:
+            _ENS.clear()
+        hit = _ENS[key] = (ensemble, DeviceEnsemble.upload(flatten(ensemble)))
+    return hit[1]
+
+
+def predict_power_batch(ensemble: TreeEnsemble, X, *, time_us=None, status=None):
+    """Rows X [n, n_features] (manifest order, raw) -> power [n] (and energy)."""
+    import torch
+
+    from .runtime import device, rf_predict
+
+    de = _device_ensemble(ensemble)
+    Xt = torch.as_tensor(np.ascontiguousarray(X, dtype=np.float64)).to(device())
+    if Xt.dim() != 2 or Xt.shape[1] != ensemble.n_features:
+        raise EnsembleError(f"expected {ensemble.n_features} feature values per row")
+    tu = None if time_us is None else torch.as_tensor(np.asarray(time_us, np.float64)).to(device())
+    st = None if status is None else torch.as_tensor(np.asarray(status, np.uint8)).to(device())
+    p, e = rf_predict(de, Xt, status=st, time_us=tu)
+    return (p.cpu().numpy(), None if e is None else e.cpu().numpy())
+
+
+def predict_power(ensemble: TreeEnsemble, features) -> float:
+    """Reference ``power.py:148-168``; x <= threshold goes left."""
+    row = _rows_for(ensemble, features)
+    p, _ = predict_power_batch(ensemble, [row])
+    return float(p[0])
+
+
+def predict_energy(power_w: float, time_us: float) -> float:
+    """Reference ``power.py:171-181``: decimal product of the printed values."""
+    if power_w < 0:
+        raise EnsembleError("power must be >= 0")
+    if time_us < 0:
+        raise EnsembleError("time must be >= 0")
+    return float(Decimal(repr(float(power_w))) * Decimal(repr(float(time_us))))
+
+
+@dataclass(frozen=True)
+class EnergyReport:
+    kernel: str
+    time_us: float
+    power_w: float
+    energy_uj: float
+
+    @classmethod
+    def build(cls, kernel: str, time_us: float, power_w: float) -> "EnergyReport":
+        return cls(kernel=kernel, time_us=time_us, power_w=power_w,
+                   energy_uj=predict_energy(power_w, time_us))
+
+
+def predict_launches(profile: ArchProfile, graph, launches, ensemble: TreeEnsemble | None = None):
+    """The reference CLI's per-launch predict loop (cli.py:184-197) as one
+    device batch: list of result dicts with the CLI's keys."""
+    out = schedule_batch([profile], [graph], launches, features=ensemble is not None)
+    rows = []
+    power = energy = None
+    if ensemble is not None:
+        idx = [FEATURE_ORDER.index(n) for n in ensemble.feature_manifest]
+        ok = out["status"] == 0
+        X = np.where(ok[:, None], out["feat"][:, idx], 0.0)
+        power, energy = predict_power_batch(ensemble, X, time_us=out["sf"][:, 7],
+                                            status=(~ok).astype(np.uint8))
+    for k, L in enumerate(launches):
+        st = out["status"][k]
+        if st == abi.STATUS_INFEASIBLE_LAUNCH:
+            raise ScheduleError(_infeasible_message(L))
+        si, sf = out["si"][k], out["sf"][k]
+        nb, tpb = _launch_tuple(L)[:2]
+        row = {"kernel": graph.name, "n_blocks": nb, "threads_per_block": tpb,
+               "waves": int(si[3]), "threads_per_sm": int(si[1]), "blocks_per_sm": int(si[2]),
+               "gm_latency_cycles": float(sf[0]), "d_kernel_cycles": float(sf[1]),
+               "overhead_cycles": float(sf[2]), "gm_penalty_cycles": float(sf[3]),
+               "sm_penalty_cycles": float(sf[4]), "cm_penalty_cycles": float(sf[5]),
+               "d_total_cycles": float(sf[6]), "time_us": float(sf[7])}
+        if ensemble is not None:
+            if st == abi.STATUS_INFEASIBLE_OCCUPANCY:
+                raise ScheduleError(f"block of {tpb} threads does not fit on one SM")
+            row["power_w"] = float(power[k])
+            row["energy_uj"] = predict_energy(row["power_w"], row["time_us"])
+        rows.append(row)
+    return rows
+
+
+__all__ = ["LaunchConfig", "KernelSchedule", "FeatureVector", "EnergyReport", "schedule_kernel",
+           "extract_features", "predict_power", "predict_energy", "schedule_batch",
+           "extract_features_batch", "predict_power_batch", "predict_launches", "load_ensemble",
+           "FEATURE_ORDER", "SELECTED_FEATURES", "CorpusBuilder"]

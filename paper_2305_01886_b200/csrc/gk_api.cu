@@ -1,0 +1,177 @@
+// gk_api.cu -- the C-ABI of libgk (declared in include/gk.h).
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "gk_internal.cuh"
+
+static thread_local char g_err[512] = "";
+
+void gk_set_error(const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof g_err, fmt, ap);
+    va_end(ap);
+}
+
+int gk_check_launch(const char *what) {
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        gk_set_error("%s: %s", what, cudaGetErrorString(e));
+        return -2;
+    }
+    return 0;
+}
+
+// defined in gk_sched.cu / gk_rf.cu
+int gk_launch_static(const gk_corpus *, const gk_grid *, gk_kstat *, double *, cudaStream_t);
+size_t gk_sched_scratch_bytes(const gk_grid *, uint32_t, uint32_t);
+int gk_launch_sched(const gk_corpus *, const gk_grid *, const gk_kstat *, const double *, uint8_t *,
+                    int64_t *, double *, double *, const int32_t *, uint32_t, double *, double *,
+                    const gk_trace *, uint32_t, uint32_t, double *, cudaStream_t);
+int gk_launch_rf(const gk_ensemble *, uint32_t, const double *, int64_t, int64_t, const uint8_t *,
+                 const double *, double *, double *, uint32_t, uint32_t, cudaStream_t);
+
+namespace {
+
+struct Scratch {
+    void *p = nullptr;
+    size_t n = 0;
+    ~Scratch() {
+        if (p) cudaFree(p);
+    }
+};
+thread_local Scratch g_scratch;
+
+int scratch(size_t bytes, void **out) {
+    if (g_scratch.n < bytes) {
+        if (g_scratch.p) cudaFree(g_scratch.p);
+        g_scratch.p = nullptr;
+        g_scratch.n = 0;
+        const cudaError_t e = cudaMalloc(&g_scratch.p, bytes);
+        if (e != cudaSuccess) {
+            gk_set_error("scratch allocation of %zu B: %s", bytes, cudaGetErrorString(e));
+            return -2;
+        }
+        g_scratch.n = bytes;
+    }
+    *out = g_scratch.p;
+    return 0;
+}
+
+int check_grid(const gk_corpus *C, const gk_grid *G) {
+    if (!C || !G) {
+        gk_set_error("null corpus or grid");
+        return -1;
+    }
+    if (G->n_arch == 0 || G->n_cfg == 0) {
+        gk_set_error("grid needs at least one arch and one config");
+        return -1;
+    }
+    return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int gk_abi_version(void) { return GK_ABI_VERSION; }
+
+const char *gk_last_error(void) { return g_err; }
+
+int gk_device_sm_count(void) {
+    int dev = 0, n = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
+    return n;
+}
+
+int gk_static_features(const gk_corpus *corpus, const gk_grid *grid, gk_kstat *out_kstat,
+                       double *out_latsum, void *stream) {
+    if (int rc = check_grid(corpus, grid)) return rc;
+    return gk_launch_static(corpus, grid, out_kstat, out_latsum, (cudaStream_t)stream);
+}
+
+int gk_schedule_features(const gk_corpus *corpus, const gk_grid *grid, const gk_kstat *kstat,
+                         const double *latsum, uint8_t *out_status, int64_t *out_si,
+                         double *out_sf, double *out_feat, const int32_t *sel_idx, uint32_t n_sel,
+                         double *out_sel, const gk_trace *trace, void *stream) {
+    if (int rc = check_grid(corpus, grid)) return rc;
+    if (trace && trace->start && grid->n_k != 1) {
+        gk_set_error("per-instruction trace needs a single-kernel grid");
+        return -1;
+    }
+    if (out_sel && (!sel_idx || n_sel == 0)) {
+        gk_set_error("out_sel given without sel_idx");
+        return -1;
+    }
+    const cudaStream_t st = (cudaStream_t)stream;
+    const uint32_t max_n = corpus->max_n ? corpus->max_n : 1;
+    const uint32_t max_blk = corpus->max_blk ? corpus->max_blk : 1;
+    void *ws = nullptr;
+    if (int rc = scratch(gk_sched_scratch_bytes(grid, max_n, max_blk), &ws)) return rc;
+    return gk_launch_sched(corpus, grid, kstat, latsum, out_status, out_si, out_sf, out_feat,
+                           sel_idx, n_sel, out_sel, nullptr, trace, max_n, max_blk, (double *)ws,
+                           st);
+}
+
+int gk_rf_predict(const gk_ensemble *ens, const double *X, int64_t ld, int64_t n_rows,
+                  const uint8_t *status, const double *time_us, double *out_power,
+                  double *out_energy, void *stream) {
+    if (!ens || !X || !out_power) {
+        gk_set_error("gk_rf_predict: null argument");
+        return -1;
+    }
+    if (out_energy && !time_us) {
+        gk_set_error("gk_rf_predict: energy requested without time_us");
+        return -1;
+    }
+    return gk_launch_rf(ens, 1, X, ld, n_rows, status, time_us, out_power, out_energy, 0, 1,
+                        (cudaStream_t)stream);
+}
+
+size_t gk_sweep_workspace_bytes(const gk_grid *grid, uint32_t n_sel) {
+    const size_t n_points = (size_t)grid->n_k * grid->n_arch * grid->n_cfg;
+    size_t b = 0;
+    b += ((sizeof(gk_kstat) * grid->n_k + 255) / 256) * 256;
+    b += ((sizeof(double) * 3 * grid->n_k * grid->n_arch + 255) / 256) * 256;
+    b += ((sizeof(double) * n_points * n_sel + 255) / 256) * 256;
+    return b;
+}
+
+int gk_predict_energy_sweep(const gk_corpus *corpus, const gk_grid *grid,
+                            const gk_ensemble *ens_host, const int32_t *sel_idx, uint32_t n_sel,
+                            void *work, uint8_t *out_status, double *out_time_us,
+                            double *out_power, double *out_energy, void *stream) {
+    if (int rc = check_grid(corpus, grid)) return rc;
+    if (!ens_host || !sel_idx || !n_sel || !work || !out_status || !out_time_us || !out_power ||
+        !out_energy) {
+        gk_set_error("gk_predict_energy_sweep: null argument");
+        return -1;
+    }
+    if (grid->n_arch > 4) {
+        gk_set_error("gk_predict_energy_sweep: at most 4 archs per sweep");
+        return -1;
+    }
+    const cudaStream_t st = (cudaStream_t)stream;
+    char *w = (char *)work;
+    gk_kstat *ks = (gk_kstat *)w;
+    w += ((sizeof(gk_kstat) * grid->n_k + 255) / 256) * 256;
+    double *latsum = (double *)w;
+    w += ((sizeof(double) * 3 * grid->n_k * grid->n_arch + 255) / 256) * 256;
+    double *sel = (double *)w;
+    const size_t n_points = (size_t)grid->n_k * grid->n_arch * grid->n_cfg;
+    if (int rc = gk_launch_static(corpus, grid, ks, latsum, st)) return rc;
+    const uint32_t max_n = corpus->max_n ? corpus->max_n : 1;
+    const uint32_t max_blk = corpus->max_blk ? corpus->max_blk : 1;
+    void *ws = nullptr;
+    if (int rc = scratch(gk_sched_scratch_bytes(grid, max_n, max_blk), &ws)) return rc;
+    if (int rc = gk_launch_sched(corpus, grid, ks, latsum, out_status, nullptr, nullptr, nullptr,
+                                 sel_idx, n_sel, sel, out_time_us, nullptr, max_n, max_blk,
+                                 (double *)ws, st))
+        return rc;
+    return gk_launch_rf(ens_host, grid->n_arch, sel, n_sel, (int64_t)n_points, out_status,
+                        out_time_us, out_power, out_energy, grid->n_cfg, grid->n_arch, st);
+}
+
+}  // extern "C"

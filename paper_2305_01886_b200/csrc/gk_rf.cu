@@ -1,0 +1,188 @@
+// gk_rf.cu -- K4 (+K6): tree-ensemble inference and the energy epilogue.
+//
+// Reference: power.py:128-145 (_scaled_input), :148-168 (predict_power),
+// :171-181 (predict_energy).  Nothing here is a dense contraction, so no
+// tensor cores: the kernel is a gather-bound traversal over 16-byte nodes
+// (BFS layout, right = left + 1, so one 16-byte load per visit).
+//
+// Layout per CTA: a tile of 128 rows is staged into shared memory with a bulk
+// async copy (cp.async.bulk, the TMA 1-D path) when the rows are contiguous,
+// scaled in place (x = (v - lo) / (hi - lo), or 0 when hi <= lo), then every
+// thread walks kIlp trees concurrently for its row.  Leaves are added to the
+// running total strictly in tree order, so the fp64 sum is bit-identical to
+// the reference's sequential `total += leaf`.
+#include "gk_internal.cuh"
+
+namespace gk {
+
+constexpr int kRfThreads = 128;
+constexpr int kIlp = 4;
+constexpr int kMaxFeat = 64;
+
+struct RfArgs {
+    gk_ensemble ens[4];        // up to 4 ensembles selected per row by `arch`
+    uint32_t n_ens;
+    const double *X;
+    int64_t ld, n_rows;
+    const uint8_t *status;
+    const double *time_us;     // optional, indexed like rows
+    double *power, *energy;
+    // row -> arch map for grids: arch = (row / n_cfg) % n_arch (n_cfg = 0: arch 0)
+    uint32_t n_cfg, n_arch;
+};
+
+__device__ __forceinline__ void bulk_g2s(void *smem_dst, const void *gsrc, uint32_t bytes,
+                                         uint64_t *bar) {
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
+    const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(d),
+        "l"(gsrc), "r"(bytes), "r"(b)
+        : "memory");
+}
+
+__global__ void __launch_bounds__(kRfThreads) k4_rf_predict(RfArgs R) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t bar;
+    const int64_t row0 = (int64_t)blockIdx.x * kRfThreads;
+    const int64_t nr = min((int64_t)kRfThreads, R.n_rows - row0);
+    const uint32_t nf = R.ens[0].n_feat;
+    double *xs = reinterpret_cast<double *>(smem_raw);  // [kRfThreads][ld] raw, then scaled
+
+    // ---- stage the row tile (contiguous when ld == n_feat)
+    const bool bulk = (R.ld == (int64_t)nf) && ((nr * nf * 8) % 16 == 0) &&
+                      ((reinterpret_cast<uintptr_t>(R.X + row0 * R.ld) & 15) == 0);
+    if (bulk) {
+        const uint32_t bytes = (uint32_t)(nr * nf * 8);
+        if (threadIdx.x == 0) {
+            const uint32_t b = (uint32_t)__cvta_generic_to_shared(&bar);
+            asm volatile("mbarrier.init.shared.b64 [%0], 1;\n" ::"r"(b));
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+            asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;\n" ::"r"(b), "r"(bytes)
+                         : "memory");
+            bulk_g2s(xs, R.X + row0 * R.ld, bytes, &bar);
+        }
+        __syncthreads();
+        const uint32_t b = (uint32_t)__cvta_generic_to_shared(&bar);
+        asm volatile(
+            "{\n .reg .pred p;\n WAIT_%=:\n"
+            " mbarrier.try_wait.parity.shared.b64 p, [%0], 0;\n"
+            " @!p bra WAIT_%=;\n}\n" ::"r"(b)
+            : "memory");
+    } else {
+        for (int64_t q = threadIdx.x; q < nr * nf; q += kRfThreads) {
+            const int64_t r = q / nf, f = q % nf;
+            xs[r * nf + f] = R.X[(row0 + r) * R.ld + f];
+        }
+        __syncthreads();
+    }
+    const int64_t row = row0 + threadIdx.x;
+    if (threadIdx.x >= nr) return;
+    const uint32_t ai = R.n_cfg ? (uint32_t)((row / R.n_cfg) % R.n_arch) : 0u;
+    const gk_ensemble &E = R.ens[ai < R.n_ens ? ai : 0];
+    const double NaN = __longlong_as_double(0x7ff8000000000000ll);
+    if (R.status && R.status[row]) {
+        R.power[row] = NaN;
+        if (R.energy) R.energy[row] = NaN;
+        return;
+    }
+    double *x = xs + (size_t)threadIdx.x * nf;
+    for (uint32_t f = 0; f < nf; f++) {
+        const double lo = E.scale_lo[f], hi = E.scale_hi[f];
+        x[f] = hi > lo ? __ddiv_rn(__dsub_rn(x[f], lo), __dsub_rn(hi, lo)) : 0.0;
+    }
+    const gk_node *__restrict__ nodes = E.nodes;
+    double total = E.base_score;
+    uint32_t t = 0;
+    for (; t + kIlp <= E.n_trees; t += kIlp) {
+        const gk_node *base[kIlp];
+        int32_t idx[kIlp];
+        double leaf[kIlp];
+        bool done[kIlp];
+#pragma unroll
+        for (int q = 0; q < kIlp; q++) {
+            base[q] = nodes + E.tree_off[t + q];
+            idx[q] = 0;
+            done[q] = false;
+            leaf[q] = 0.0;
+        }
+        bool all = false;
+        while (!all) {
+            all = true;
+#pragma unroll
+            for (int q = 0; q < kIlp; q++) {
+                if (!done[q]) {
+                    const double2 raw = __ldg(reinterpret_cast<const double2 *>(base[q] + idx[q]));
+                    const int2 fl = make_int2(__double2loint(raw.y), __double2hiint(raw.y));
+                    if (fl.x < 0) {
+                        leaf[q] = raw.x;
+                        done[q] = true;
+                    } else {
+                        idx[q] = x[fl.x] <= raw.x ? fl.y : fl.y + 1;
+                        all = false;
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < kIlp; q++) total = __dadd_rn(total, leaf[q]);  // tree order
+    }
+    for (; t < E.n_trees; t++) {
+        const gk_node *b = nodes + E.tree_off[t];
+        int32_t i = 0;
+        while (true) {
+            const double2 raw = __ldg(reinterpret_cast<const double2 *>(b + i));
+            const int f = __double2loint(raw.y), l = __double2hiint(raw.y);
+            if (f < 0) {
+                total = __dadd_rn(total, raw.x);
+                break;
+            }
+            i = x[f] <= raw.x ? l : l + 1;
+        }
+    }
+    R.power[row] = total;
+    if (R.energy) R.energy[row] = __dmul_rn(total, R.time_us[row]);
+}
+
+}  // namespace gk
+
+int gk_launch_rf(const gk_ensemble *ens, uint32_t n_ens, const double *X, int64_t ld,
+                 int64_t n_rows, const uint8_t *status, const double *time_us, double *power,
+                 double *energy, uint32_t n_cfg, uint32_t n_arch, cudaStream_t st) {
+    if (n_rows <= 0) return 0;
+    if (n_ens < 1 || n_ens > 4) {
+        gk_set_error("gk_rf_predict: 1..4 ensembles per launch (got %u)", n_ens);
+        return -1;
+    }
+    gk::RfArgs R;
+    memset(&R, 0, sizeof R);
+    const uint32_t nf = ens[0].n_feat;
+    for (uint32_t a = 0; a < n_ens; a++) {
+        R.ens[a] = ens[a];
+        if (ens[a].n_feat != nf) {
+            gk_set_error("gk_rf_predict: ensembles of one sweep must share the manifest");
+            return -1;
+        }
+    }
+    if (nf < 1 || nf > (uint32_t)gk::kMaxFeat || ld < (int64_t)nf) {
+        gk_set_error("gk_rf_predict: n_feat=%u ld=%lld unsupported", nf, (long long)ld);
+        return -1;
+    }
+    R.n_ens = n_ens;
+    R.X = X;
+    R.ld = ld;
+    R.n_rows = n_rows;
+    R.status = status;
+    R.time_us = time_us;
+    R.power = power;
+    R.energy = energy;
+    R.n_cfg = n_cfg;
+    R.n_arch = n_arch ? n_arch : 1;
+    const size_t smem = (size_t)gk::kRfThreads * nf * sizeof(double);
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(gk::k4_rf_predict, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+    const int64_t blocks = (n_rows + gk::kRfThreads - 1) / gk::kRfThreads;
+    gk::k4_rf_predict<<<(unsigned)blocks, gk::kRfThreads, smem, st>>>(R);
+    return gk_check_launch("k4_rf_predict");
+}

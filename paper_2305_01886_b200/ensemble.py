@@ -1,0 +1,255 @@
+"""Tree-ensemble documents (host side): load + validate, and flatten to the
+16-byte device node layout of ``include/gk.h``.
+
+Loading / validation restates the reference (``pkg/src/gpukalc/power.py:22-125``)
+and keeps its error messages.  Flattening renumbers each tree breadth-first so
+that every split's children are adjacent (``right == left + 1``) and the top
+levels of every tree are contiguous -- the layout the traversal kernel gathers
+from.  Leaves keep the reference's values; traversal order and the x <= thr
+rule are unchanged (``power.py:156-168``).
+"""
+
+from __future__ import annotations
+
+import json
+from collections.abc import Mapping
+from dataclasses import dataclass, field
+from pathlib import Path
+
+import numpy as np
+
+from .errors import EnsembleError
+
+ENSEMBLE_SCHEMA_VERSION = 1
+NODE_DT = np.dtype({"names": ["v", "feature", "left"], "formats": ["<f8", "<i4", "<i4"],
+                    "offsets": [0, 8, 12], "itemsize": 16})
+
+
+@dataclass(frozen=True)
+class TreeEnsemble:
+    """Reference ``power.py:22-33`` (same fields)."""
+
+    base_score: float
+    feature_manifest: tuple
+    scale_min: tuple
+    scale_max: tuple
+    trees: tuple
+    gains: tuple
+    _flat: dict = field(default_factory=dict, compare=False, repr=False)
+
+    @property
+    def n_features(self) -> int:
+        return len(self.feature_manifest)
+
+
+def _check_tree(nodes, n_features: int, t: int) -> None:
+    """Reference ``power.py:36-70``: field checks, then exactly-once reachability."""
+    if not nodes:
+        raise EnsembleError(f"tree {t} has no nodes")
+    n = len(nodes)
+    for i, nd in enumerate(nodes):
+        at = f"tree {t} node {i}"
+        if "value" in nd:
+            if not isinstance(nd["value"], (int, float)):
+                raise EnsembleError(f"{at}: leaf value must be a number")
+            continue
+        for key in ("feature", "threshold", "left", "right"):
+            if key not in nd:
+                raise EnsembleError(f"{at}: missing '{key}'")
+        f = nd["feature"]
+        if not isinstance(f, int) or not 0 <= f < n_features:
+            raise EnsembleError(f"{at}: feature index {f} out of range")
+        for ch in (nd["left"], nd["right"]):
+            if not isinstance(ch, int) or not 0 <= ch < n:
+                raise EnsembleError(f"{at}: child index {ch} out of range")
+    seen = bytearray(n)
+    todo = [0]
+    while todo:
+        i = todo.pop()
+        if seen[i]:
+            raise EnsembleError(f"tree {t}: node {i} reached twice")
+        seen[i] = 1
+        nd = nodes[i]
+        if "value" not in nd:
+            todo.append(nd["left"])
+            todo.append(nd["right"])
+    if not all(seen):
+        raise EnsembleError(f"tree {t}: node {seen.index(0)} unreachable")
+
+
+def load_ensemble(source) -> TreeEnsemble:
+    """JSON path or parsed mapping -> TreeEnsemble (reference ``power.py:73-125``)."""
+    if isinstance(source, Mapping):
+        doc = source
+    else:
+        try:
+            doc = json.loads(Path(source).read_text())
+        except (OSError, json.JSONDecodeError) as exc:
+            raise EnsembleError(f"cannot read ensemble: {exc}") from exc
+    if doc.get("schema_version") != ENSEMBLE_SCHEMA_VERSION:
+        raise EnsembleError(f"unsupported ensemble schema_version {doc.get('schema_version')!r}, "
+                            f"expected {ENSEMBLE_SCHEMA_VERSION}")
+    man = doc.get("feature_manifest")
+    if not isinstance(man, list) or not man:
+        raise EnsembleError("feature_manifest must be a non-empty list")
+    if any(not isinstance(m, str) for m in man):
+        raise EnsembleError("feature_manifest entries must be strings")
+    if len(set(man)) != len(man):
+        raise EnsembleError("feature_manifest has duplicate names")
+    k = len(man)
+    sc = doc.get("scaling")
+    if not isinstance(sc, Mapping) or "min" not in sc or "max" not in sc:
+        raise EnsembleError("scaling must provide 'min' and 'max' arrays")
+    lo, hi = list(sc["min"]), list(sc["max"])
+    if len(lo) != k or len(hi) != k:
+        raise EnsembleError(f"scaling arrays must have {k} entries to match the manifest")
+    for i, (a, b) in enumerate(zip(lo, hi)):
+        if b < a:
+            raise EnsembleError(f"scaling for '{man[i]}' has max < min")
+    trees = doc.get("trees")
+    if not isinstance(trees, list):
+        raise EnsembleError("trees must be a list")
+    for t, tree in enumerate(trees):
+        if not isinstance(tree, Mapping) or "nodes" not in tree:
+            raise EnsembleError(f"tree {t} must be an object with 'nodes'")
+        _check_tree(tree["nodes"], k, t)
+    gains = doc.get("gains", [0.0] * k)
+    if len(gains) != k:
+        raise EnsembleError(f"gains must have {k} entries to match the manifest")
+    if any(g < 0 for g in gains):
+        raise EnsembleError("gains must be >= 0")
+    return TreeEnsemble(base_score=float(doc.get("base_score", 0.0)),
+                        feature_manifest=tuple(man), scale_min=tuple(float(v) for v in lo),
+                        scale_max=tuple(float(v) for v in hi),
+                        trees=tuple(tuple(dict(n) for n in tr["nodes"]) for tr in trees),
+                        gains=tuple(float(g) for g in gains))
+
+
+@dataclass
+class FlatEnsemble:
+    """Device layout of one ensemble (host numpy arrays)."""
+
+    nodes: np.ndarray      # NODE_DT
+    tree_off: np.ndarray   # int64 [n_trees]
+    scale_lo: np.ndarray   # f64 [n_feat]
+    scale_hi: np.ndarray
+    base_score: float
+    max_depth: int
+    manifest: tuple
+
+    @property
+    def n_trees(self) -> int:
+        return len(self.tree_off)
+
+    @property
+    def n_feat(self) -> int:
+        return len(self.scale_lo)
+
+
+def _flatten_tree(nodes) -> tuple[np.ndarray, int]:
+    out = np.zeros(len(nodes), NODE_DT)
+    order = [0]           # old ids in new order (BFS, children adjacent)
+    depth = [0]
+    k = 0
+    max_d = 0
+    while k < len(order):
+        nd = nodes[order[k]]
+        if "value" in nd:
+            out[k] = (float(nd["value"]), -1, 0)
+        else:
+            left = len(order)
+            order.append(nd["left"])
+            order.append(nd["right"])
+            depth += [depth[k] + 1, depth[k] + 1]
+            max_d = max(max_d, depth[k] + 1)
+            out[k] = (float(nd["threshold"]), int(nd["feature"]), left)
+        k += 1
+    return out, max_d
+
+
+def flatten(ens: TreeEnsemble) -> FlatEnsemble:
+    """TreeEnsemble -> FlatEnsemble (cached on the ensemble object)."""
+    cached = ens._flat.get("flat")
+    if cached is not None:
+        return cached
+    parts, offs, off, md = [], [], 0, 0
+    for tree in ens.trees:
+        arr, d = _flatten_tree(tree)
+        parts.append(arr)
+        offs.append(off)
+        off += len(arr)
+        md = max(md, d)
+    nodes = np.concatenate(parts) if parts else np.zeros(1, NODE_DT)
+    flat = FlatEnsemble(nodes=nodes, tree_off=np.asarray(offs, dtype=np.int64),
+                        scale_lo=np.asarray(ens.scale_min, dtype=np.float64),
+                        scale_hi=np.asarray(ens.scale_max, dtype=np.float64),
+                        base_score=float(ens.base_score), max_depth=md,
+                        manifest=tuple(ens.feature_manifest))
+    ens._flat["flat"] = flat
+    return flat
+
+
+def random_forest_flat(n_trees: int, depth: int, manifest, scale_lo, scale_hi, seed: int,
+                       split_p: float = 0.93, leaf_scale: float | None = None) -> FlatEnsemble:
+    """A declared synthetic ensemble for throughput runs (BASELINE config #4/#5):
+    n_trees trees of max depth `depth`, each node below the max depth splitting
+    with probability split_p (0.93 at depth 16 gives ~109k nodes/tree, the size
+    sklearn grows at 1M rows x depth 16 -- SURVEY §7.3.4).  Thresholds are uniform
+    in scaled space; leaves are RF-style (mean value / n_trees)."""
+    rng = np.random.default_rng(seed)
+    nf = len(manifest)
+    scale = (1.0 / n_trees) if leaf_scale is None else leaf_scale
+    parts, offs, off = [], [], 0
+    for _ in range(n_trees):
+        level_n = 1
+        levels = []
+        for d in range(depth + 1):
+            split = rng.random(level_n) < (split_p if d > 0 else 1.0)
+            if d == depth:
+                split[:] = False
+            levels.append(split)
+            level_n = int(split.sum()) * 2
+            if level_n == 0:
+                break
+        n_nodes = sum(len(s) for s in levels)
+        arr = np.zeros(n_nodes, NODE_DT)
+        base = 0
+        for d, split in enumerate(levels):
+            cnt = len(split)
+            nxt = base + cnt
+            idx = np.arange(base, base + cnt)
+            sp = idx[split]
+            arr["feature"][sp] = rng.integers(0, nf, len(sp))
+            arr["v"][sp] = rng.random(len(sp))
+            arr["left"][sp] = nxt + 2 * np.arange(len(sp))
+            lf = idx[~split]
+            arr["feature"][lf] = -1
+            arr["v"][lf] = (30.0 + 120.0 * rng.random(len(lf))) * scale
+            base = nxt
+        parts.append(arr)
+        offs.append(off)
+        off += n_nodes
+    return FlatEnsemble(nodes=np.concatenate(parts), tree_off=np.asarray(offs, dtype=np.int64),
+                        scale_lo=np.asarray(scale_lo, dtype=np.float64),
+                        scale_hi=np.asarray(scale_hi, dtype=np.float64), base_score=0.0,
+                        max_depth=depth, manifest=tuple(manifest))
+
+
+def flat_to_document(flat: FlatEnsemble) -> dict:
+    """FlatEnsemble -> reference JSON document (for cross-checks on small ensembles)."""
+    trees = []
+    ends = list(flat.tree_off[1:]) + [len(flat.nodes)]
+    for o, e in zip(flat.tree_off, ends):
+        nodes = []
+        for nd in flat.nodes[o:e]:
+            if nd["feature"] < 0:
+                nodes.append({"value": float(nd["v"])})
+            else:
+                nodes.append({"feature": int(nd["feature"]), "threshold": float(nd["v"]),
+                              "left": int(nd["left"]), "right": int(nd["left"]) + 1})
+        trees.append({"nodes": nodes})
+    return {"schema_version": 1, "base_score": flat.base_score,
+            "feature_manifest": list(flat.manifest),
+            "scaling": {"min": [float(v) for v in flat.scale_lo],
+                        "max": [float(v) for v in flat.scale_hi]},
+            "trees": trees, "gains": [0.0] * len(flat.manifest)}

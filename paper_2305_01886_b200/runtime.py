@@ -1,0 +1,278 @@
+"""Device runtime: loads ``libgk.so`` (sm_100a) and drives its C-ABI with
+torch-owned device buffers.
+
+PyTorch is plumbing here -- device memory, streams, host<->device copies.  All
+arithmetic of the hot path runs inside libgk's kernels.  There is no CPU
+fallback: if the library or a CUDA device is missing, every entry point raises
+:class:`DeviceError`.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from pathlib import Path
+
+import numpy as np
+
+from . import abi
+from .errors import DeviceError
+from .pack import KSTAT_DT, Corpus, arch_records, config_array, latency_table
+
+LIB_PATH = Path(__file__).resolve().parent / "libgk.so"
+EXPORTS = ("gk_abi_version", "gk_last_error", "gk_device_sm_count", "gk_static_features",
+           "gk_schedule_features", "gk_rf_predict", "gk_sweep_workspace_bytes",
+           "gk_predict_energy_sweep")
+_lib = None
+
+
+def load_library(path: Path | None = None):
+    """ctypes handle of libgk with argtypes set.  Does not touch the GPU."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = Path(path or LIB_PATH)
+    if not p.exists():
+        raise DeviceError(f"{p} is missing: build it with `python -m paper_2305_01886_b200.build` "
+                          "(there is no CPU fallback)")
+    try:
+        L = C.CDLL(str(p))
+    except OSError as exc:
+        raise DeviceError(f"cannot load {p}: {exc}") from exc
+    vp, u32, i64 = C.c_void_p, C.c_uint32, C.c_int64
+    L.gk_abi_version.restype = C.c_int
+    L.gk_last_error.restype = C.c_char_p
+    L.gk_device_sm_count.restype = C.c_int
+    L.gk_static_features.argtypes = [vp, vp, vp, vp, vp]
+    L.gk_schedule_features.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, u32, vp, vp, vp]
+    L.gk_rf_predict.argtypes = [vp, vp, i64, i64, vp, vp, vp, vp, vp]
+    L.gk_sweep_workspace_bytes.argtypes = [vp, u32]
+    L.gk_sweep_workspace_bytes.restype = C.c_size_t
+    L.gk_predict_energy_sweep.argtypes = [vp, vp, vp, vp, u32, vp, vp, vp, vp, vp, vp]
+    if L.gk_abi_version() != 1:
+        raise DeviceError("libgk ABI version mismatch")
+    if path is None:
+        _lib = L
+    return L
+
+
+def _torch():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise DeviceError("no CUDA device: the sm_100a path has no CPU fallback")
+    return torch
+
+
+def device():
+    return _torch().device("cuda", _torch().cuda.current_device())
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        raise DeviceError(load_library().gk_last_error().decode() or f"libgk error {rc}")
+
+
+def _stream(stream=None) -> int:
+    t = _torch()
+    s = stream if stream is not None else t.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _dev(a: np.ndarray, dev=None):
+    """numpy -> device tensor of raw bytes (structured dtypes go as uint8)."""
+    t = _torch()
+    a = np.ascontiguousarray(a)
+    host = t.from_numpy(a.view(np.uint8).reshape(-1) if a.dtype.fields else a)
+    return host.to(dev or device(), non_blocking=False)
+
+
+def _ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+@dataclass
+class DeviceCorpus:
+    """A packed corpus resident in HBM."""
+
+    corpus: Corpus
+    bufs: dict = field(default_factory=dict)
+    desc: abi.GkCorpus | None = None
+
+    @classmethod
+    def upload(cls, corpus: Corpus) -> "DeviceCorpus":
+        dc = cls(corpus.check())
+        for k in ("tok", "preds", "blk", "fpreds", "topo", "ker"):
+            arr = getattr(corpus, k)
+            if len(arr) == 0:
+                arr = np.zeros(1, arr.dtype)
+            dc.bufs[k] = _dev(arr)
+        b = dc.bufs
+        dc.desc = abi.GkCorpus(_ptr(b["tok"]), _ptr(b["preds"]), _ptr(b["blk"]), _ptr(b["fpreds"]),
+                               _ptr(b["topo"]), _ptr(b["ker"]), corpus.n_tok, len(corpus.blk),
+                               corpus.n_ker, max(len(corpus.sigs), 1), corpus.max_n,
+                               corpus.max_blk)
+        return dc
+
+    @property
+    def nbytes(self) -> int:
+        return sum(t.numel() * t.element_size() for t in self.bufs.values())
+
+
+@dataclass
+class DeviceGrid:
+    """kernels x archs x configs, resident in HBM."""
+
+    n_k: int
+    n_arch: int
+    n_cfg: int
+    bufs: dict = field(default_factory=dict)
+    desc: abi.GkGrid | None = None
+
+    @classmethod
+    def build(cls, dcorpus: DeviceCorpus, profiles, configs, kernel_ids=None, n_tw=None,
+              gm=None) -> "DeviceGrid":
+        """n_tw / gm: optional per-config overrides (schedule_block/_cfg faces)."""
+        corpus = dcorpus.corpus
+        kid = (np.arange(corpus.n_ker, dtype=np.uint32) if kernel_ids is None
+               else np.asarray(kernel_ids, dtype=np.uint32))
+        if len(kid) and int(kid.max()) >= corpus.n_ker:
+            raise ValueError("kernel id out of range")
+        cfg = config_array(configs)
+        arch = arch_records(profiles)
+        lat = np.ascontiguousarray(latency_table(profiles, corpus.sigs))
+        g = cls(len(kid), len(arch), len(cfg))
+        g.bufs = {"kid": _dev(kid if len(kid) else np.zeros(1, np.uint32)), "cfg": _dev(cfg),
+                  "arch": _dev(arch), "lat": _dev(lat)}
+        if n_tw is not None:
+            g.bufs["n_tw"] = _dev(np.asarray(n_tw, dtype=np.int64))
+        if gm is not None:
+            g.bufs["gm"] = _dev(np.asarray(gm, dtype=np.float64))
+        g.desc = abi.GkGrid(_ptr(g.bufs["kid"]), _ptr(g.bufs["cfg"]), _ptr(g.bufs["arch"]),
+                            _ptr(g.bufs["lat"]), _ptr(g.bufs.get("n_tw")),
+                            _ptr(g.bufs.get("gm")), len(kid), len(cfg), len(arch), 0)
+        return g
+
+    @property
+    def n_points(self) -> int:
+        return self.n_k * self.n_arch * self.n_cfg
+
+
+@dataclass
+class DeviceEnsemble:
+    flat: object
+    bufs: dict = field(default_factory=dict)
+    desc: abi.GkEnsemble | None = None
+
+    @classmethod
+    def upload(cls, flat) -> "DeviceEnsemble":
+        if flat.n_trees == 0:
+            # zero-tree ensembles (reference fixture ensemble_constant.json) keep one dummy node
+            pass
+        de = cls(flat)
+        de.bufs = {"nodes": _dev(flat.nodes), "off": _dev(flat.tree_off if flat.n_trees
+                                                         else np.zeros(1, np.int64)),
+                   "lo": _dev(flat.scale_lo), "hi": _dev(flat.scale_hi)}
+        b = de.bufs
+        de.desc = abi.GkEnsemble(_ptr(b["nodes"]), _ptr(b["off"]), _ptr(b["lo"]), _ptr(b["hi"]),
+                                 float(flat.base_score), flat.n_trees, flat.n_feat,
+                                 flat.max_depth)
+        return de
+
+
+# ------------------------------------------------------------------ calls
+
+
+def static_features(dc: DeviceCorpus, dg: DeviceGrid, stream=None):
+    t = _torch()
+    dev = device()
+    ks = t.empty(dg.n_k * KSTAT_DT.itemsize, dtype=t.uint8, device=dev)
+    ls = t.empty((dg.n_arch, dg.n_k, 3), dtype=t.float64, device=dev)
+    _check(load_library().gk_static_features(C.byref(dc.desc), C.byref(dg.desc), _ptr(ks),
+                                             _ptr(ls), _stream(stream)))
+    return ks, ls
+
+
+def schedule_features(dc: DeviceCorpus, dg: DeviceGrid, *, si=True, sf=True, feat=True,
+                      sel_idx=None, trace=False, stream=None) -> dict:
+    """K1 + K2/K3 over a grid; returns device tensors keyed like the oracle."""
+    t = _torch()
+    dev = device()
+    n = dg.n_points
+    ks, ls = static_features(dc, dg, stream)
+    out = {"status": t.empty(n, dtype=t.uint8, device=dev)}
+    if si:
+        out["si"] = t.empty((n, abi.NSI), dtype=t.int64, device=dev)
+    if sf:
+        out["sf"] = t.empty((n, abi.NSF), dtype=t.float64, device=dev)
+    if feat:
+        out["feat"] = t.empty((n, abi.NFEAT), dtype=t.float64, device=dev)
+    sel_t = None
+    if sel_idx is not None:
+        sel_t = _dev(np.asarray(sel_idx, dtype=np.int32))
+        out["sel"] = t.empty((n, len(sel_idx)), dtype=t.float64, device=dev)
+    tr = None
+    if trace:
+        if dg.n_k != 1:
+            raise ValueError("trace needs a single-kernel grid")
+        k = dc.corpus.ker[int(dg.bufs["kid"][0].item())]
+        nt, nb = int(k["n_tok"]), int(k["n_blk"])
+        for key, shape, dt in (("start", (n, nt), t.float64), ("duration", (n, nt), t.float64),
+                               ("latency", (n, nt), t.float64), ("n_batches", (n, nt), t.int64),
+                               ("blk_delay", (n, nb), t.float64),
+                               ("blk_finish", (n, nb), t.float64)):
+            out["tr_" + key] = t.zeros(shape, dtype=dt, device=dev)
+        tr = abi.GkTrace(*[_ptr(out["tr_" + k]) for k in ("start", "duration", "latency",
+                                                          "n_batches", "blk_delay", "blk_finish")])
+    _check(load_library().gk_schedule_features(
+        C.byref(dc.desc), C.byref(dg.desc), _ptr(ks), _ptr(ls), _ptr(out["status"]),
+        _ptr(out.get("si")), _ptr(out.get("sf")), _ptr(out.get("feat")), _ptr(sel_t),
+        0 if sel_idx is None else len(sel_idx), _ptr(out.get("sel")),
+        C.byref(tr) if tr is not None else None, _stream(stream)))
+    out["kstat"], out["latsum"] = ks, ls
+    return out
+
+
+def rf_predict(de: DeviceEnsemble, X, *, status=None, time_us=None, stream=None):
+    """K4 (+K6) over device rows X [n, >= n_feat] float64."""
+    t = _torch()
+    if X.dtype != t.float64 or not X.is_cuda or X.dim() != 2:
+        raise ValueError("X must be a 2-D float64 CUDA tensor")
+    X = X.contiguous()
+    n = X.shape[0]
+    power = t.empty(n, dtype=t.float64, device=X.device)
+    energy = t.empty(n, dtype=t.float64, device=X.device) if time_us is not None else None
+    _check(load_library().gk_rf_predict(C.byref(de.desc), _ptr(X), X.shape[1], n, _ptr(status),
+                                        _ptr(time_us), _ptr(power), _ptr(energy),
+                                        _stream(stream)))
+    return power, energy
+
+
+class Sweep:
+    """Preallocated fused energy sweep (K1 -> K2/K3 -> K4 -> K6) over one grid."""
+
+    def __init__(self, dc: DeviceCorpus, dg: DeviceGrid, ensembles, sel_idx):
+        t = _torch()
+        if len(ensembles) != dg.n_arch:
+            raise ValueError("one ensemble per arch")
+        self.dc, self.dg, self.ens = dc, dg, list(ensembles)
+        self.sel = _dev(np.asarray(sel_idx, dtype=np.int32))
+        self.n_sel = len(sel_idx)
+        arr = (abi.GkEnsemble * len(ensembles))(*[e.desc for e in ensembles])
+        self.ens_arr = arr
+        L = load_library()
+        ws = L.gk_sweep_workspace_bytes(C.byref(dg.desc), self.n_sel)
+        dev = device()
+        self.work = t.empty(max(ws, 256), dtype=t.uint8, device=dev)
+        n = dg.n_points
+        self.status = t.empty(n, dtype=t.uint8, device=dev)
+        self.time_us = t.empty(n, dtype=t.float64, device=dev)
+        self.power = t.empty(n, dtype=t.float64, device=dev)
+        self.energy = t.empty(n, dtype=t.float64, device=dev)
+
+    def run(self, stream=None):
+        _check(load_library().gk_predict_energy_sweep(
+            C.byref(self.dc.desc), C.byref(self.dg.desc), self.ens_arr, _ptr(self.sel),
+            self.n_sel, _ptr(self.work), _ptr(self.status), _ptr(self.time_us), _ptr(self.power),
+            _ptr(self.energy), _stream(stream)))
+        return self.status, self.time_us, self.power, self.energy
