@@ -206,29 +206,15 @@ def run_ours(args, rank, world, local_rank):
 
 
 def per_kernel_split(rt, dc, dg, sweep, W, flush, steps):
-    """Average device time of each stage, CUDA events on the launching stream."""
-    import torch
-
-    stream = torch.cuda.current_stream()
-    ks, ls = rt.static_features(dc, dg)
-    names = ["k1_static", "k23_schedule", "k4_rf_predict"]
-    acc = {n: 0.0 for n in names}
+    """Average device time of each stage of the sweep: CUDA events recorded by
+    libgk between its launches on the launching stream (no host work between)."""
+    acc = {}
     n = max(steps, 1)
-    out = None
     for _ in range(n):
         flush.zero_()
-        e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-        e[0].record(stream)
-        ks, ls = rt.static_features(dc, dg)
-        e[1].record(stream)
-        out = rt.schedule_features(dc, dg, si=False, sf=True, feat=False, sel_idx=W["sel"])
-        e[2].record(stream)
-        rt.rf_predict(sweep.ens[0], out["sel"], status=out["status"], time_us=out["sf"][:, 7])
-        e[3].record(stream)
-        torch.cuda.synchronize()
-        for i, nm in enumerate(names):
-            acc[nm] += e[i].elapsed_time(e[i + 1])
-    return {k: v / n for k, v in acc.items()}
+        for k, v in sweep.stage_ms().items():
+            acc[k] = acc.get(k, 0.0) + v / n
+    return acc
 
 
 def run_e2e(rt, W, c, dg, sweep, steps, flush):
@@ -322,6 +308,7 @@ def main():
     ap.add_argument("--trees", type=int, default=500)
     ap.add_argument("--depth", type=int, default=16)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline (profiling)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -391,8 +378,10 @@ def main():
     peak, peak_kind = hbm_peak()
     achieved = alg[dom] / (split[dom] / 1e3) / 1e9
     # CPU baseline on rank 0 (bounded sample)
-    nk = sample_kernels(W, args.cpu_seconds, threads, R["flats"])
-    cp, cs = cpu_sample(args, W, R["flats"], nk, threads)
+    nk, cp, cs = 0, 0, 1.0
+    if not args.no_cpu:
+        nk = sample_kernels(W, args.cpu_seconds, threads, R["flats"])
+        cp, cs = cpu_sample(args, W, R["flats"], nk, threads)
     line = {
         "metric": metric, "value": value, "unit": "points/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,

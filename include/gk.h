@@ -43,14 +43,20 @@ enum { GK_OK = 0, GK_INFEASIBLE_LAUNCH = 1, GK_INFEASIBLE_OCCUPANCY = 2 };
 #define GK_MAX_BP 8   /* piecewise global-latency breakpoints per arch */
 #define GK_NFEAT 32   /* FEATURE_ORDER length (features.py:21-54)      */
 
-/* One PTX instruction, program order (8 B).  The DFG predecessors of token i
+/* One PTX instruction, program order (16 B).  The DFG predecessors of token i
  * are preds[tok[i].pred0 .. tok[i+1].pred0) (block-local producer indices);
- * the token array carries one sentinel entry at the end. */
+ * the token array carries one sentinel entry at the end.  lst_row / lst_len
+ * place the instruction's reservation span: its resource's span list occupies
+ * rows [lst_row, lst_row + res_cnt[res]) of the block's span table and
+ * lst_len same-resource instructions precede it in the block. */
 typedef struct {
-    uint8_t  res;    /* GK_SP..GK_WS                                  */
-    uint8_t  cls;    /* class code (bits 0-1) | GK_F_* flags           */
-    uint16_t sig;    /* latency signature id -> gk_arch-major lat table */
-    uint32_t pred0;  /* offset into preds[]                            */
+    uint8_t  res;     /* GK_SP..GK_WS                                  */
+    uint8_t  cls;     /* class code (bits 0-1) | GK_F_* flags           */
+    uint16_t sig;     /* latency signature id -> gk_arch-major lat table */
+    uint32_t pred0;   /* offset into preds[]                            */
+    uint16_t lst_row; /* first row of this resource's list in the block */
+    uint16_t lst_len; /* earlier same-resource instructions in the block */
+    uint32_t pad_;
 } gk_token;
 
 /* One basic block (40 B). */
@@ -209,6 +215,12 @@ int gk_predict_energy_sweep(const gk_corpus *corpus, const gk_grid *grid,
                             uint32_t n_sel, void *work, uint8_t *out_status,
                             double *out_time_us, double *out_power, double *out_energy,
                             void *stream);
+
+/* Profiling aid: when enabled, gk_predict_energy_sweep records CUDA events
+ * between its K1 / K2+K3 / K4 launches; gk_get_stage_ms waits for the last
+ * sweep and returns the three stage durations in ms. */
+int gk_set_stage_timing(int on);
+int gk_get_stage_ms(float *out3);
 
 #ifdef __cplusplus
 }

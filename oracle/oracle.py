@@ -26,7 +26,8 @@ _lib = None
 
 
 def build(force: bool = False) -> Path:
-    if force or not LIB.exists() or LIB.stat().st_mtime < (HERE / "gk_oracle.c").stat().st_mtime:
+    deps = [HERE / "gk_oracle.c", HERE.parent / "include" / "gk.h"]
+    if force or not LIB.exists() or any(LIB.stat().st_mtime < d.stat().st_mtime for d in deps):
         subprocess.run(["make", "-C", str(HERE), "-B" if force else "libgk_oracle.so"],
                        check=True, capture_output=True)
     return LIB

@@ -50,7 +50,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     objs, procs = [], []
     for src in SOURCES:
         obj = objdir / (Path(src).stem + ".o")
-        cmd = [nvcc(), *ARCH, *NVFLAGS, "-c", str(CSRC / src), "-o", str(obj)]
+        extra = os.environ.get("GK_NVCC_EXTRA", "").split()
+        cmd = [nvcc(), *ARCH, *NVFLAGS, *extra, "-c", str(CSRC / src), "-o", str(obj)]
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT,
                                             text=True)))
         objs.append(str(obj))

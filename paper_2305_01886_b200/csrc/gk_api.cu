@@ -34,6 +34,17 @@ int gk_launch_rf(const gk_ensemble *, uint32_t, const double *, int64_t, int64_t
 
 namespace {
 
+// optional per-stage timing of the fused sweep (profiling aid; synchronises)
+bool g_stage_timing = false;
+float g_stage_ms[3] = {0.f, 0.f, 0.f};
+cudaEvent_t g_ev[4] = {nullptr, nullptr, nullptr, nullptr};
+
+void stage_mark(int i, cudaStream_t st) {
+    if (!g_stage_timing) return;
+    if (!g_ev[i]) cudaEventCreate(&g_ev[i]);
+    cudaEventRecord(g_ev[i], st);
+}
+
 struct Scratch {
     void *p = nullptr;
     size_t n = 0;
@@ -76,6 +87,21 @@ int check_grid(const gk_corpus *C, const gk_grid *G) {
 extern "C" {
 
 int gk_abi_version(void) { return GK_ABI_VERSION; }
+
+int gk_set_stage_timing(int on) {
+    g_stage_timing = on != 0;
+    return 0;
+}
+
+int gk_get_stage_ms(float *out3) {
+    if (!g_ev[3]) {
+        gk_set_error("no timed sweep recorded");
+        return -1;
+    }
+    if (cudaEventSynchronize(g_ev[3]) != cudaSuccess) return -2;
+    for (int i = 0; i < 3; i++) cudaEventElapsedTime(&out3[i], g_ev[i], g_ev[i + 1]);
+    return 0;
+}
 
 const char *gk_last_error(void) { return g_err; }
 
@@ -161,7 +187,9 @@ int gk_predict_energy_sweep(const gk_corpus *corpus, const gk_grid *grid,
     w += ((sizeof(double) * 3 * grid->n_k * grid->n_arch + 255) / 256) * 256;
     double *sel = (double *)w;
     const size_t n_points = (size_t)grid->n_k * grid->n_arch * grid->n_cfg;
+    stage_mark(0, st);
     if (int rc = gk_launch_static(corpus, grid, ks, latsum, st)) return rc;
+    stage_mark(1, st);
     const uint32_t max_n = corpus->max_n ? corpus->max_n : 1;
     const uint32_t max_blk = corpus->max_blk ? corpus->max_blk : 1;
     void *ws = nullptr;
@@ -170,8 +198,11 @@ int gk_predict_energy_sweep(const gk_corpus *corpus, const gk_grid *grid,
                                  sel_idx, n_sel, sel, out_time_us, nullptr, max_n, max_blk,
                                  (double *)ws, st))
         return rc;
-    return gk_launch_rf(ens_host, grid->n_arch, sel, n_sel, (int64_t)n_points, out_status,
-                        out_time_us, out_power, out_energy, grid->n_cfg, grid->n_arch, st);
+    stage_mark(2, st);
+    const int rc = gk_launch_rf(ens_host, grid->n_arch, sel, n_sel, (int64_t)n_points, out_status,
+                                out_time_us, out_power, out_energy, grid->n_cfg, grid->n_arch, st);
+    stage_mark(3, st);
+    return rc;
 }
 
 }  // extern "C"

@@ -1,29 +1,26 @@
 // gk_sched.cu -- K1 (static segmented counts) and K2/K3 (per-point cycle
 // estimator + feature composition) for sm_100a.
 //
-// K3 design: one warp = 4 points of the SAME kernel (4
-// segments x 8 lanes).  All segments walk the kernel's token stream in
-// lock-step (warp-uniform control flow; the per-resource span-list lengths
-// depend only on the token stream), while each segment carries its own
-// reservation table.  The reference's sequential first-fit scan
-// (scheduler.py:59-68) is evaluated exactly with a segmented prefix-max over
-// the (start, end)-sorted span list: t_k = max(ready, e_0..e_{k-1}); the
-// answer is t_k at the first k with e_k > t_k and s_k >= t_k + length, else
-// the running max -- valid for negative-length spans too.
-// insort (scheduler.py:70-71) becomes a segmented ballot count + shift.
-// Span lists live in shared memory (spilling to a global scratch slot for
-// blocks longer than kSmemInstr); latency / unit / gap tables are staged in
-// shared memory per CTA.
+// K3 design: one warp = 32 points of the SAME kernel, one
+// point per lane.  All lanes walk the kernel's token stream in lock-step
+// (warp-uniform token loads and loop bounds -- list lengths depend only on the
+// token stream), each carrying its own reservation table in shared memory.
+// The reference's sequential first-fit (scheduler.py:59-68) is kept exactly:
+// spans of every block are sorted (start, end) tuples; while no span of the
+// block has negative length the spans are disjoint, hence their ends sorted,
+// and the prefix the reference skips with `continue` (ends <= ready) is jumped
+// by binary search; otherwise (negative global latency) the
+// scan starts at the list head.  insort-right (scheduler.py:70-71) is a
+// binary search plus shift.  Latency / unit / gap tables are staged in shared
+// memory per CTA; `pipeline * (batches - 1)` is computed once per point.
 #include <stdio.h>
+#include <stdlib.h>
 
 #include "gk_internal.cuh"
 
 namespace gk {
 
-constexpr int kSeg = 8;              // lanes per point
-constexpr int kPts = 32 / kSeg;      // points per warp
-constexpr int kWarps = 8;            // warps per CTA
-constexpr int kSmemInstr = 48;       // per-point span/fin capacity in shared memory
+constexpr int kWarps = 4;            // warps per CTA (each warp: 32 points of one kernel)
 
 // ------------------------------------------------------------------ K1
 
@@ -127,6 +124,17 @@ __global__ void k1_latsum_wide(gk_corpus C, gk_grid G, double *__restrict__ lats
 }
 
 // ------------------------------------------------------------ K2 / K3
+//
+// Lane-per-point: a warp owns 32 points of ONE kernel (consecutive (arch,
+// config) pairs), so every lane walks the same token stream (uniform loads and
+// control flow) while carrying its own reservation table.  Per-point tables
+// live in shared memory as [row][lane] (conflict-free 8-byte accesses):
+//   fin[row]      finish time of instruction `row` of the current block
+//   ss/se[row]    sorted (start, end) spans; resource r's list occupies rows
+//                 [tok.lst_row, +res_cnt[r]) and holds tok.lst_len spans when
+//                 instruction i is scheduled.
+// Blocks longer than the shared slab use the same layout in a global scratch
+// slab (L1/L2 resident).
 
 struct PointOut {
     uint8_t *status;
@@ -140,143 +148,11 @@ struct PointOut {
     int has_trace;
 };
 
-// shared-memory staging of the per-arch tables
 struct ArchSmem {
     double pipeline;
     double gap[GK_NRES];
     int64_t units[GK_NRES];
 };
-
-// One segment's reservation table + per-instruction finish times.
-struct SegMem {
-    double *fin;   // [cap]
-    double *ss;    // span starts [cap], resource r at [res_off[r], +res_cnt[r])
-    double *se;    // span ends
-};
-
-// Schedule one basic block for the 4 points of this warp.  Returns the block
-// delay of this lane's point (segment-uniform).  scheduler.py:137-185.
-__device__ __forceinline__ double schedule_block(
-    const gk_corpus &C, const gk_block &B, const ArchSmem *__restrict__ arch_s,
-    const double *__restrict__ lat_s, uint32_t n_sig, int ai, int64_t n_tw, double gm_lat,
-    SegMem mem, int sl, unsigned seg_mask, int seg_shift, double *tr_start, double *tr_dur,
-    double *tr_lat, int64_t *tr_nb, bool write_trace) {
-    const ArchSmem &A = arch_s[ai];
-    uint32_t res_off[GK_NRES], res_len[GK_NRES];
-    {
-        uint32_t o = 0;
-#pragma unroll
-        for (int r = 0; r < GK_NRES; r++) {
-            res_off[r] = o;
-            res_len[r] = 0;
-            o += B.res_cnt[r];
-        }
-    }
-    double delay = 0.0;
-    const gk_token *tok = C.tok + B.tok0;
-    for (uint32_t i = 0; i < B.n; i++) {
-        const gk_token T = tok[i];
-        const uint32_t next_pred = tok[i + 1].pred0;
-        const int r = T.res;
-        const double lat = ((T.cls & 3) == GK_GLOBAL) ? gm_lat : lat_s[ai * n_sig + T.sig];
-        const int64_t units = A.units[r];
-        const int64_t nb = (n_tw + units - 1) / units;  // types.py:150-152
-        const double d = __dadd_rn(lat, __dmul_rn(A.pipeline, (double)(nb - 1)));
-        const double gap = A.gap[r];
-        const double len = __dadd_rn(d, gap);
-        // ready = max(0, finish of DFG producers)   scheduler.py:166-168
-        double ready = 0.0;
-        for (uint32_t q = T.pred0; q < next_pred; q++) ready = dmax(ready, mem.fin[C.preds[q]]);
-
-        // ---- earliest_start: segmented prefix-max scan over sorted spans
-        const uint32_t L = res_len[r];
-        const uint32_t base = res_off[r];
-        double carry = ready, start = 0.0;
-        bool found = false;
-        for (uint32_t c0 = 0; c0 < L; c0 += kSeg) {
-            const uint32_t k = c0 + sl;
-            const bool valid = k < L;
-            const double s = valid ? mem.ss[base + k] : 0.0;
-            const double e = valid ? mem.se[base + k] : -__longlong_as_double(0x7ff0000000000000ll);
-            double pm = e;  // inclusive prefix max of ends inside the chunk
-#pragma unroll
-            for (int off = 1; off < kSeg; off <<= 1) {
-                const double o = shfl_up_d(pm, off, kSeg);
-                if (sl >= off) pm = dmax(pm, o);
-            }
-            double ex = shfl_up_d(pm, 1, kSeg);
-            const double tk = sl == 0 ? carry : dmax(carry, ex);
-            const bool hit = valid && !found && (e > tk) && (s >= __dadd_rn(tk, len));
-            const unsigned bal = (__ballot_sync(GK_FULL, hit) >> seg_shift) & 0xffu;
-            const double tsel = shfl_d(tk, bal ? __ffs(bal) - 1 : 0, kSeg);
-            const double cmax = shfl_d(pm, kSeg - 1, kSeg);
-            if (!found) {
-                if (bal) {
-                    start = tsel;
-                    found = true;
-                } else {
-                    carry = dmax(carry, cmax);
-                }
-            }
-            if (__all_sync(GK_FULL, found)) break;
-        }
-        if (!found) start = carry;
-        const double fin = __dadd_rn(start, d);
-        const double end = __dadd_rn(fin, gap);  // (start + d) + gap, scheduler.py:171
-
-        // ---- insort-right: pos = #elements <= (start, end)
-        uint32_t pos = 0;
-        for (uint32_t c0 = 0; c0 < L; c0 += kSeg) {
-            const uint32_t k = c0 + sl;
-            const bool valid = k < L;
-            bool le = false;
-            if (valid) {
-                const double s = mem.ss[base + k], e = mem.se[base + k];
-                le = !(start < s || (start == s && end < e));
-            }
-            const unsigned bal = (__ballot_sync(GK_FULL, le) >> seg_shift) & 0xffu;
-            pos += __popc(bal);
-            // sorted list: once a chunk is not all-le for every segment, stop
-            const bool seg_done = __popc(bal) < min((uint32_t)kSeg, L - c0);
-            if (__all_sync(GK_FULL, seg_done)) break;
-        }
-        // shift elements [pos, L) up by one, last chunk first
-        if (L > 0) {
-            for (int c0 = (int)((L - 1) / kSeg) * kSeg; c0 >= 0; c0 -= kSeg) {
-                const uint32_t k = (uint32_t)c0 + sl;
-                const bool mv = k < L && k >= pos;
-                double s = 0.0, e = 0.0;
-                if (mv) {
-                    s = mem.ss[base + k];
-                    e = mem.se[base + k];
-                }
-                __syncwarp();
-                if (mv) {
-                    mem.ss[base + k + 1] = s;
-                    mem.se[base + k + 1] = e;
-                }
-                __syncwarp();
-                if (!__any_sync(GK_FULL, pos < (uint32_t)c0)) break;
-            }
-        }
-        if (sl == 0) {
-            mem.ss[base + pos] = start;
-            mem.se[base + pos] = end;
-            mem.fin[i] = fin;
-            if (write_trace) {
-                tr_start[i] = start;
-                tr_dur[i] = d;
-                tr_lat[i] = lat;
-                tr_nb[i] = nb;
-            }
-        }
-        __syncwarp();
-        res_len[r] = L + 1;
-        delay = dmax(delay, fin);  // scheduler.py:184
-    }
-    (void)seg_mask;
-    return delay;
-}
 
 struct PointScalars {
     int active;
@@ -285,6 +161,111 @@ struct PointScalars {
     int64_t cap, n_schd, n_sm, waves;
     double gm;
 };
+
+// Per-lane constants of one point, selected by the warp-uniform resource id.
+struct ResTerms {
+    double dt[GK_NRES];   // pipeline * (ceil(n_tw / units_r) - 1)
+    double gap[GK_NRES];
+    int64_t nb[GK_NRES];
+    __device__ __forceinline__ void pick(int r, double &d, double &g, int64_t &n) const {
+        switch (r) {  // r is warp-uniform: a jump, not divergence
+            case 0: d = dt[0]; g = gap[0]; n = nb[0]; break;
+            case 1: d = dt[1]; g = gap[1]; n = nb[1]; break;
+            case 2: d = dt[2]; g = gap[2]; n = nb[2]; break;
+            case 3: d = dt[3]; g = gap[3]; n = nb[3]; break;
+            default: d = dt[4]; g = gap[4]; n = nb[4]; break;
+        }
+    }
+};
+
+struct Slab {       // [row][32] tables of the current block (smem or global)
+    double *fin, *ss, *se;
+};
+
+#define ROW(a, r) (a)[(size_t)(r) * 32 + lane]
+
+// schedule_block (scheduler.py:137-185) for this lane's point; returns delay.
+__device__ __forceinline__ double schedule_block(const gk_corpus &C, const gk_block &B,
+                                                 const ResTerms &RT, const double *lat_a,
+                                                 double gm_lat, Slab m, int lane,
+                                                 double *tr_start, double *tr_dur,
+                                                 double *tr_lat, int64_t *tr_nb) {
+    double delay = 0.0;
+    bool neg = false;  // a negative-length span exists: ends may be unsorted
+    const gk_token *tok = C.tok + B.tok0;
+    for (uint32_t i = 0; i < B.n; i++) {
+        const gk_token T = tok[i];
+        const uint32_t p1 = tok[i + 1].pred0;
+        double dterm, gap;
+        int64_t nb;
+        RT.pick(T.res, dterm, gap, nb);
+        const double lat = ((T.cls & 3) == GK_GLOBAL) ? gm_lat : lat_a[T.sig];
+        const double d = __dadd_rn(lat, dterm);  // lat + pipeline * (nb - 1)
+        const double len = __dadd_rn(d, gap);
+        double ready = 0.0;  // scheduler.py:166-168
+        for (uint32_t q = T.pred0; q < p1; q++) ready = dmax(ready, ROW(m.fin, C.preds[q]));
+
+        // earliest_start (scheduler.py:59-68).  With only non-negative spans
+        // the list is disjoint, so its ends are sorted and every span before
+        // the first end > ready is skipped by the reference's `continue`.
+        const uint32_t base = T.lst_row, L = T.lst_len;
+        uint32_t k = 0;
+        if (!neg && L > 0) {
+            if (ROW(m.se, base + L - 1) <= ready) {
+                k = L;  // frontier: every span ends by `ready` (the common case)
+            } else {
+                uint32_t lo = 0, hi = L - 1;
+                while (lo < hi) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    if (ROW(m.se, base + mid) > ready) hi = mid;
+                    else lo = mid + 1;
+                }
+                k = lo;
+            }
+        }
+        double t = ready;
+        for (; k < L; k++) {
+            const double s = ROW(m.ss, base + k), e = ROW(m.se, base + k);
+            if (e <= t) continue;
+            if (s >= __dadd_rn(t, len)) break;
+            t = e;
+        }
+        const double start = t;
+        const double fin = __dadd_rn(start, d);
+        const double end = __dadd_rn(fin, gap);  // (start + d) + gap
+        neg |= end < start;
+        // insort-right on (start, end) tuples (scheduler.py:70-71)
+        uint32_t lo = L;
+        if (L > 0) {
+            const double s = ROW(m.ss, base + L - 1), e = ROW(m.se, base + L - 1);
+            if (start < s || (start == s && end < e)) {  // not an append: search
+                uint32_t l2 = 0, hi = L - 1;
+                while (l2 < hi) {
+                    const uint32_t mid = (l2 + hi) >> 1;
+                    const double sm = ROW(m.ss, base + mid), em = ROW(m.se, base + mid);
+                    if (start < sm || (start == sm && end < em)) hi = mid;
+                    else l2 = mid + 1;
+                }
+                lo = l2;
+            }
+        }
+        for (uint32_t q = L; q > lo; q--) {
+            ROW(m.ss, base + q) = ROW(m.ss, base + q - 1);
+            ROW(m.se, base + q) = ROW(m.se, base + q - 1);
+        }
+        ROW(m.ss, base + lo) = start;
+        ROW(m.se, base + lo) = end;
+        ROW(m.fin, i) = fin;
+        delay = dmax(delay, fin);  // scheduler.py:184
+        if (tr_start) {
+            tr_start[i] = start;
+            tr_dur[i] = d;
+            tr_lat[i] = lat;
+            tr_nb[i] = nb;
+        }
+    }
+    return delay;
+}
 
 __device__ __forceinline__ void finish_point(const gk_corpus &C, const gk_grid &G,
                                              const gk_kstat *__restrict__ ks,
@@ -398,66 +379,69 @@ __device__ __forceinline__ void finish_point(const gk_corpus &C, const gk_grid &
                                 tput(A.tps_a, A.tps_b, A.tps_c, A.tp_floor, shar_sm))),
             shar_sm);
     }
-    double f[GK_NFEAT];
-    f[0] = comp_sm != 0 ? __ddiv_rn(comp_lat, comp_sm) : 0.0;
-    f[1] = glob_sm != 0 ? __ddiv_rn(glob_lat, glob_sm) : 0.0;
-    f[2] = misc_sm != 0 ? __ddiv_rn(misc_lat, misc_sm) : 0.0;
-    f[3] = shar_sm != 0 ? __ddiv_rn(shar_lat, shar_sm) : 0.0;
-    f[4] = (double)S.branches;
-    f[5] = (double)S.cnt[GK_COMPUTE];
-    f[6] = comp_sm;
-    f[7] = comp_lat;
-    f[8] = (double)S.cnt[GK_GLOBAL];
-    f[9] = glob_sm;
-    f[10] = glob_lat;
-    f[11] = (double)(waves * S.loads);
-    f[12] = (double)(waves * S.stores);
-    f[13] = (double)S.cnt[GK_MISC];
-    f[14] = misc_sm;
-    f[15] = misc_lat;
-    f[16] = (double)S.cnt[GK_SHARED];
-    f[17] = shar_sm;
-    f[18] = shar_lat;
-    f[19] = (double)(nB < A.nSM ? nB : A.nSM);
-    f[20] = (double)((P.n_sm + A.Sz_w - 1) / A.Sz_w);
-    f[21] = wv;
-    f[22] = x;
-    f[23] = __dmul_rn(__ddiv_rn(x, (double)(A.nWS * A.Sz_w)), __ddiv_rn(total_inst, (double)A.nDU));
-    f[24] = cache_pen;
-    f[25] = glb_pen;
-    f[26] = sh_pen;
-    f[27] = __ddiv_rn((double)(ob * wpb), (double)A.wSM_max);
-    f[28] = (double)c.regs;
-    f[29] = (double)c.shmem;
-    f[30] = (double)tpb;
-    f[31] = (double)nB;
+    // features on demand (no 32-double array: keeps register pressure down)
+    auto feature = [&](int q) -> double {
+        switch (q) {
+            case 0: return comp_sm != 0 ? __ddiv_rn(comp_lat, comp_sm) : 0.0;
+            case 1: return glob_sm != 0 ? __ddiv_rn(glob_lat, glob_sm) : 0.0;
+            case 2: return misc_sm != 0 ? __ddiv_rn(misc_lat, misc_sm) : 0.0;
+            case 3: return shar_sm != 0 ? __ddiv_rn(shar_lat, shar_sm) : 0.0;
+            case 4: return (double)S.branches;
+            case 5: return (double)S.cnt[GK_COMPUTE];
+            case 6: return comp_sm;
+            case 7: return comp_lat;
+            case 8: return (double)S.cnt[GK_GLOBAL];
+            case 9: return glob_sm;
+            case 10: return glob_lat;
+            case 11: return (double)(waves * S.loads);
+            case 12: return (double)(waves * S.stores);
+            case 13: return (double)S.cnt[GK_MISC];
+            case 14: return misc_sm;
+            case 15: return misc_lat;
+            case 16: return (double)S.cnt[GK_SHARED];
+            case 17: return shar_sm;
+            case 18: return shar_lat;
+            case 19: return (double)(nB < A.nSM ? nB : A.nSM);
+            case 20: return (double)((P.n_sm + A.Sz_w - 1) / A.Sz_w);
+            case 21: return wv;
+            case 22: return x;
+            case 23:
+                return __dmul_rn(__ddiv_rn(x, (double)(A.nWS * A.Sz_w)),
+                                 __ddiv_rn(total_inst, (double)A.nDU));
+            case 24: return cache_pen;
+            case 25: return glb_pen;
+            case 26: return sh_pen;
+            case 27: return __ddiv_rn((double)(ob * wpb), (double)A.wSM_max);
+            case 28: return (double)c.regs;
+            case 29: return (double)c.shmem;
+            case 30: return (double)tpb;
+            default: return (double)nB;
+        }
+    };
     if (O.feat) {
         double *o = O.feat + p * GK_NFEAT;
-#pragma unroll
-        for (int j = 0; j < GK_NFEAT; j++) o[j] = f[j];
+        for (int j = 0; j < GK_NFEAT; j++) o[j] = feature(j);
     }
     if (O.sel) {
         double *o = O.sel + p * O.n_sel;
-        for (uint32_t j = 0; j < O.n_sel; j++) {
-            const int fi = O.sel_idx[j];
-            double v = 0.0;
-#pragma unroll
-            for (int q = 0; q < GK_NFEAT; q++) v = q == fi ? f[q] : v;
-            o[j] = v;
-        }
+        for (uint32_t j = 0; j < O.n_sel; j++) o[j] = feature(O.sel_idx[j]);
     }
 }
 
-// Persistent warps over work items (kernel, 4 consecutive (arch, config) pairs).
-__global__ void __launch_bounds__(kWarps * 32) k23_schedule(
+
+// Persistent warps over work items (kernel, up to 32 consecutive (arch, config) pairs).
+#ifndef GK_K23_MINB
+#define GK_K23_MINB 6
+#endif
+__global__ void __launch_bounds__(kWarps * 32, GK_K23_MINB) k23_schedule(
     gk_corpus C, gk_grid G, const gk_kstat *__restrict__ ks, const double *__restrict__ latsum,
-    PointOut O, uint64_t n_items, uint32_t items_per_kernel, uint32_t smem_cap,
-    double *__restrict__ gscratch, uint32_t gscratch_instr, uint32_t max_blk) {
+    PointOut O, uint64_t n_items, uint32_t items_per_kernel, uint32_t ns,
+    double *__restrict__ gscratch, uint32_t g_rows, uint32_t max_blk) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const uint32_t n_arch = G.n_arch, n_sig = C.n_sig;
     ArchSmem *arch_s = reinterpret_cast<ArchSmem *>(smem_raw);
     double *lat_s = reinterpret_cast<double *>(arch_s + n_arch);
-    double *seg_base = lat_s + (size_t)n_arch * n_sig;
+    double *slab_base = lat_s + (size_t)n_arch * n_sig;
     for (uint32_t t = threadIdx.x; t < n_arch; t += blockDim.x) {
         const gk_arch &A = G.arch[t];
         arch_s[t].pipeline = A.pipeline;
@@ -470,31 +454,36 @@ __global__ void __launch_bounds__(kWarps * 32) k23_schedule(
     __syncthreads();
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int seg = lane / kSeg, sl = lane % kSeg, seg_shift = seg * kSeg;
-    const unsigned seg_mask = 0xffu << seg_shift;
-    // this segment's shared-memory slab: fin | ss | se, smem_cap entries each
-    double *my_smem = seg_base + ((size_t)(warp * kPts + seg)) * 3 * smem_cap;
-    const uint64_t gwarp = ((uint64_t)blockIdx.x * kWarps + warp);
+    Slab smem_slab;
+    smem_slab.fin = slab_base + (size_t)warp * 3 * ns * 32;
+    smem_slab.ss = smem_slab.fin + (size_t)ns * 32;
+    smem_slab.se = smem_slab.ss + (size_t)ns * 32;
+    const uint64_t gwarp = (uint64_t)blockIdx.x * kWarps + warp;
     const uint64_t n_warps = (uint64_t)gridDim.x * kWarps;
-    // global slab: [3 * gscratch_instr] spans + [2 * max_blk] block delay/finish
-    const size_t gslab = 3 * (size_t)gscratch_instr + 2 * (size_t)max_blk;
-    double *my_g = gscratch + (gwarp * kPts + seg) * gslab;
-    double *blk_delay = my_g + 3 * (size_t)gscratch_instr;
-    double *blk_finish = blk_delay + max_blk;
+    const size_t gslab = (3 * (size_t)g_rows + 2 * (size_t)max_blk) * 32;
+    double *my_g = gscratch + gwarp * gslab;
+    Slab glob_slab;
+    glob_slab.fin = my_g;
+    glob_slab.ss = my_g + (size_t)g_rows * 32;
+    glob_slab.se = my_g + 2 * (size_t)g_rows * 32;
+    double *blk_delay = my_g + 3 * (size_t)g_rows * 32;   // [max_blk][32]
+    double *blk_finish = blk_delay + (size_t)max_blk * 32;
     const uint32_t P_k = n_arch * G.n_cfg;
+    const double NaN = __longlong_as_double(0x7ff8000000000000ll);
 
     for (uint64_t item = gwarp; item < n_items; item += n_warps) {
         const uint32_t ki = (uint32_t)(item / items_per_kernel);
-        const uint32_t j = (uint32_t)(item % items_per_kernel) * kPts + seg;
+        const uint32_t j0 = (uint32_t)(item % items_per_kernel) * 32;
         PointScalars P;
-        P.active = j < P_k;
-        const uint32_t jj = P.active ? j : (uint32_t)(item % items_per_kernel) * kPts;
+        P.active = j0 + lane < P_k;
+        const uint32_t j = P.active ? j0 + lane : j0;
         P.ki = ki;
-        P.ai = jj / G.n_cfg;
-        P.ci = jj % G.n_cfg;
-        P.p = (size_t)ki * P_k + jj;
+        P.ai = j / G.n_cfg;
+        P.ci = j % G.n_cfg;
+        P.p = (size_t)ki * P_k + j;
         const gk_kernel K = C.ker[G.kernel_ids[ki]];
         const gk_arch &A = G.arch[P.ai];
+        const ArchSmem &AS = arch_s[P.ai];
         const gk_config cfg = G.cfg[P.ci];
         P.cap = block_cap(A, cfg);
         const bool feasible = P.cap >= 1;
@@ -506,62 +495,58 @@ __global__ void __launch_bounds__(kWarps * 32) k23_schedule(
         int64_t n_tw = P.n_sm;  // schedule_block / schedule_cfg faces override these
         if (G.n_tw_override && G.n_tw_override[P.ci] > 0) n_tw = G.n_tw_override[P.ci];
         if (G.gm_override && !isnan(G.gm_override[P.ci])) P.gm = G.gm_override[P.ci];
-
+        ResTerms RT;
+#pragma unroll
+        for (int r = 0; r < GK_NRES; r++) {
+            const int64_t u = AS.units[r];
+            RT.nb[r] = (n_tw + u - 1) / u;  // batches, types.py:150-152
+            RT.dt[r] = __dmul_rn(AS.pipeline, (double)(RT.nb[r] - 1));
+            RT.gap[r] = AS.gap[r];
+        }
+        const double *lat_a = lat_s + (size_t)P.ai * n_sig;
         const bool write_trace = O.has_trace && P.active && feasible;
-        // schedule every block (scheduler.py:203-205)
-        for (uint32_t b = 0; b < K.n_blk; b++) {
+
+        for (uint32_t b = 0; b < K.n_blk; b++) {  // scheduler.py:203-205
             const gk_block B = C.blk[K.blk0 + b];
-            SegMem mem;
-            if (B.n <= smem_cap) {
-                mem.fin = my_smem;
-                mem.ss = my_smem + smem_cap;
-                mem.se = my_smem + 2 * smem_cap;
-            } else {
-                mem.fin = my_g;
-                mem.ss = my_g + gscratch_instr;
-                mem.se = my_g + 2 * (size_t)gscratch_instr;
-            }
-            const size_t t0 = B.tok0 - K.tok0;
-            const size_t trow = P.p * K.n_tok + t0;
+            const Slab m = B.n <= ns ? smem_slab : glob_slab;
+            const size_t trow = P.p * K.n_tok + (B.tok0 - K.tok0);
             const double dl = schedule_block(
-                C, B, arch_s, lat_s, n_sig, (int)P.ai, n_tw, P.gm, mem, sl, seg_mask, seg_shift,
-                write_trace ? O.trace.start + trow : nullptr,
+                C, B, RT, lat_a, P.gm, m, lane, write_trace ? O.trace.start + trow : nullptr,
                 write_trace ? O.trace.duration + trow : nullptr,
                 write_trace ? O.trace.latency + trow : nullptr,
-                write_trace ? O.trace.n_batches + trow : nullptr, write_trace);
-            if (sl == 0) blk_delay[b] = dl;
+                write_trace ? O.trace.n_batches + trow : nullptr);
+            ROW(blk_delay, b) = dl;
         }
-        __syncwarp();
-        if (sl == 0 && P.active) {
-            // schedule_cfg composition (scheduler.py:206-211)
-            const uint32_t *topo = C.topo + K.topo0;
-            for (uint32_t q = 0; q < K.n_blk; q++) {
-                const uint32_t i = topo[q];
-                const gk_block &B = C.blk[K.blk0 + i];
-                double d_in = 0.0;
-                for (uint32_t u = 0; u < B.n_fpred; u++) {
-                    const double f = blk_finish[C.fpreds[B.fpred0 + u]];
-                    d_in = u == 0 ? f : dmax(d_in, f);
-                }
-                blk_finish[i] = __dadd_rn(d_in, __dmul_rn(blk_delay[i], (double)B.mult));
+        // schedule_cfg composition (scheduler.py:206-211)
+        const uint32_t *topo = C.topo + K.topo0;
+        for (uint32_t q = 0; q < K.n_blk; q++) {
+            const uint32_t i = topo[q];
+            const gk_block &B = C.blk[K.blk0 + i];
+            double d_in = 0.0;  // max(..., default=0.0)
+            for (uint32_t u = 0; u < B.n_fpred; u++) {
+                const double f = ROW(blk_finish, C.fpreds[B.fpred0 + u]);
+                d_in = u == 0 ? f : dmax(d_in, f);
             }
-            double cfg_delay = 0.0;
-            bool first = true;
+            ROW(blk_finish, i) = __dadd_rn(d_in, __dmul_rn(ROW(blk_delay, i), (double)B.mult));
+        }
+        double cfg_delay = 0.0;
+        bool first = true;
+        for (uint32_t b = 0; b < K.n_blk; b++) {
+            if (!C.blk[K.blk0 + b].is_exit) continue;
+            const double f = ROW(blk_finish, b);
+            if (first || f > cfg_delay) cfg_delay = f;
+            first = false;
+        }
+        if (write_trace) {
             for (uint32_t b = 0; b < K.n_blk; b++) {
-                if (!C.blk[K.blk0 + b].is_exit) continue;
-                if (first || blk_finish[b] > cfg_delay) cfg_delay = blk_finish[b];
-                first = false;
+                O.trace.blk_delay[P.p * K.n_blk + b] = ROW(blk_delay, b);
+                O.trace.blk_finish[P.p * K.n_blk + b] = ROW(blk_finish, b);
             }
-            if (write_trace) {
-                for (uint32_t b = 0; b < K.n_blk; b++) {
-                    O.trace.blk_delay[P.p * K.n_blk + b] = blk_delay[b];
-                    O.trace.blk_finish[P.p * K.n_blk + b] = blk_finish[b];
-                }
-            }
+        }
+        if (P.active) {
             if (feasible) {
                 finish_point(C, G, ks, latsum, K, P, cfg_delay, O);
             } else {
-                const double NaN = __longlong_as_double(0x7ff8000000000000ll);
                 if (O.status) O.status[P.p] = GK_INFEASIBLE_LAUNCH;
                 if (O.si)
                     for (int q = 0; q < GK_NSI; q++) O.si[P.p * GK_NSI + q] = 0;
@@ -574,7 +559,6 @@ __global__ void __launch_bounds__(kWarps * 32) k23_schedule(
                     for (uint32_t q = 0; q < O.n_sel; q++) O.sel[P.p * O.n_sel + q] = NaN;
             }
         }
-        __syncwarp();
     }
 }
 
@@ -593,6 +577,19 @@ int sm_count() {
     }
     return g_sm_count;
 }
+// per-lane shared-memory rows (instructions per block held on chip); GK_SMEM_ROWS tunes it
+uint32_t smem_rows_cap() {
+    static uint32_t v = 0;
+    if (!v) {
+        const char *e = getenv("GK_SMEM_ROWS");
+        // measured on B200: L1-backed tables at 24 warps/SM beat a shared slab at
+        // lower occupancy (profiles/README.md); 0 = all tables in the L1 scratch
+        v = e ? (uint32_t)atoi(e) + 1 : 1;  // stored +1 so that 0 rows is representable
+        if (v > 257) v = 257;
+    }
+    return v - 1;
+}
+constexpr int kMaxCtaPerSm = 16;
 }  // namespace
 
 int gk_launch_static(const gk_corpus *C, const gk_grid *G, gk_kstat *ks, double *latsum,
@@ -607,11 +604,19 @@ int gk_launch_static(const gk_corpus *C, const gk_grid *G, gk_kstat *ks, double 
     return gk_check_launch("k1_static");
 }
 
+static uint32_t smem_rows(uint32_t max_n) {
+    const uint32_t cap = smem_rows_cap();
+    return max_n < cap ? max_n : cap;
+}
+static uint32_t global_rows(uint32_t max_n) {
+    return max_n > smem_rows_cap() ? (max_n ? max_n : 1) : 1;
+}
+
 size_t gk_sched_scratch_bytes(const gk_grid *G, uint32_t max_n, uint32_t max_blk) {
     (void)G;
-    const size_t warps = (size_t)sm_count() * 8 * gk::kWarps;  // upper bound of resident warps
-    const size_t slab = 3 * (size_t)max_n + 2 * (size_t)max_blk;
-    return warps * gk::kPts * slab * sizeof(double);
+    const size_t warps = (size_t)sm_count() * kMaxCtaPerSm * gk::kWarps;
+    const size_t slab = (3 * (size_t)global_rows(max_n) + 2 * (size_t)max_blk) * 32;
+    return warps * slab * sizeof(double);
 }
 
 int gk_launch_sched(const gk_corpus *C, const gk_grid *G, const gk_kstat *ks, const double *latsum,
@@ -620,7 +625,7 @@ int gk_launch_sched(const gk_corpus *C, const gk_grid *G, const gk_kstat *ks, co
                     uint32_t max_n, uint32_t max_blk, double *gscratch, cudaStream_t st) {
     const uint64_t P_k = (uint64_t)G->n_arch * G->n_cfg;
     if (G->n_k == 0 || P_k == 0) return 0;
-    const uint32_t ipk = (uint32_t)((P_k + gk::kPts - 1) / gk::kPts);
+    const uint32_t ipk = (uint32_t)((P_k + 31) / 32);
     const uint64_t n_items = (uint64_t)G->n_k * ipk;
     gk::PointOut O;
     O.status = status;
@@ -634,24 +639,27 @@ int gk_launch_sched(const gk_corpus *C, const gk_grid *G, const gk_kstat *ks, co
     O.has_trace = trace != nullptr && trace->start != nullptr;
     if (O.has_trace) O.trace = *trace;
     else memset(&O.trace, 0, sizeof O.trace);
-    const uint32_t smem_cap = max_n < (uint32_t)gk::kSmemInstr ? (max_n ? max_n : 1) : gk::kSmemInstr;
+    const uint32_t ns = smem_rows(max_n);
     const size_t smem = G->n_arch * (sizeof(gk::ArchSmem) + (size_t)C->n_sig * sizeof(double)) +
-                        (size_t)gk::kWarps * gk::kPts * 3 * smem_cap * sizeof(double);
+                        (size_t)gk::kWarps * 3 * ns * 32 * sizeof(double);
     if (smem > 48 * 1024) {
         cudaFuncSetAttribute(gk::k23_schedule, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
     }
+    // the reservation tables that do not fit the shared slab live in L1: prefer L1
+    cudaFuncSetAttribute(gk::k23_schedule, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         ns == 0 ? 0 : -1);
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gk::k23_schedule, gk::kWarps * 32, smem);
     if (per_sm < 1) {
         gk_set_error("k23_schedule: %zu B shared memory per CTA does not fit", smem);
         return -1;
     }
-    if (per_sm > 8) per_sm = 8;
+    if (per_sm > kMaxCtaPerSm) per_sm = kMaxCtaPerSm;
     uint64_t grid = (uint64_t)sm_count() * per_sm;
     const uint64_t need = (n_items + gk::kWarps - 1) / gk::kWarps;
     if (grid > need) grid = need;
     gk::k23_schedule<<<(unsigned)grid, gk::kWarps * 32, smem, st>>>(
-        *C, *G, ks, latsum, O, n_items, ipk, smem_cap, gscratch, max_n, max_blk);
+        *C, *G, ks, latsum, O, n_items, ipk, ns, gscratch, global_rows(max_n), max_blk);
     return gk_check_launch("k23_schedule");
 }

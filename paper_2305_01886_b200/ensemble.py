@@ -190,10 +190,10 @@ def flatten(ens: TreeEnsemble) -> FlatEnsemble:
 
 
 def random_forest_flat(n_trees: int, depth: int, manifest, scale_lo, scale_hi, seed: int,
-                       split_p: float = 0.93, leaf_scale: float | None = None) -> FlatEnsemble:
+                       split_p: float = 0.985, leaf_scale: float | None = None) -> FlatEnsemble:
     """A declared synthetic ensemble for throughput runs (BASELINE config #4/#5):
     n_trees trees of max depth `depth`, each node below the max depth splitting
-    with probability split_p (0.93 at depth 16 gives ~109k nodes/tree, the size
+    with probability split_p (0.985 at depth 16 gives ~110k nodes/tree, the size
     sklearn grows at 1M rows x depth 16 -- SURVEY §7.3.4).  Thresholds are uniform
     in scaled space; leaves are RF-style (mean value / n_trees)."""
     rng = np.random.default_rng(seed)

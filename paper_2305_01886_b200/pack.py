@@ -27,9 +27,9 @@ from .profiles import ArchProfile, latency_kind, resolve_signature
 GK_MAX_BP = 8
 NRES = 5
 
-TOKEN_DT = np.dtype({"names": ["res", "cls", "sig", "pred0"],
-                     "formats": ["u1", "u1", "<u2", "<u4"],
-                     "offsets": [0, 1, 2, 4], "itemsize": 8})
+TOKEN_DT = np.dtype({"names": ["res", "cls", "sig", "pred0", "lst_row", "lst_len"],
+                     "formats": ["u1", "u1", "<u2", "<u4", "<u2", "<u2"],
+                     "offsets": [0, 1, 2, 4, 8, 10], "itemsize": 16})
 BLOCK_DT = np.dtype({"names": ["mult", "tok0", "n", "fpred0", "n_fpred", "n_glob", "res_cnt",
                                "is_exit"],
                      "formats": ["<i8", "<u4", "<u4", "<u4", "<u2", "<u2", ("<u2", (5,)), "u1"],
@@ -52,7 +52,7 @@ _ARCH_FIELDS = [
     ("seg_icpt", ("<f8", (GK_MAX_BP + 1,))),
 ]
 ARCH_DT = np.dtype(_ARCH_FIELDS, align=True)
-assert TOKEN_DT.itemsize == 8 and BLOCK_DT.itemsize == 40 and KERNEL_DT.itemsize == 32
+assert TOKEN_DT.itemsize == 16 and BLOCK_DT.itemsize == 40 and KERNEL_DT.itemsize == 32
 assert ARCH_DT.itemsize == 488 and KSTAT_DT.itemsize == 64
 
 _FLAG_BRANCH, _FLAG_GLOAD, _FLAG_GSTORE = 0x04, 0x08, 0x10
@@ -111,7 +111,7 @@ class CorpusBuilder:
     def __init__(self):
         self._sig: dict = {}
         self.sigs: list = []
-        self._tok: list = []     # (res, cls, sig)
+        self._tok: list = []     # (res, cls, sig, lst_row, lst_len)
         self._pred_cnt: list = []
         self._preds: list = []
         self._blk: list = []
@@ -148,7 +148,13 @@ class CorpusBuilder:
             dfg = [[] for _ in range(n)]
             for u, v in blk.dfg_edges:
                 dfg[v].append(u)
+            if n > 65535:
+                raise ScheduleError("basic block longer than 65535 instructions")
             res_cnt = [0] * NRES
+            for inst in ins:
+                res_cnt[_code(inst.resource, RESOURCE_CODE)] += 1
+            res_row = [sum(res_cnt[:r]) for r in range(NRES)]
+            seen = [0] * NRES
             n_glob = 0
             t0 = len(self._tok)
             for i, inst in enumerate(ins):
@@ -164,8 +170,9 @@ class CorpusBuilder:
                         flags |= _FLAG_GLOAD
                     elif inst.root == "st":
                         flags |= _FLAG_GSTORE
-                res_cnt[rc] += 1
-                self._tok.append((rc, flags, self._sig_id(kl, inst.root, latency_kind(inst.suffixes))))
+                self._tok.append((rc, flags, self._sig_id(kl, inst.root, latency_kind(inst.suffixes)),
+                                  res_row[rc], seen[rc]))
+                seen[rc] += 1
                 ps = sorted(set(dfg[i]))
                 if any(p >= i or p < 0 for p in ps):
                     raise ScheduleError("DFG edge does not point forward inside its block")
@@ -190,6 +197,8 @@ class CorpusBuilder:
             tok["res"][:n_tok] = arr[:, 0]
             tok["cls"][:n_tok] = arr[:, 1]
             tok["sig"][:n_tok] = arr[:, 2]
+            tok["lst_row"][:n_tok] = arr[:, 3]
+            tok["lst_len"][:n_tok] = arr[:, 4]
         cnt = np.asarray(self._pred_cnt, dtype=np.int64)
         tok["pred0"][1:] = np.cumsum(cnt)
         blk = np.zeros(len(self._blk), BLOCK_DT)

@@ -22,7 +22,7 @@ from .pack import KSTAT_DT, Corpus, arch_records, config_array, latency_table
 LIB_PATH = Path(__file__).resolve().parent / "libgk.so"
 EXPORTS = ("gk_abi_version", "gk_last_error", "gk_device_sm_count", "gk_static_features",
            "gk_schedule_features", "gk_rf_predict", "gk_sweep_workspace_bytes",
-           "gk_predict_energy_sweep")
+           "gk_predict_energy_sweep", "gk_set_stage_timing", "gk_get_stage_ms")
 _lib = None
 
 
@@ -49,6 +49,8 @@ def load_library(path: Path | None = None):
     L.gk_sweep_workspace_bytes.argtypes = [vp, u32]
     L.gk_sweep_workspace_bytes.restype = C.c_size_t
     L.gk_predict_energy_sweep.argtypes = [vp, vp, vp, vp, u32, vp, vp, vp, vp, vp, vp]
+    L.gk_set_stage_timing.argtypes = [C.c_int]
+    L.gk_get_stage_ms.argtypes = [vp]
     if L.gk_abi_version() != 1:
         raise DeviceError("libgk ABI version mismatch")
     if path is None:
@@ -269,6 +271,18 @@ class Sweep:
         self.time_us = t.empty(n, dtype=t.float64, device=dev)
         self.power = t.empty(n, dtype=t.float64, device=dev)
         self.energy = t.empty(n, dtype=t.float64, device=dev)
+
+    def stage_ms(self, stream=None) -> dict:
+        """Run one sweep with per-stage CUDA events (synchronises); ms per stage."""
+        L = load_library()
+        L.gk_set_stage_timing(1)
+        try:
+            self.run(stream)
+            out = (C.c_float * 3)()
+            _check(L.gk_get_stage_ms(out))
+        finally:
+            L.gk_set_stage_timing(0)
+        return {"k1_static": out[0], "k23_schedule": out[1], "k4_rf_predict": out[2]}
 
     def run(self, stream=None):
         _check(load_library().gk_predict_energy_sweep(

@@ -21,10 +21,21 @@ SETS = ("c1", "c2", "rnd", "c5")
 
 
 def corpus_digest(c) -> str:
+    """Digest of the packed corpus's semantic fields (independent of record padding
+    and of derived fields), so a layout change does not invalidate the goldens."""
     h = hashlib.sha256()
-    for a in (c.tok, c.preds, c.blk, c.fpreds, c.topo, c.ker):
-        h.update(np.ascontiguousarray(a).tobytes())
-    h.update(json.dumps(c.sigs).encode())
+    t = c.tok
+    for f in ("res", "cls", "sig", "pred0"):
+        h.update(np.ascontiguousarray(t[f]).astype(np.int64).tobytes())
+    b = c.blk
+    for f in ("mult", "tok0", "n", "fpred0", "n_fpred", "n_glob", "res_cnt", "is_exit"):
+        h.update(np.ascontiguousarray(b[f]).astype(np.int64).tobytes())
+    k = c.ker
+    for f in ("blk0", "n_blk", "topo0", "max_n", "tok0", "n_tok"):
+        h.update(np.ascontiguousarray(k[f]).astype(np.int64).tobytes())
+    for a in (c.preds, c.fpreds, c.topo):
+        h.update(np.ascontiguousarray(a).astype(np.int64).tobytes())
+    h.update(json.dumps([list(s) for s in c.sigs]).encode())
     return h.hexdigest()
 
 

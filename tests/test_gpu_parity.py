@@ -184,10 +184,10 @@ def test_rf_fixture_ensembles_on_device():
 
     fx = fixtures()
     st = rt.DeviceEnsemble.upload(flatten(load_ensemble(fx["ensembles"]["stump"])))
-    p, _ = rt.rf_predict(st, torch.tensor([[256.0], [513.0], [512.0], [768.0]], device="cuda"))
+    p, _ = rt.rf_predict(st, torch.tensor([[256.0], [513.0], [512.0], [768.0]], dtype=torch.float64, device="cuda"))
     assert p.cpu().tolist() == [45.0, 55.0, 45.0, 55.0]
     cst = rt.DeviceEnsemble.upload(flatten(load_ensemble(fx["ensembles"]["constant"])))
-    p, _ = rt.rf_predict(cst, torch.tensor([[1024.0, 1.0]], device="cuda"))
+    p, _ = rt.rf_predict(cst, torch.tensor([[1024.0, 1.0]], dtype=torch.float64, device="cuda"))
     assert p.cpu().tolist() == [42.5]
 
 
