@@ -152,13 +152,16 @@ typedef struct {
 } gk_grid;
 
 /* Flattened tree ensemble (power.py:22-33).  Node = 16 B: for a split,
- * {threshold, feature, left} with right = left + 1; for a leaf, {value, -1, 0}.
- * Child indices are tree-local; trees are contiguous from tree_off[t]. */
+ * {threshold, feature, left} with right = left + 1; for a leaf,
+ * {value, -1, self} -- a leaf's `left` is its own index, so a fixed number of
+ * descent steps absorbs at the leaf.  Child indices are tree-local; trees are
+ * contiguous from tree_off[t]; tree_depth[t] is the depth of tree t. */
 typedef struct { double v; int32_t feature; int32_t left; } gk_node;
 
 typedef struct {
     const gk_node *nodes;
     const int64_t *tree_off;    /* n_trees                        */
+    const int32_t *tree_depth;  /* n_trees                        */
     const double  *scale_lo;    /* n_feat  (power.py:128-145)     */
     const double  *scale_hi;
     double   base_score;

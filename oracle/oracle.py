@@ -122,7 +122,8 @@ def schedule_features(hg: HostGrid, *, sel_idx=None, trace: bool = False, thread
 def rf_predict(flat, X, *, status=None, time_us=None, threads=None):
     X = np.ascontiguousarray(X, dtype=np.float64)
     n = X.shape[0]
-    keep = [flat.nodes, flat.tree_off, flat.scale_lo, flat.scale_hi]
+    keep = [flat.nodes, flat.tree_off, np.ascontiguousarray(flat.tree_depth, dtype=np.int32),
+            flat.scale_lo, flat.scale_hi]
     e = abi.GkEnsemble(*[_p(a) for a in keep], flat.base_score, flat.n_trees, flat.n_feat,
                        flat.max_depth)
     power = np.zeros(n)

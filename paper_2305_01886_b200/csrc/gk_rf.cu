@@ -91,41 +91,35 @@ __global__ void __launch_bounds__(kRfThreads) k4_rf_predict(RfArgs R) {
         const double lo = E.scale_lo[f], hi = E.scale_hi[f];
         x[f] = hi > lo ? __ddiv_rn(__dsub_rn(x[f], lo), __dsub_rn(hi, lo)) : 0.0;
     }
+    // Branch-free descent: kIlp trees in lock-step for max(depth) steps; a
+    // leaf's `left` is itself so finished walks stay put.  Same comparisons
+    // (x <= threshold goes left) and the same leaves as the reference walk.
     const gk_node *__restrict__ nodes = E.nodes;
     double total = E.base_score;
     uint32_t t = 0;
     for (; t + kIlp <= E.n_trees; t += kIlp) {
         const gk_node *base[kIlp];
         int32_t idx[kIlp];
-        double leaf[kIlp];
-        bool done[kIlp];
+        double v[kIlp];
+        int d = 0;
 #pragma unroll
         for (int q = 0; q < kIlp; q++) {
-            base[q] = nodes + E.tree_off[t + q];
+            base[q] = nodes + __ldg(E.tree_off + t + q);
             idx[q] = 0;
-            done[q] = false;
-            leaf[q] = 0.0;
+            d = max(d, __ldg(E.tree_depth + t + q));
         }
-        bool all = false;
-        while (!all) {
-            all = true;
+        for (int s = 0; s <= d; s++) {
 #pragma unroll
             for (int q = 0; q < kIlp; q++) {
-                if (!done[q]) {
-                    const double2 raw = __ldg(reinterpret_cast<const double2 *>(base[q] + idx[q]));
-                    const int2 fl = make_int2(__double2loint(raw.y), __double2hiint(raw.y));
-                    if (fl.x < 0) {
-                        leaf[q] = raw.x;
-                        done[q] = true;
-                    } else {
-                        idx[q] = x[fl.x] <= raw.x ? fl.y : fl.y + 1;
-                        all = false;
-                    }
-                }
+                const double2 raw = __ldg(reinterpret_cast<const double2 *>(base[q] + idx[q]));
+                const int f = __double2loint(raw.y), l = __double2hiint(raw.y);
+                v[q] = raw.x;
+                const bool left = f < 0 || x[f < 0 ? 0 : f] <= raw.x;
+                idx[q] = left ? l : l + 1;
             }
         }
 #pragma unroll
-        for (int q = 0; q < kIlp; q++) total = __dadd_rn(total, leaf[q]);  // tree order
+        for (int q = 0; q < kIlp; q++) total = __dadd_rn(total, v[q]);  // tree order
     }
     for (; t < E.n_trees; t++) {
         const gk_node *b = nodes + E.tree_off[t];

@@ -129,13 +129,18 @@ def load_ensemble(source) -> TreeEnsemble:
 class FlatEnsemble:
     """Device layout of one ensemble (host numpy arrays)."""
 
-    nodes: np.ndarray      # NODE_DT
+    nodes: np.ndarray      # NODE_DT; a leaf's `left` is its own index (absorbing)
     tree_off: np.ndarray   # int64 [n_trees]
     scale_lo: np.ndarray   # f64 [n_feat]
     scale_hi: np.ndarray
     base_score: float
     max_depth: int
     manifest: tuple
+    tree_depth: np.ndarray | None = None   # int32 [n_trees]
+
+    def __post_init__(self):
+        if self.tree_depth is None:
+            self.tree_depth = np.full(len(self.tree_off), self.max_depth, dtype=np.int32)
 
     @property
     def n_trees(self) -> int:
@@ -155,7 +160,7 @@ def _flatten_tree(nodes) -> tuple[np.ndarray, int]:
     while k < len(order):
         nd = nodes[order[k]]
         if "value" in nd:
-            out[k] = (float(nd["value"]), -1, 0)
+            out[k] = (float(nd["value"]), -1, k)   # absorbing leaf
         else:
             left = len(order)
             order.append(nd["left"])
@@ -172,19 +177,20 @@ def flatten(ens: TreeEnsemble) -> FlatEnsemble:
     cached = ens._flat.get("flat")
     if cached is not None:
         return cached
-    parts, offs, off, md = [], [], 0, 0
+    parts, offs, depths, off = [], [], [], 0
     for tree in ens.trees:
         arr, d = _flatten_tree(tree)
         parts.append(arr)
         offs.append(off)
+        depths.append(d)
         off += len(arr)
-        md = max(md, d)
-    nodes = np.concatenate(parts) if parts else np.zeros(1, NODE_DT)
+    nodes = np.concatenate(parts).astype(NODE_DT) if parts else np.zeros(1, NODE_DT)
     flat = FlatEnsemble(nodes=nodes, tree_off=np.asarray(offs, dtype=np.int64),
                         scale_lo=np.asarray(ens.scale_min, dtype=np.float64),
                         scale_hi=np.asarray(ens.scale_max, dtype=np.float64),
-                        base_score=float(ens.base_score), max_depth=md,
-                        manifest=tuple(ens.feature_manifest))
+                        base_score=float(ens.base_score), max_depth=max(depths, default=0),
+                        manifest=tuple(ens.feature_manifest),
+                        tree_depth=np.asarray(depths, dtype=np.int32))
     ens._flat["flat"] = flat
     return flat
 
@@ -199,7 +205,7 @@ def random_forest_flat(n_trees: int, depth: int, manifest, scale_lo, scale_hi, s
     rng = np.random.default_rng(seed)
     nf = len(manifest)
     scale = (1.0 / n_trees) if leaf_scale is None else leaf_scale
-    parts, offs, off = [], [], 0
+    parts, offs, depths, off = [], [], [], 0
     for _ in range(n_trees):
         level_n = 1
         levels = []
@@ -224,15 +230,19 @@ def random_forest_flat(n_trees: int, depth: int, manifest, scale_lo, scale_hi, s
             arr["left"][sp] = nxt + 2 * np.arange(len(sp))
             lf = idx[~split]
             arr["feature"][lf] = -1
+            arr["left"][lf] = lf                      # absorbing leaf
             arr["v"][lf] = (30.0 + 120.0 * rng.random(len(lf))) * scale
             base = nxt
         parts.append(arr)
         offs.append(off)
+        depths.append(len(levels) - 1)
         off += n_nodes
-    return FlatEnsemble(nodes=np.concatenate(parts), tree_off=np.asarray(offs, dtype=np.int64),
+    return FlatEnsemble(nodes=np.concatenate(parts).astype(NODE_DT),
+                        tree_off=np.asarray(offs, dtype=np.int64),
                         scale_lo=np.asarray(scale_lo, dtype=np.float64),
                         scale_hi=np.asarray(scale_hi, dtype=np.float64), base_score=0.0,
-                        max_depth=depth, manifest=tuple(manifest))
+                        max_depth=max(depths), manifest=tuple(manifest),
+                        tree_depth=np.asarray(depths, dtype=np.int32))
 
 
 def flat_to_document(flat: FlatEnsemble) -> dict:

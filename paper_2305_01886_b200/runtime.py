@@ -172,11 +172,13 @@ class DeviceEnsemble:
             # zero-tree ensembles (reference fixture ensemble_constant.json) keep one dummy node
             pass
         de = cls(flat)
-        de.bufs = {"nodes": _dev(flat.nodes), "off": _dev(flat.tree_off if flat.n_trees
-                                                         else np.zeros(1, np.int64)),
+        de.bufs = {"nodes": _dev(flat.nodes),
+                   "off": _dev(flat.tree_off if flat.n_trees else np.zeros(1, np.int64)),
+                   "depth": _dev(flat.tree_depth if flat.n_trees else np.zeros(1, np.int32)),
                    "lo": _dev(flat.scale_lo), "hi": _dev(flat.scale_hi)}
         b = de.bufs
-        de.desc = abi.GkEnsemble(_ptr(b["nodes"]), _ptr(b["off"]), _ptr(b["lo"]), _ptr(b["hi"]),
+        de.desc = abi.GkEnsemble(_ptr(b["nodes"]), _ptr(b["off"]), _ptr(b["depth"]),
+                                 _ptr(b["lo"]), _ptr(b["hi"]),
                                  float(flat.base_score), flat.n_trees, flat.n_feat,
                                  flat.max_depth)
         return de
