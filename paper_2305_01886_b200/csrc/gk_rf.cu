@@ -86,11 +86,17 @@ __global__ void __launch_bounds__(kRfThreads) k4_rf_predict(RfArgs R) {
         if (R.energy) R.energy[row] = NaN;
         return;
     }
-    double *x = xs + (size_t)threadIdx.x * nf;
+    // scale and transpose to [feature][thread]: the per-visit reads x[f] with a
+    // lane-varying f are then bank-conflict-free
+    double *xr = xs + (size_t)threadIdx.x * nf;
+    double *xt = xs + (size_t)kRfThreads * nf;
     for (uint32_t f = 0; f < nf; f++) {
         const double lo = E.scale_lo[f], hi = E.scale_hi[f];
-        x[f] = hi > lo ? __ddiv_rn(__dsub_rn(x[f], lo), __dsub_rn(hi, lo)) : 0.0;
+        xt[f * kRfThreads + threadIdx.x] =
+            hi > lo ? __ddiv_rn(__dsub_rn(xr[f], lo), __dsub_rn(hi, lo)) : 0.0;
     }
+    const double *x = xt + threadIdx.x;
+#define XF(f) x[(size_t)(f) * kRfThreads]
     // Branch-free descent: kIlp trees in lock-step for max(depth) steps; a
     // leaf's `left` is itself so finished walks stay put.  Same comparisons
     // (x <= threshold goes left) and the same leaves as the reference walk.
@@ -114,7 +120,7 @@ __global__ void __launch_bounds__(kRfThreads) k4_rf_predict(RfArgs R) {
                 const double2 raw = __ldg(reinterpret_cast<const double2 *>(base[q] + idx[q]));
                 const int f = __double2loint(raw.y), l = __double2hiint(raw.y);
                 v[q] = raw.x;
-                const bool left = f < 0 || x[f < 0 ? 0 : f] <= raw.x;
+                const bool left = f < 0 || XF(f < 0 ? 0 : f) <= raw.x;
                 idx[q] = left ? l : l + 1;
             }
         }
@@ -131,9 +137,10 @@ __global__ void __launch_bounds__(kRfThreads) k4_rf_predict(RfArgs R) {
                 total = __dadd_rn(total, raw.x);
                 break;
             }
-            i = x[f] <= raw.x ? l : l + 1;
+            i = XF(f) <= raw.x ? l : l + 1;
         }
     }
+#undef XF
     R.power[row] = total;
     if (R.energy) R.energy[row] = __dmul_rn(total, R.time_us[row]);
 }
@@ -172,7 +179,7 @@ int gk_launch_rf(const gk_ensemble *ens, uint32_t n_ens, const double *X, int64_
     R.energy = energy;
     R.n_cfg = n_cfg;
     R.n_arch = n_arch ? n_arch : 1;
-    const size_t smem = (size_t)gk::kRfThreads * nf * sizeof(double);
+    const size_t smem = 2 * (size_t)gk::kRfThreads * nf * sizeof(double);  // tile + transposed
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(gk::k4_rf_predict, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);

@@ -224,11 +224,27 @@ __device__ __forceinline__ double schedule_block(const gk_corpus &C, const gk_bl
             }
         }
         double t = ready;
-        for (; k < L; k++) {
-            const double s = ROW(m.ss, base + k), e = ROW(m.se, base + k);
-            if (e <= t) continue;
-            if (s >= __dadd_rn(t, len)) break;
-            t = e;
+        // 4 spans per iteration: independent loads, then the reference's
+        // sequential decisions in registers
+        bool hit = false;
+        for (; k < L && !hit; k += 4) {
+            double s4[4], e4[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const bool in = k + u < L;
+                s4[u] = in ? ROW(m.ss, base + k + u) : 0.0;
+                e4[u] = in ? ROW(m.se, base + k + u) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                if (hit || k + u >= L) continue;
+                if (e4[u] <= t) continue;
+                if (s4[u] >= __dadd_rn(t, len)) {
+                    hit = true;
+                    continue;
+                }
+                t = e4[u];
+            }
         }
         const double start = t;
         const double fin = __dadd_rn(start, d);
@@ -647,8 +663,15 @@ int gk_launch_sched(const gk_corpus *C, const gk_grid *G, const gk_kstat *ks, co
                              (int)smem);
     }
     // the reservation tables that do not fit the shared slab live in L1: prefer L1
-    cudaFuncSetAttribute(gk::k23_schedule, cudaFuncAttributePreferredSharedMemoryCarveout,
-                         ns == 0 ? 0 : -1);
+    // (a 0% carveout caps resident CTAs at 5/SM even for ~1 KB of tables: ask
+    // for just enough shared memory for the register-limited CTA count)
+    {
+        const size_t per_sm_bytes = (smem + 1024) * 8;
+        int carve = (int)((per_sm_bytes * 100 + 228 * 1024 - 1) / (228 * 1024));
+        if (carve > 100) carve = 100;
+        cudaFuncSetAttribute(gk::k23_schedule, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             carve);
+    }
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gk::k23_schedule, gk::kWarps * 32, smem);
     if (per_sm < 1) {
