@@ -16,7 +16,10 @@
 namespace gk {
 
 constexpr int kRfThreads = 128;
-constexpr int kIlp = 4;
+#ifndef GK_RF_ILP
+#define GK_RF_ILP 4
+#endif
+constexpr int kIlp = GK_RF_ILP;
 constexpr int kMaxFeat = 64;
 
 struct RfArgs {

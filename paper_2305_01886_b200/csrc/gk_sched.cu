@@ -21,6 +21,12 @@
 namespace gk {
 
 constexpr int kWarps = 4;            // warps per CTA (each warp: 32 points of one kernel)
+#ifndef GK_SCAN_UNROLL
+#define GK_SCAN_UNROLL 4
+#endif
+#ifndef GK_K23_CARVE
+#define GK_K23_CARVE -2  // -2: just enough shared memory for the resident CTAs
+#endif
 
 // ------------------------------------------------------------------ K1
 
@@ -224,19 +230,19 @@ __device__ __forceinline__ double schedule_block(const gk_corpus &C, const gk_bl
             }
         }
         double t = ready;
-        // 4 spans per iteration: independent loads, then the reference's
-        // sequential decisions in registers
+        // GK_SCAN_UNROLL spans per iteration: independent loads, then the
+        // reference's sequential decisions in registers
         bool hit = false;
-        for (; k < L && !hit; k += 4) {
-            double s4[4], e4[4];
+        for (; k < L && !hit; k += GK_SCAN_UNROLL) {
+            double s4[GK_SCAN_UNROLL], e4[GK_SCAN_UNROLL];
 #pragma unroll
-            for (int u = 0; u < 4; u++) {
+            for (int u = 0; u < GK_SCAN_UNROLL; u++) {
                 const bool in = k + u < L;
                 s4[u] = in ? ROW(m.ss, base + k + u) : 0.0;
                 e4[u] = in ? ROW(m.se, base + k + u) : 0.0;
             }
 #pragma unroll
-            for (int u = 0; u < 4; u++) {
+            for (int u = 0; u < GK_SCAN_UNROLL; u++) {
                 if (hit || k + u >= L) continue;
                 if (e4[u] <= t) continue;
                 if (s4[u] >= __dadd_rn(t, len)) {
@@ -669,8 +675,10 @@ int gk_launch_sched(const gk_corpus *C, const gk_grid *G, const gk_kstat *ks, co
         const size_t per_sm_bytes = (smem + 1024) * 8;
         int carve = (int)((per_sm_bytes * 100 + 228 * 1024 - 1) / (228 * 1024));
         if (carve > 100) carve = 100;
-        cudaFuncSetAttribute(gk::k23_schedule, cudaFuncAttributePreferredSharedMemoryCarveout,
-                             carve);
+        if (GK_K23_CARVE >= 0) carve = GK_K23_CARVE;
+        if (GK_K23_CARVE != -1)
+            cudaFuncSetAttribute(gk::k23_schedule, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 carve);
     }
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gk::k23_schedule, gk::kWarps * 32, smem);
