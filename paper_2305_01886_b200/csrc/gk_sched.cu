@@ -25,7 +25,9 @@ constexpr int kWarps = 4;            // warps per CTA (each warp: 32 points of o
 #define GK_SCAN_UNROLL 4
 #endif
 #ifndef GK_K23_CARVE
-#define GK_K23_CARVE -2  // -2: just enough shared memory for the resident CTAs
+// measured (tools/sweep_variants.sh, B200): 0% carveout (max L1 for the
+// reservation tables) beats a carveout sized for more resident CTAs
+#define GK_K23_CARVE 0  // >= 0: percent; -1: driver default; -2: just enough for the CTAs
 #endif
 
 // ------------------------------------------------------------------ K1
