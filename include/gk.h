@@ -222,6 +222,42 @@ int gk_predict_energy_sweep(const gk_corpus *corpus, const gk_grid *grid,
 /* Profiling aid: when enabled, gk_predict_energy_sweep records CUDA events
  * between its K1 / K2+K3 / K4 launches; gk_get_stage_ms waits for the last
  * sweep and returns the three stage durations in ms. */
+/* ---- K5: random-forest training (replaces RandomForestRegressor.fit as built by
+ * gpukalc_trainer.training._make_model, training.py:73-76; sklearn internals
+ * SK/ensemble/_forest.py:95-175, SK/tree/_splitter.pyx).  Host driver:
+ * paper_2305_01886_b200/forest.py.  Task / split records:
+ *   task  = {int32 tree, begin, end, parity}   (row segment in rows0/rows1)
+ *   split = {int32 feat (-1: leaf), bin, n_left, pad; double proxy} */
+
+/* counts[t][i] = bincount(RandomState(tree_seeds[t]).randint(0, n, n))[i] */
+int gk_rf_bootstrap(const uint32_t *tree_seeds, uint32_t n_trees, int64_t n_rows,
+                    uint32_t *counts, void *stream);
+/* rows[tree_base[t] ..] = indices i with counts[t][i] > 0 (fill[t] = how many) */
+int gk_rf_compact(const uint32_t *counts, uint32_t n_trees, int64_t n_rows,
+                  const int64_t *tree_base, int32_t *rows, int32_t *fill, void *stream);
+/* Xb[i][f] = #{edges[f][j] < float32(X[i][f])}; per-bin min/max (order-mapped) */
+int gk_rf_bin(const double *X, int64_t n_rows, int32_t n_feat, int64_t ld, const float *edges,
+              const int32_t *n_edges, uint8_t *Xb, uint32_t *bin_min, uint32_t *bin_max,
+              void *stream);
+/* best split of every task (small / medium / big index lists) */
+int gk_rf_split_level(const uint8_t *Xb, const int64_t *yfp, const double *y,
+                      const uint32_t *counts, int64_t n_rows, int32_t n_feat,
+                      const void *tasks, const int32_t *small_ids, int32_t n_small,
+                      const int32_t *med_ids, int32_t n_med, const int32_t *big_ids,
+                      int32_t n_big, int32_t big_max_chunks, const int32_t *rows0,
+                      const int32_t *rows1, void *hist_ws, void *split_out, void *stream);
+size_t gk_rf_hist_bytes(int32_t n_big, int32_t n_feat);
+/* move each split task's rows to [begin, begin+n_left) / [.., end) of the other buffer */
+int gk_rf_partition(const uint8_t *Xb, const int64_t *yfp, const double *y,
+                    const uint32_t *counts, int64_t n_rows, int32_t n_feat, const void *tasks,
+                    int32_t n_tasks, const void *split, const int32_t *ids, int32_t n_ids,
+                    int32_t max_rows, int32_t *rows0, int32_t *rows1, int32_t *cursor,
+                    void *stream);
+/* per leaf segment: {n, sum w, sum w*y, sum w*y^2} (fixed reduction order) */
+int gk_rf_leaf_stats(const uint32_t *counts, int64_t n_rows, const double *y, const void *leaves,
+                     int32_t n_leaves, const int32_t *rows0, const int32_t *rows1, double *out,
+                     void *stream);
+
 int gk_set_stage_timing(int on);
 int gk_get_stage_ms(float *out3);
 

@@ -20,7 +20,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libgk.so"
-SOURCES = ["gk_api.cu", "gk_sched.cu", "gk_rf.cu"]
+SOURCES = ["gk_api.cu", "gk_sched.cu", "gk_rf.cu", "gk_rftrain.cu"]
 HEADERS = ["gk_internal.cuh", "gk_exp.h", "gk_exp_table.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ["-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",

@@ -1,0 +1,665 @@
+// gk_rftrain.cu -- K5: random-forest training (RandomForestRegressor.fit as
+// wrapped by gpukalc_trainer.training._make_model, training.py:73-76).
+//
+// Reference semantics (scikit-learn):
+//  * bootstrap: counts = bincount(RandomState(tree_seed).randint(0, n, n))
+//    (SK/ensemble/_forest.py:95-112, 150-156) -- reproduced bit-exactly here
+//    with one MT19937 stream per tree (warp-parallel twist) and numpy's masked
+//    rejection for bounded integers;
+//  * squared-error trees, all features per split, min_samples_split = 2,
+//    min_samples_leaf = 1, leaf value = weighted mean.
+// Split search is histogram-based over u8 feature bins (quantile edges, one
+// bin per distinct value when a feature has <= 256 of them), so trees are not
+// identical to sklearn's exact float32 midpoints -- the parity bar for training
+// is R^2 / MAPE (BASELINE.json).  Sums of w*y use 64-bit fixed point, so split
+// decisions are deterministic despite atomics.
+//
+// Level-wise growth over a batch of trees; a "task" is one node to split:
+//   rows <= 64       -> one warp, all-pairs prefix sums (k5_split_small)
+//   rows <= kMedRows -> one CTA, shared-memory histograms per 16-feature chunk
+//   larger           -> row-chunked CTAs accumulate global histograms, then
+//                       one CTA per task evaluates (k5_hist_big + k5_eval_big)
+#include "gk_internal.cuh"
+
+namespace gk {
+
+constexpr int kFC = 16;          // features per histogram chunk
+constexpr int kBins = 256;
+constexpr int kMedRows = 32768;  // larger nodes use the multi-CTA histogram path
+constexpr int kSmallRows = 64;
+
+struct RfTrainData {
+    const uint8_t *Xb;      // [n][F] bins
+    const int64_t *yfp;     // [n] y in fixed point
+    const double *y;        // [n]
+    const uint32_t *counts; // [n_trees][n] bootstrap counts
+    int64_t n;
+    int32_t F;
+};
+
+struct RfTask {             // one node to split (or one leaf to summarise)
+    int32_t tree, begin, end, parity;
+};
+
+struct RfSplit {
+    int32_t feat, bin, n_left, pad;
+    double proxy;
+};
+
+// ---------------------------------------------------------------- bootstrap
+
+// One warp per tree: MT19937 (init_genrand(seed)), tempering, numpy's masked
+// rejection for randint(0, n) (mask = 2^bitlen(n-1) - 1, accept v <= n-1),
+// counts[v] += 1 for the first n accepted draws.
+__global__ void __launch_bounds__(128) k5_bootstrap(const uint32_t *__restrict__ seeds,
+                                                    int n_trees, int64_t n,
+                                                    uint32_t *__restrict__ counts) {
+    __shared__ uint32_t mt_s[4][624];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int t = blockIdx.x * 4 + w;
+    if (t >= n_trees) return;
+    uint32_t *mt = mt_s[w];
+    uint32_t *cnt = counts + (size_t)t * n;
+    const uint32_t rng = (uint32_t)(n - 1);
+    if (rng == 0) {
+        if (lane == 0) cnt[0] = (uint32_t)n;
+        return;
+    }
+    uint32_t mask = rng;
+    mask |= mask >> 1; mask |= mask >> 2; mask |= mask >> 4; mask |= mask >> 8; mask |= mask >> 16;
+    if (lane == 0) {
+        mt[0] = seeds[t];
+        for (int i = 1; i < 624; i++) mt[i] = 1812433253u * (mt[i - 1] ^ (mt[i - 1] >> 30)) + (uint32_t)i;
+    }
+    __syncwarp();
+    int64_t accepted = 0;
+    auto twist = [&](int k) {
+        const uint32_t y = (mt[k] & 0x80000000u) | (mt[(k + 1) % 624] & 0x7fffffffu);
+        return mt[(k + 397) % 624] ^ (y >> 1) ^ ((y & 1u) ? 0x9908b0dfu : 0u);
+    };
+    while (accepted < n) {
+        // twist in three dependency phases: [0,227) old operands, [227,454)
+        // needs phase-1 results, [454,623) needs phase-2, 623 needs mt[0] new
+        for (int k = lane; k < 227; k += 32) {
+            const uint32_t v = twist(k);
+            __syncwarp(__activemask());
+            mt[k] = v;
+        }
+        __syncwarp();
+        for (int k = 227 + lane; k < 454; k += 32) {
+            const uint32_t v = twist(k);
+            __syncwarp(__activemask());
+            mt[k] = v;
+        }
+        __syncwarp();
+        for (int k = 454 + lane; k < 623; k += 32) {
+            const uint32_t v = twist(k);
+            __syncwarp(__activemask());
+            mt[k] = v;
+        }
+        __syncwarp();
+        if (lane == 0) mt[623] = twist(623);
+        __syncwarp();
+        for (int k0 = 0; k0 < 624 && accepted < n; k0 += 32) {
+            const int k = k0 + lane;
+            uint32_t y = k < 624 ? mt[k] : 0u;
+            y ^= y >> 11;
+            y ^= (y << 7) & 0x9d2c5680u;
+            y ^= (y << 15) & 0xefc60000u;
+            y ^= y >> 18;
+            const uint32_t v = y & mask;
+            const bool ok = k < 624 && v <= rng;
+            const unsigned bal = __ballot_sync(GK_FULL, ok);
+            const int before = __popc(bal & ((1u << lane) - 1u));
+            if (ok && accepted + before < n) atomicAdd(cnt + v, 1u);
+            accepted += __popc(bal);
+        }
+        __syncwarp();
+    }
+}
+
+// rows with count > 0, per tree, compacted (order within a tree is not kept)
+__global__ void k5_compact(const uint32_t *__restrict__ counts, int n_trees, int64_t n,
+                           const int64_t *__restrict__ tree_base, int32_t *__restrict__ rows,
+                           int32_t *__restrict__ fill) {
+    const int t = blockIdx.y;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool in = i < n && counts[(size_t)t * n + i] > 0;
+    const unsigned bal = __ballot_sync(GK_FULL, in);
+    if (!bal) return;
+    const int lane = threadIdx.x & 31;
+    int base = 0;
+    if (lane == __ffs(bal) - 1) base = atomicAdd(fill + t, __popc(bal));
+    base = __shfl_sync(GK_FULL, base, __ffs(bal) - 1);
+    if (in) rows[tree_base[t] + base + __popc(bal & ((1u << lane) - 1u))] = (int32_t)i;
+}
+
+// ---------------------------------------------------------------- binning
+
+__device__ __forceinline__ uint32_t f2ord(float f) {  // order-preserving float -> uint
+    const uint32_t u = __float_as_uint(f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+// Xb[r][f] = #edges < float32(X[r][f]); per-bin min/max of the float32 values
+__global__ void k5_bin(const double *__restrict__ X, int64_t n, int F, int64_t ld,
+                       const float *__restrict__ edges, const int32_t *__restrict__ n_edges,
+                       uint8_t *__restrict__ Xb, uint32_t *__restrict__ bmin,
+                       uint32_t *__restrict__ bmax) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n * F) return;
+    const int64_t r = i / F;
+    const int f = (int)(i % F);
+    const float v = (float)X[r * ld + f];  // sklearn fits on float32 X
+    const float *e = edges + (size_t)f * (kBins - 1);
+    int lo = 0, hi = n_edges[f];
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (e[mid] < v) lo = mid + 1;
+        else hi = mid;
+    }
+    Xb[i] = (uint8_t)lo;
+    const uint32_t o = f2ord(v);
+    atomicMin(bmin + f * kBins + lo, o);
+    atomicMax(bmax + f * kBins + lo, o);
+}
+
+// ------------------------------------------------------------ split search
+
+struct BestSplit {
+    double proxy;
+    int feat, bin;
+    uint32_t n_left;
+};
+
+__device__ __forceinline__ bool better(double p, int f, int b, const BestSplit &o) {
+    return p > o.proxy || (p == o.proxy && (f < o.feat || (f == o.feat && b < o.bin)));
+}
+
+// Evaluate all boundaries of one feature's histogram with one warp:
+// left = bins <= b; proxy = S_L^2 / W_L + S_R^2 / W_R (sklearn's MSE proxy).
+__device__ __forceinline__ BestSplit eval_feature(const uint64_t *cw, const int64_t *s, int f,
+                                                  int lane) {
+    uint64_t c8[8];
+    int64_t s8[8];
+    uint64_t cacc = 0;
+    int64_t sacc = 0;
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+        cacc += cw[lane * 8 + j];
+        sacc += s[lane * 8 + j];
+        c8[j] = cacc;
+        s8[j] = sacc;
+    }
+    // exclusive warp scan of the per-lane totals
+    uint64_t cpre = cacc;
+    int64_t spre = sacc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t a = __shfl_up_sync(GK_FULL, cpre, o);
+        const int64_t b = __shfl_up_sync(GK_FULL, spre, o);
+        if (lane >= o) {
+            cpre += a;
+            spre += b;
+        }
+    }
+    const uint64_t ctot = __shfl_sync(GK_FULL, cpre, 31);
+    const int64_t stot = __shfl_sync(GK_FULL, spre, 31);
+    cpre -= cacc;
+    spre -= sacc;
+    const uint32_t C = (uint32_t)(ctot >> 32), W = (uint32_t)ctot;
+    BestSplit best{-1.0, 0x7fffffff, 0x7fffffff, 0};
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+        const int b = lane * 8 + j;
+        if (b >= kBins - 1) continue;
+        const uint64_t cl = cpre + c8[j];
+        const uint32_t CL = (uint32_t)(cl >> 32), WL = (uint32_t)cl;
+        if (CL < 1 || C - CL < 1) continue;
+        const double SL = (double)(spre + s8[j]), SR = (double)(stot - spre - s8[j]);
+        const double p = SL * SL / (double)WL + SR * SR / (double)(W - WL);
+        if (better(p, f, b, best)) best = BestSplit{p, f, b, CL};
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        BestSplit q;
+        q.proxy = __shfl_xor_sync(GK_FULL, best.proxy, o);
+        q.feat = __shfl_xor_sync(GK_FULL, best.feat, o);
+        q.bin = __shfl_xor_sync(GK_FULL, best.bin, o);
+        q.n_left = __shfl_xor_sync(GK_FULL, best.n_left, o);
+        if (better(q.proxy, q.feat, q.bin, best)) best = q;
+    }
+    return best;
+}
+
+// parent proxy S^2/W: a split must improve on it (else the node is pure)
+__device__ __forceinline__ void finish_split(const BestSplit &b, double parent, RfSplit *out) {
+    RfSplit r;
+    const bool ok = b.feat != 0x7fffffff && b.proxy > parent + 1e-12 * fabs(parent);
+    r.feat = ok ? b.feat : -1;
+    r.bin = ok ? b.bin : 0;
+    r.n_left = ok ? (int32_t)b.n_left : 0;
+    r.pad = 0;
+    r.proxy = ok ? b.proxy : 0.0;
+    *out = r;
+}
+
+struct HistSmem {
+    uint64_t cw[kFC][kBins];   // (count << 32) | weight
+    int64_t s[kFC][kBins];     // sum of w * y (fixed point)
+    BestSplit best[8];
+    double parent;
+};
+
+// add one task's rows [p0, p1) to the shared histograms of feature chunk fc
+__device__ __forceinline__ void accumulate(HistSmem &H, const RfTrainData &D, const RfTask &T,
+                                           const int32_t *__restrict__ rows, int p0, int p1,
+                                           int fc) {
+    const int f0 = fc * kFC, nf = min(kFC, D.F - f0);
+    const uint32_t *cnt = D.counts + (size_t)T.tree * D.n;
+    for (int p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
+        const int32_t r = rows[p];
+        const uint32_t w = cnt[r];
+        const uint64_t cw = (1ull << 32) | w;
+        const int64_t sv = (int64_t)w * D.yfp[r];
+        const uint8_t *xb = D.Xb + (size_t)r * D.F + f0;
+        for (int j = 0; j < nf; j++) {
+            const int b = xb[j];
+            atomicAdd((unsigned long long *)&H.cw[j][b], (unsigned long long)cw);
+            atomicAdd((unsigned long long *)&H.s[j][b], (unsigned long long)sv);
+        }
+    }
+}
+
+__device__ __forceinline__ void zero_hist(HistSmem &H) {
+    uint64_t *a = &H.cw[0][0];
+    int64_t *b = &H.s[0][0];
+    for (int i = threadIdx.x; i < kFC * kBins; i += blockDim.x) {
+        a[i] = 0;
+        b[i] = 0;
+    }
+}
+
+// evaluate the kFC features in shared memory; fold into H.best[warp]
+__device__ __forceinline__ void eval_chunk(HistSmem &H, int F, int fc, BestSplit &mine) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    for (int j = warp; j < kFC; j += nwarps) {
+        const int f = fc * kFC + j;
+        if (f >= F) break;
+        const BestSplit b = eval_feature(H.cw[j], H.s[j], f, lane);
+        if (better(b.proxy, b.feat, b.bin, mine)) mine = b;
+    }
+}
+
+__device__ __forceinline__ void reduce_best(HistSmem &H, BestSplit mine, RfSplit *out) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    if (lane == 0) H.best[warp] = mine;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        BestSplit b = H.best[0];
+        for (int w = 1; w < nwarps; w++)
+            if (better(H.best[w].proxy, H.best[w].feat, H.best[w].bin, b)) b = H.best[w];
+        finish_split(b, H.parent, out);
+    }
+}
+
+__device__ __forceinline__ void parent_proxy(HistSmem &H) {
+    // totals from feature 0's histogram (every row lands in exactly one bin)
+    if (threadIdx.x < 32) {
+        uint64_t c = 0;
+        int64_t s = 0;
+        for (int b = threadIdx.x; b < kBins; b += 32) {
+            c += H.cw[0][b];
+            s += H.s[0][b];
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            c += __shfl_xor_sync(GK_FULL, c, o);
+            s += __shfl_xor_sync(GK_FULL, s, o);
+        }
+        if (threadIdx.x == 0) {
+            const double S = (double)s;
+            H.parent = S * S / (double)(uint32_t)c;
+        }
+    }
+}
+
+// medium tasks: one CTA per task, feature chunks in sequence
+__global__ void __launch_bounds__(256) k5_split_medium(RfTrainData D, const RfTask *__restrict__ tasks,
+                                                       const int32_t *__restrict__ task_ids,
+                                                       const int32_t *__restrict__ rows0,
+                                                       const int32_t *__restrict__ rows1,
+                                                       RfSplit *__restrict__ out) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    HistSmem &H = *reinterpret_cast<HistSmem *>(smem_raw);
+    const int ti = task_ids[blockIdx.x];
+    const RfTask T = tasks[ti];
+    const int32_t *rows = T.parity ? rows1 : rows0;
+    BestSplit mine{-1.0, 0x7fffffff, 0x7fffffff, 0};
+    const int n_fc = (D.F + kFC - 1) / kFC;
+    for (int fc = 0; fc < n_fc; fc++) {
+        zero_hist(H);
+        __syncthreads();
+        accumulate(H, D, T, rows, T.begin, T.end, fc);
+        __syncthreads();
+        if (fc == 0) parent_proxy(H);
+        eval_chunk(H, D.F, fc, mine);
+        __syncthreads();
+    }
+    reduce_best(H, mine, out + ti);
+}
+
+// big tasks: CTA = (task, row chunk, feature chunk) -> global histograms
+__global__ void __launch_bounds__(256) k5_hist_big(RfTrainData D, const RfTask *__restrict__ tasks,
+                                                   const int32_t *__restrict__ task_ids,
+                                                   const int32_t *__restrict__ rows0,
+                                                   const int32_t *__restrict__ rows1,
+                                                   uint64_t *__restrict__ gcw,
+                                                   int64_t *__restrict__ gs) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    HistSmem &H = *reinterpret_cast<HistSmem *>(smem_raw);
+    const int bi = blockIdx.z;           // index among big tasks
+    const RfTask T = tasks[task_ids[bi]];
+    const int32_t *rows = T.parity ? rows1 : rows0;
+    const int fc = blockIdx.y;
+    const int p0 = T.begin + blockIdx.x * kMedRows;
+    if (p0 >= T.end) return;
+    const int p1 = min(T.end, p0 + kMedRows);
+    zero_hist(H);
+    __syncthreads();
+    accumulate(H, D, T, rows, p0, p1, fc);
+    __syncthreads();
+    const int f0 = fc * kFC, nf = min(kFC, D.F - f0);
+    uint64_t *dcw = gcw + ((size_t)bi * D.F + f0) * kBins;
+    int64_t *ds = gs + ((size_t)bi * D.F + f0) * kBins;
+    for (int i = threadIdx.x; i < nf * kBins; i += blockDim.x) {
+        const uint64_t c = (&H.cw[0][0])[i];
+        if (c) {
+            atomicAdd((unsigned long long *)(dcw + i), (unsigned long long)c);
+            atomicAdd((unsigned long long *)(ds + i), (unsigned long long)(&H.s[0][0])[i]);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k5_eval_big(RfTrainData D, const int32_t *__restrict__ task_ids,
+                                                   const uint64_t *__restrict__ gcw,
+                                                   const int64_t *__restrict__ gs,
+                                                   RfSplit *__restrict__ out) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    HistSmem &H = *reinterpret_cast<HistSmem *>(smem_raw);
+    const int bi = blockIdx.x;
+    BestSplit mine{-1.0, 0x7fffffff, 0x7fffffff, 0};
+    const int n_fc = (D.F + kFC - 1) / kFC;
+    for (int fc = 0; fc < n_fc; fc++) {
+        const int f0 = fc * kFC, nf = min(kFC, D.F - f0);
+        const uint64_t *scw = gcw + ((size_t)bi * D.F + f0) * kBins;
+        const int64_t *ss = gs + ((size_t)bi * D.F + f0) * kBins;
+        for (int i = threadIdx.x; i < kFC * kBins; i += blockDim.x) {
+            (&H.cw[0][0])[i] = i < nf * kBins ? scw[i] : 0;
+            (&H.s[0][0])[i] = i < nf * kBins ? ss[i] : 0;
+        }
+        __syncthreads();
+        if (fc == 0) parent_proxy(H);
+        eval_chunk(H, D.F, fc, mine);
+        __syncthreads();
+    }
+    reduce_best(H, mine, out + task_ids[bi]);
+}
+
+// small tasks (<= 64 rows): one warp; per feature, each lane's keys are
+// evaluated against all rows (prefix sums by broadcast)
+__global__ void __launch_bounds__(128) k5_split_small(RfTrainData D, const RfTask *__restrict__ tasks,
+                                                     const int32_t *__restrict__ task_ids,
+                                                     int n_ids, const int32_t *__restrict__ rows0,
+                                                     const int32_t *__restrict__ rows1,
+                                                     RfSplit *__restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int wi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (wi >= n_ids) return;
+    const int ti = task_ids[wi];
+    const RfTask T = tasks[ti];
+    const int32_t *rows = T.parity ? rows1 : rows0;
+    const int m = T.end - T.begin;
+    const uint32_t *cnt = D.counts + (size_t)T.tree * D.n;
+    int32_t r[2];
+    uint32_t w[2];
+    int64_t s[2];
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+        const int i = lane + 32 * h;
+        r[h] = i < m ? rows[T.begin + i] : -1;
+        w[h] = i < m ? cnt[r[h]] : 0u;
+        s[h] = i < m ? (int64_t)w[h] * D.yfp[r[h]] : 0;
+    }
+    // totals
+    uint32_t W = w[0] + w[1];
+    int64_t S = s[0] + s[1];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        W += __shfl_xor_sync(GK_FULL, W, o);
+        S += __shfl_xor_sync(GK_FULL, S, o);
+    }
+    const double parent = (double)S * (double)S / (double)W;
+    BestSplit best{-1.0, 0x7fffffff, 0x7fffffff, 0};
+    for (int f = 0; f < D.F; f++) {
+        int k[2];
+#pragma unroll
+        for (int h = 0; h < 2; h++) k[h] = r[h] >= 0 ? D.Xb[(size_t)r[h] * D.F + f] : 1 << 20;
+        uint32_t cl[2] = {0, 0}, wl[2] = {0, 0};
+        int64_t sl[2] = {0, 0};
+        for (int src = 0; src < 32; src++) {
+#pragma unroll
+            for (int h2 = 0; h2 < 2; h2++) {
+                const int kk = __shfl_sync(GK_FULL, k[h2], src);
+                const uint32_t ww = __shfl_sync(GK_FULL, w[h2], src);
+                const int64_t ss = __shfl_sync(GK_FULL, s[h2], src);
+                const bool valid = kk < (1 << 20);
+#pragma unroll
+                for (int h = 0; h < 2; h++) {
+                    if (valid && kk <= k[h]) {
+                        cl[h] += 1;
+                        wl[h] += ww;
+                        sl[h] += ss;
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            if (r[h] < 0 || k[h] >= kBins - 1) continue;
+            if (cl[h] < 1 || (uint32_t)m - cl[h] < 1) continue;
+            const double SL = (double)sl[h], SR = (double)(S - sl[h]);
+            const double p = SL * SL / (double)wl[h] + SR * SR / (double)(W - wl[h]);
+            if (better(p, f, k[h], best)) best = BestSplit{p, f, k[h], cl[h]};
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        BestSplit q;
+        q.proxy = __shfl_xor_sync(GK_FULL, best.proxy, o);
+        q.feat = __shfl_xor_sync(GK_FULL, best.feat, o);
+        q.bin = __shfl_xor_sync(GK_FULL, best.bin, o);
+        q.n_left = __shfl_xor_sync(GK_FULL, best.n_left, o);
+        if (better(q.proxy, q.feat, q.bin, best)) best = q;
+    }
+    if (lane == 0) finish_split(best, parent, out + ti);
+}
+
+// ---------------------------------------------------------------- partition
+
+// CTA = (task, 4096-position chunk); rows of split tasks scatter to
+// [begin, begin + n_left) / [begin + n_left, end) of the other buffer
+__global__ void __launch_bounds__(256) k5_partition(RfTrainData D, const RfTask *__restrict__ tasks,
+                                                    const RfSplit *__restrict__ split,
+                                                    const int32_t *__restrict__ task_ids,
+                                                    const int32_t *__restrict__ rows0,
+                                                    int32_t *__restrict__ rows1_out0,
+                                                    const int32_t *__restrict__ rows1,
+                                                    int32_t *__restrict__ rows0_out1,
+                                                    int32_t *__restrict__ cursor) {
+    const int ti = task_ids[blockIdx.y];
+    const RfTask T = tasks[ti];
+    if (T.begin + (int)(blockIdx.x * blockDim.x) >= T.end) return;  // whole CTA past the node
+    const RfSplit sp = split[ti];
+    const int32_t *in = T.parity ? rows1 : rows0;
+    int32_t *outp = T.parity ? rows0_out1 : rows1_out0;
+    const int p = T.begin + blockIdx.x * blockDim.x + threadIdx.x;
+    const bool valid = p < T.end;
+    const int32_t r = valid ? in[p] : 0;
+    const bool left = valid && D.Xb[(size_t)r * D.F + sp.feat] <= sp.bin;
+    const bool right = valid && !left;
+    const int lane = threadIdx.x & 31;
+    const unsigned bl = __ballot_sync(GK_FULL, left), br = __ballot_sync(GK_FULL, right);
+    int lb = 0, rb = 0;
+    if (lane == 0) {
+        if (bl) lb = atomicAdd(cursor + 2 * ti, __popc(bl));
+        if (br) rb = atomicAdd(cursor + 2 * ti + 1, __popc(br));
+    }
+    lb = __shfl_sync(GK_FULL, lb, 0);
+    rb = __shfl_sync(GK_FULL, rb, 0);
+    const unsigned below = (1u << lane) - 1u;
+    if (left) outp[T.begin + lb + __popc(bl & below)] = r;
+    if (right) outp[T.begin + sp.n_left + rb + __popc(br & below)] = r;
+}
+
+// ---------------------------------------------------------------- leaf stats
+
+// one warp per leaf segment: n, sum w, sum w*y, sum w*y^2 in a fixed order
+__global__ void k5_leaf_stats(RfTrainData D, const RfTask *__restrict__ leaves, int n_leaves,
+                              const int32_t *__restrict__ rows0, const int32_t *__restrict__ rows1,
+                              double *__restrict__ out /*[n_leaves][4]*/) {
+    const int lane = threadIdx.x & 31;
+    const int li = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (li >= n_leaves) return;
+    const RfTask T = leaves[li];
+    const int32_t *rows = T.parity ? rows1 : rows0;
+    const uint32_t *cnt = D.counts + (size_t)T.tree * D.n;
+    double w = 0.0, sy = 0.0, sy2 = 0.0;
+    for (int p = T.begin + lane; p < T.end; p += 32) {
+        const int32_t r = rows[p];
+        const double ww = (double)cnt[r], yy = D.y[r];
+        w += ww;
+        sy += ww * yy;
+        sy2 += ww * yy * yy;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        w += __shfl_xor_sync(GK_FULL, w, o);
+        sy += __shfl_xor_sync(GK_FULL, sy, o);
+        sy2 += __shfl_xor_sync(GK_FULL, sy2, o);
+    }
+    if (lane == 0) {
+        out[4 * li + 0] = (double)(T.end - T.begin);
+        out[4 * li + 1] = w;
+        out[4 * li + 2] = sy;
+        out[4 * li + 3] = sy2;
+    }
+}
+
+}  // namespace gk
+
+// ------------------------------------------------------------------ C-ABI
+
+extern "C" {
+
+int gk_rf_bootstrap(const uint32_t *tree_seeds, uint32_t n_trees, int64_t n_rows,
+                    uint32_t *counts, void *stream) {
+    if (n_rows < 1 || n_rows > 0xffffffffll) {
+        gk_set_error("gk_rf_bootstrap: n_rows out of range");
+        return -1;
+    }
+    const cudaStream_t st = (cudaStream_t)stream;
+    cudaMemsetAsync(counts, 0, sizeof(uint32_t) * (size_t)n_trees * n_rows, st);
+    gk::k5_bootstrap<<<(n_trees + 3) / 4, 128, 0, st>>>(tree_seeds, (int)n_trees, n_rows, counts);
+    return gk_check_launch("k5_bootstrap");
+}
+
+int gk_rf_compact(const uint32_t *counts, uint32_t n_trees, int64_t n_rows,
+                  const int64_t *tree_base, int32_t *rows, int32_t *fill, void *stream) {
+    const cudaStream_t st = (cudaStream_t)stream;
+    cudaMemsetAsync(fill, 0, sizeof(int32_t) * n_trees, st);
+    dim3 grid((unsigned)((n_rows + 255) / 256), n_trees);
+    gk::k5_compact<<<grid, 256, 0, st>>>(counts, (int)n_trees, n_rows, tree_base, rows, fill);
+    return gk_check_launch("k5_compact");
+}
+
+int gk_rf_bin(const double *X, int64_t n_rows, int32_t n_feat, int64_t ld, const float *edges,
+              const int32_t *n_edges, uint8_t *Xb, uint32_t *bin_min, uint32_t *bin_max,
+              void *stream) {
+    const cudaStream_t st = (cudaStream_t)stream;
+    cudaMemsetAsync(bin_min, 0xff, sizeof(uint32_t) * n_feat * gk::kBins, st);
+    cudaMemsetAsync(bin_max, 0x00, sizeof(uint32_t) * n_feat * gk::kBins, st);
+    const int64_t tot = n_rows * n_feat;
+    gk::k5_bin<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(X, n_rows, n_feat, ld, edges,
+                                                              n_edges, Xb, bin_min, bin_max);
+    return gk_check_launch("k5_bin");
+}
+
+// One level of split search + partition for a task list.
+//   tasks[n_tasks] (tree, begin, end, parity); small/med/big index lists
+//   partition ids: tasks that split after the search (filled by the host)
+int gk_rf_split_level(const uint8_t *Xb, const int64_t *yfp, const double *y,
+                      const uint32_t *counts, int64_t n_rows, int32_t n_feat,
+                      const void *tasks, const int32_t *small_ids, int32_t n_small,
+                      const int32_t *med_ids, int32_t n_med, const int32_t *big_ids,
+                      int32_t n_big, int32_t big_max_chunks, const int32_t *rows0,
+                      const int32_t *rows1, void *hist_ws, void *split_out, void *stream) {
+    const cudaStream_t st = (cudaStream_t)stream;
+    gk::RfTrainData D{Xb, yfp, y, counts, n_rows, n_feat};
+    const gk::RfTask *T = (const gk::RfTask *)tasks;
+    gk::RfSplit *out = (gk::RfSplit *)split_out;
+    const size_t smem = sizeof(gk::HistSmem);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(gk::k5_split_medium, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(gk::k5_hist_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(gk::k5_eval_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    if (n_small > 0)
+        gk::k5_split_small<<<(n_small * 32 + 127) / 128, 128, 0, st>>>(D, T, small_ids, n_small,
+                                                                       rows0, rows1, out);
+    if (n_med > 0)
+        gk::k5_split_medium<<<n_med, 256, smem, st>>>(D, T, med_ids, rows0, rows1, out);
+    if (n_big > 0) {
+        uint64_t *gcw = (uint64_t *)hist_ws;
+        int64_t *gs = (int64_t *)(gcw + (size_t)n_big * n_feat * gk::kBins);
+        cudaMemsetAsync(hist_ws, 0, 2 * sizeof(uint64_t) * (size_t)n_big * n_feat * gk::kBins, st);
+        dim3 grid(big_max_chunks, (n_feat + gk::kFC - 1) / gk::kFC, n_big);
+        gk::k5_hist_big<<<grid, 256, smem, st>>>(D, T, big_ids, rows0, rows1, gcw, gs);
+        gk::k5_eval_big<<<n_big, 256, smem, st>>>(D, big_ids, gcw, gs, out);
+    }
+    return gk_check_launch("k5_split_level");
+}
+
+size_t gk_rf_hist_bytes(int32_t n_big, int32_t n_feat) {
+    return 2 * sizeof(uint64_t) * (size_t)n_big * n_feat * gk::kBins;
+}
+
+int gk_rf_partition(const uint8_t *Xb, const int64_t *yfp, const double *y,
+                    const uint32_t *counts, int64_t n_rows, int32_t n_feat, const void *tasks,
+                    int32_t n_tasks, const void *split, const int32_t *ids, int32_t n_ids,
+                    int32_t max_rows, int32_t *rows0, int32_t *rows1, int32_t *cursor,
+                    void *stream) {
+    if (n_ids <= 0) return 0;
+    const cudaStream_t st = (cudaStream_t)stream;
+    gk::RfTrainData D{Xb, yfp, y, counts, n_rows, n_feat};
+    cudaMemsetAsync(cursor, 0, sizeof(int32_t) * 2 * (size_t)n_tasks, st);
+    dim3 grid((unsigned)((max_rows + 255) / 256), n_ids);
+    gk::k5_partition<<<grid, 256, 0, st>>>(D, (const gk::RfTask *)tasks, (const gk::RfSplit *)split,
+                                           ids, rows0, rows1, rows1, rows0, cursor);
+    return gk_check_launch("k5_partition");
+}
+
+int gk_rf_leaf_stats(const uint32_t *counts, int64_t n_rows, const double *y, const void *leaves,
+                     int32_t n_leaves, const int32_t *rows0, const int32_t *rows1, double *out,
+                     void *stream) {
+    if (n_leaves <= 0) return 0;
+    const cudaStream_t st = (cudaStream_t)stream;
+    gk::RfTrainData D{nullptr, nullptr, y, counts, n_rows, 0};
+    gk::k5_leaf_stats<<<(n_leaves * 32 + 127) / 128, 128, 0, st>>>(
+        D, (const gk::RfTask *)leaves, n_leaves, rows0, rows1, out);
+    return gk_check_launch("k5_leaf_stats");
+}
+
+}  // extern "C"

@@ -1,0 +1,394 @@
+"""GPU random forest (K5) behind scikit-learn's estimator shape.
+
+Drop-in for the estimator the reference trainer builds in
+``gpukalc_trainer.training._make_model`` (``training.py:73-76``):
+``RandomForestRegressor(n_estimators, max_depth, random_state)`` with
+``fit(X, y)``, ``predict(X)`` and ``estimators_[k].tree_`` carrying the arrays
+``gpukalc_trainer.export.ensemble_document`` reads (``export.py:26-50``):
+node_count, children_left/right, feature, threshold, value, impurity,
+weighted_n_node_samples (+ n_node_samples, max_depth).
+
+Semantics kept from scikit-learn: per-tree seeds are
+successive ``RandomState(seed).randint(2**31 - 1)`` draws
+(SK/ensemble/_base.py:77-81); bootstrap weights are
+``bincount(RandomState(tree_seed).randint(0, n, n))`` (SK/ensemble/_forest.py:
+95-112, 150-156), generated bit-exactly on the device; X is fitted as float32
+(SK/tree/_classes.py:244); squared error, all features, min_samples_split 2,
+min_samples_leaf 1; thresholds are midpoints between adjacent training values
+(SK/tree/_splitter.pyx:459-460); predictions average the trees in order.
+Split search is histogram-based (<= 256 bins per feature), so trees differ
+from sklearn's exact search; the parity bar is R^2 / MAPE (BASELINE.json).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from .ensemble import NODE_DT, FlatEnsemble
+
+N_BINS = 256
+SMALL, MEDIUM = 64, 32768
+TASK_DT = np.dtype([("tree", "<i4"), ("begin", "<i4"), ("end", "<i4"), ("parity", "<i4")])
+SPLIT_DT = np.dtype({"names": ["feat", "bin", "n_left", "pad", "proxy"],
+                     "formats": ["<i4", "<i4", "<i4", "<i4", "<f8"],
+                     "offsets": [0, 4, 8, 12, 16], "itemsize": 24})
+TREE_LEAF, TREE_UNDEFINED = -1, -2
+
+
+def _lib():
+    from .runtime import load_library
+
+    L = load_library()
+    if not getattr(L, "_rf_bound", False):
+        vp, i32, i64, u32 = C.c_void_p, C.c_int32, C.c_int64, C.c_uint32
+        L.gk_rf_bootstrap.argtypes = [vp, u32, i64, vp, vp]
+        L.gk_rf_compact.argtypes = [vp, u32, i64, vp, vp, vp, vp]
+        L.gk_rf_bin.argtypes = [vp, i64, i32, i64, vp, vp, vp, vp, vp, vp]
+        L.gk_rf_split_level.argtypes = [vp, vp, vp, vp, i64, i32, vp, vp, i32, vp, i32, vp, i32,
+                                        i32, vp, vp, vp, vp, vp]
+        L.gk_rf_hist_bytes.argtypes = [i32, i32]
+        L.gk_rf_hist_bytes.restype = C.c_size_t
+        L.gk_rf_partition.argtypes = [vp, vp, vp, vp, i64, i32, vp, i32, vp, vp, i32, i32, vp,
+                                      vp, vp, vp]
+        L.gk_rf_leaf_stats.argtypes = [vp, i64, vp, vp, i32, vp, vp, vp, vp]
+        L._rf_bound = True
+    return L
+
+
+def _check(rc):
+    from .runtime import _check as chk
+
+    chk(rc)
+
+
+def tree_seeds(random_state, n_estimators: int) -> np.ndarray:
+    """Per-tree seeds as scikit-learn draws them (SK/ensemble/_base.py:77-81)."""
+    rs = random_state if isinstance(random_state, np.random.RandomState) else \
+        np.random.RandomState(random_state)
+    return np.array([rs.randint(np.iinfo(np.int32).max) for _ in range(n_estimators)],
+                    dtype=np.int64)
+
+
+def bin_edges(Xf: np.ndarray, n_bins: int = N_BINS, sample: int = 200_000):
+    """Per-feature bin edges on float32 data: one bin per distinct value when a
+    feature has <= n_bins of them, else quantile edges.  Deterministic."""
+    n, F = Xf.shape
+    if n > sample:
+        idx = np.random.default_rng(0).choice(n, sample, replace=False)
+        S = Xf[np.sort(idx)]
+    else:
+        S = Xf
+    edges = np.zeros((F, n_bins - 1), np.float32)
+    n_edges = np.zeros(F, np.int32)
+    for f in range(F):
+        u = np.unique(S[:, f])
+        if len(u) <= n_bins:
+            e = u[:-1]
+        else:
+            q = np.quantile(S[:, f], np.linspace(0.0, 1.0, n_bins + 1)[1:-1], method="lower")
+            e = np.unique(q.astype(np.float32))
+        edges[f, : len(e)] = e
+        n_edges[f] = len(e)
+    return edges, n_edges
+
+
+@dataclass
+class Tree:
+    """The subset of sklearn's ``Tree`` the reference exporter reads."""
+
+    node_count: int
+    children_left: np.ndarray
+    children_right: np.ndarray
+    feature: np.ndarray
+    threshold: np.ndarray
+    value: np.ndarray              # [node_count, 1, 1]
+    impurity: np.ndarray
+    n_node_samples: np.ndarray
+    weighted_n_node_samples: np.ndarray
+    max_depth: int
+
+
+@dataclass
+class TreeEstimator:
+    tree_: Tree
+    random_state: int
+
+
+class RandomForestRegressor:
+    """GPU-trained random forest with scikit-learn's constructor/fit/predict."""
+
+    def __init__(self, n_estimators: int = 100, *, max_depth: int | None = None,
+                 random_state=None, n_bins: int = N_BINS, trees_per_batch: int = 32,
+                 shard: tuple[int, int] | None = None):
+        self.n_estimators = n_estimators
+        self.max_depth = max_depth
+        self.random_state = random_state
+        self.n_bins = n_bins
+        self.trees_per_batch = trees_per_batch
+        self.shard = shard  # (rank, world): build trees t with t % world == rank
+        self.estimators_: list = []
+
+    # ------------------------------------------------------------------ fit
+    def fit(self, X, y, sample_weight=None):
+        import torch
+
+        from .runtime import _ptr, device
+
+        if sample_weight is not None:
+            raise NotImplementedError("sample_weight is not supported (training.py never passes it)")
+        X = np.ascontiguousarray(X, dtype=np.float64)
+        y = np.ascontiguousarray(y, dtype=np.float64).reshape(-1)
+        n, F = X.shape
+        if F > 64 * 1024 or n >= 2 ** 31:
+            raise ValueError("too many rows / features")
+        self.n_features_in_ = F
+        L = _lib()
+        dev = device()
+        Xf = X.astype(np.float32)
+        edges, n_edges = bin_edges(Xf, self.n_bins)
+        Xd = torch.from_numpy(Xf.astype(np.float64)).to(dev)
+        Xb = torch.empty(n * F, dtype=torch.uint8, device=dev)
+        bmin = torch.empty(F * N_BINS, dtype=torch.int32, device=dev)
+        bmax = torch.empty(F * N_BINS, dtype=torch.int32, device=dev)
+        ed = torch.from_numpy(edges).to(dev)
+        ne = torch.from_numpy(n_edges).to(dev)
+        _check(L.gk_rf_bin(_ptr(Xd), n, F, F, _ptr(ed), _ptr(ne), _ptr(Xb), _ptr(bmin), _ptr(bmax),
+                           torch.cuda.current_stream().cuda_stream))
+        del Xd
+        self._thr_tables(bmin.cpu().numpy().view(np.uint32).reshape(F, N_BINS),
+                         bmax.cpu().numpy().view(np.uint32).reshape(F, N_BINS))
+        ymax = float(np.max(np.abs(y))) if n else 1.0
+        shift = int(np.floor(62 - np.log2(max(ymax, 1e-300) * n + 1e-300)))
+        shift = max(min(shift, 60), -60)
+        yfp = torch.from_numpy(np.rint(np.ldexp(y, shift)).astype(np.int64)).to(dev)
+        yd = torch.from_numpy(y).to(dev)
+        self._dev = dict(Xb=Xb, yfp=yfp, y=yd, n=n, F=F)
+
+        seeds = tree_seeds(self.random_state, self.n_estimators)
+        todo = list(range(self.n_estimators))
+        if self.shard is not None:
+            rank, world = self.shard
+            todo = [t for t in todo if t % world == rank]
+        self.estimators_ = [None] * self.n_estimators
+        for b0 in range(0, len(todo), self.trees_per_batch):
+            batch = todo[b0: b0 + self.trees_per_batch]
+            for t, tree in zip(batch, self._grow_batch(seeds[batch])):
+                self.estimators_[t] = TreeEstimator(tree_=tree, random_state=int(seeds[t]))
+        if self.shard is None:
+            self._flat = None
+        del self._dev
+        return self
+
+    def _thr_tables(self, bmin_ord, bmax_ord):
+        def ord2f(u):
+            u = u.astype(np.uint32)
+            bits = np.where(u & 0x80000000, u & 0x7FFFFFFF, ~u)
+            return bits.astype(np.uint32).view(np.float32).astype(np.float64)
+
+        empty = bmin_ord == 0xFFFFFFFF
+        vmin = np.where(empty, np.inf, ord2f(bmin_ord))
+        vmax = np.where(empty, -np.inf, ord2f(bmax_ord))
+        F = vmin.shape[0]
+        # last non-empty bin <= b (its max) and first non-empty bin > b (its min)
+        lo = np.full((F, N_BINS), -np.inf)
+        hi = np.full((F, N_BINS), np.inf)
+        cur = np.full(F, -np.inf)
+        for b in range(N_BINS):
+            cur = np.where(empty[:, b], cur, vmax[:, b])
+            lo[:, b] = cur
+        cur = np.full(F, np.inf)
+        for b in range(N_BINS - 1, -1, -1):
+            hi[:, b] = cur
+            cur = np.where(empty[:, b], cur, vmin[:, b])
+        thr = lo / 2.0 + hi / 2.0              # SK/tree/_splitter.pyx:459-460
+        bad = (thr == hi) | ~np.isfinite(thr)
+        self._thr = np.where(bad, lo, thr)
+
+    def _grow_batch(self, seeds):
+        import torch
+
+        from .runtime import _ptr, device
+
+        L = _lib()
+        dev = device()
+        D = self._dev
+        n, F = D["n"], D["F"]
+        st = torch.cuda.current_stream().cuda_stream
+        TB = len(seeds)
+        seeds_d = torch.from_numpy(seeds.astype(np.uint32)).to(dev)
+        counts = torch.empty(TB * n, dtype=torch.int32, device=dev)
+        _check(L.gk_rf_bootstrap(_ptr(seeds_d), TB, n, _ptr(counts), st))
+        m = (counts.view(TB, n) > 0).sum(dim=1).cpu().numpy().astype(np.int64)
+        base = np.concatenate([[0], np.cumsum(m)[:-1]]).astype(np.int64)
+        total = int(m.sum())
+        base_d = torch.from_numpy(base).to(dev)
+        rows0 = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
+        rows1 = torch.empty_like(rows0)
+        fill = torch.empty(TB, dtype=torch.int32, device=dev)
+        _check(L.gk_rf_compact(_ptr(counts), TB, n, _ptr(base_d), _ptr(rows0), _ptr(fill), st))
+        max_depth = self.max_depth if self.max_depth is not None else 1 << 30
+
+        # node storage per tree (BFS ids; children of one split are adjacent)
+        cap = [2 * int(mt) + 1 for mt in m]
+        node_base = np.concatenate([[0], np.cumsum(cap)[:-1]]).astype(np.int64)
+        n_nodes_tot = int(sum(cap))
+        feat = np.full(n_nodes_tot, TREE_UNDEFINED, np.int32)
+        nbin = np.zeros(n_nodes_tot, np.int32)
+        left = np.full(n_nodes_tot, TREE_LEAF, np.int32)
+        depth = np.zeros(n_nodes_tot, np.int32)
+        next_id = np.ones(TB, np.int64)
+        leaves = []           # (tree, node, parity, begin, end) arrays per level
+        splits_by_level = []  # (parent gidx, left gidx) arrays per level
+
+        # level 0 tasks: one root per tree
+        t_tree = np.arange(TB, dtype=np.int32)
+        t_node = np.zeros(TB, np.int64)
+        t_begin = base.astype(np.int32)
+        t_end = (base + m).astype(np.int32)
+        t_par = np.zeros(TB, np.int32)
+        t_depth = 0
+        # a root with < 2 samples or max_depth 0 is a leaf right away
+        elig = (t_end - t_begin >= 2) & (t_depth < max_depth)
+        if (~elig).any():
+            leaves.append((t_tree[~elig], t_node[~elig], t_par[~elig], t_begin[~elig], t_end[~elig]))
+        t_tree, t_node, t_begin, t_end, t_par = (a[elig] for a in (t_tree, t_node, t_begin, t_end, t_par))
+        cursor = torch.empty(2 * max(len(t_tree), 1), dtype=torch.int32, device=dev)
+        while len(t_tree):
+            nt = len(t_tree)
+            tasks = np.zeros(nt, TASK_DT)
+            tasks["tree"], tasks["begin"], tasks["end"], tasks["parity"] = t_tree, t_begin, t_end, t_par
+            size = t_end - t_begin
+            ids_small = np.nonzero(size <= SMALL)[0].astype(np.int32)
+            ids_med = np.nonzero((size > SMALL) & (size <= MEDIUM))[0].astype(np.int32)
+            ids_big = np.nonzero(size > MEDIUM)[0].astype(np.int32)
+            tasks_d = torch.from_numpy(tasks.view(np.uint8)).to(dev)
+            ids_d = {k: torch.from_numpy(v if len(v) else np.zeros(1, np.int32)).to(dev)
+                     for k, v in (("s", ids_small), ("m", ids_med), ("b", ids_big))}
+            split_d = torch.empty(nt * SPLIT_DT.itemsize, dtype=torch.uint8, device=dev)
+            n_big = len(ids_big)
+            big_chunks = int(((size[ids_big] + MEDIUM - 1) // MEDIUM).max()) if n_big else 0
+            hist = torch.empty(max(int(L.gk_rf_hist_bytes(n_big, F)), 8), dtype=torch.uint8,
+                               device=dev)
+            _check(L.gk_rf_split_level(
+                _ptr(D["Xb"]), _ptr(D["yfp"]), _ptr(D["y"]), _ptr(counts), n, F, _ptr(tasks_d),
+                _ptr(ids_d["s"]), len(ids_small), _ptr(ids_d["m"]), len(ids_med), _ptr(ids_d["b"]),
+                n_big, big_chunks, _ptr(rows0), _ptr(rows1), _ptr(hist), _ptr(split_d), st))
+            sp = split_d.cpu().numpy().view(SPLIT_DT)
+            s = sp["feat"] >= 0
+            # leaves of this level stay where they are
+            if (~s).any():
+                leaves.append((t_tree[~s], t_node[~s], t_par[~s], t_begin[~s], t_end[~s]))
+            if not s.any():
+                break
+            ids_split = np.nonzero(s)[0].astype(np.int32)
+            if len(cursor) < 2 * nt:
+                cursor = torch.empty(2 * nt, dtype=torch.int32, device=dev)
+            ids_split_d = torch.from_numpy(ids_split).to(dev)
+            _check(L.gk_rf_partition(
+                _ptr(D["Xb"]), _ptr(D["yfp"]), _ptr(D["y"]), _ptr(counts), n, F, _ptr(tasks_d), nt,
+                _ptr(split_d), _ptr(ids_split_d), len(ids_split), int(size[ids_split].max()),
+                _ptr(rows0), _ptr(rows1), _ptr(cursor), st))
+            # children: adjacent BFS ids per tree, in task order
+            pt, pn = t_tree[s], t_node[s]
+            rank = np.zeros(len(pt), np.int64)
+            if len(pt):
+                starts = np.r_[0, np.nonzero(np.diff(pt))[0] + 1]
+                run_len = np.diff(np.r_[starts, len(pt)])
+                rank = np.arange(len(pt)) - np.repeat(starts, run_len)
+            lid = next_id[pt] + 2 * rank
+            np.add.at(next_id, pt, 2)
+            gpar = node_base[pt] + pn
+            feat[gpar] = sp["feat"][s]
+            nbin[gpar] = sp["bin"][s]
+            left[gpar] = lid
+            splits_by_level.append((gpar, node_base[pt] + lid))
+            nl = sp["n_left"][s].astype(np.int32)
+            cb = np.empty(2 * len(pt), np.int32)
+            ce = np.empty(2 * len(pt), np.int32)
+            cb[0::2], ce[0::2] = t_begin[s], t_begin[s] + nl
+            cb[1::2], ce[1::2] = t_begin[s] + nl, t_end[s]
+            ct = np.repeat(pt, 2)
+            cn = np.empty(2 * len(pt), np.int64)
+            cn[0::2], cn[1::2] = lid, lid + 1
+            cpar = np.repeat(1 - t_par[s], 2).astype(np.int32)
+            t_depth += 1
+            depth[node_base[ct] + cn] = t_depth
+            elig = (ce - cb >= 2) & (t_depth < max_depth)
+            if (~elig).any():
+                leaves.append((ct[~elig], cn[~elig], cpar[~elig], cb[~elig], ce[~elig]))
+            t_tree, t_node, t_begin, t_end, t_par = ct[elig], cn[elig], cb[elig], ce[elig], cpar[elig]
+
+        # leaf statistics (deterministic warp reductions), then bottom-up sums
+        lt = np.concatenate([a[0] for a in leaves]).astype(np.int32)
+        ln = np.concatenate([a[1] for a in leaves])
+        lp = np.concatenate([a[2] for a in leaves]).astype(np.int32)
+        lb = np.concatenate([a[3] for a in leaves]).astype(np.int32)
+        le = np.concatenate([a[4] for a in leaves]).astype(np.int32)
+        lv = np.zeros(len(lt), TASK_DT)
+        lv["tree"], lv["begin"], lv["end"], lv["parity"] = lt, lb, le, lp
+        lv_d = torch.from_numpy(lv.view(np.uint8)).to(dev)
+        stats_d = torch.empty(4 * len(lt), dtype=torch.float64, device=dev)
+        _check(L.gk_rf_leaf_stats(_ptr(counts), n, _ptr(D["y"]), _ptr(lv_d), len(lt), _ptr(rows0),
+                                  _ptr(rows1), _ptr(stats_d), st))
+        stats = np.zeros((n_nodes_tot, 4))
+        stats[node_base[lt] + ln] = stats_d.cpu().numpy().reshape(-1, 4)
+        for gpar, glid in reversed(splits_by_level):
+            stats[gpar] = stats[glid] + stats[glid + 1]
+
+        trees = []
+        for k in range(TB):
+            cnt = int(next_id[k])
+            g = slice(int(node_base[k]), int(node_base[k]) + cnt)
+            f = feat[g].copy()
+            cl = left[g].copy()
+            is_split = cl >= 0
+            cr = np.where(is_split, cl + 1, TREE_LEAF).astype(np.int64)
+            thr = np.full(cnt, float(TREE_UNDEFINED))
+            thr[is_split] = self._thr[f[is_split], nbin[g][is_split]]
+            f = np.where(is_split, f, TREE_UNDEFINED).astype(np.int64)
+            st_ = stats[g]
+            w = st_[:, 1]
+            val = st_[:, 2] / w
+            imp = st_[:, 3] / w - val * val
+            trees.append(Tree(node_count=cnt, children_left=cl.astype(np.int64), children_right=cr,
+                              feature=f, threshold=thr, value=val.reshape(-1, 1, 1), impurity=imp,
+                              n_node_samples=st_[:, 0].astype(np.int64), weighted_n_node_samples=w,
+                              max_depth=int(depth[g].max()) if cnt else 0))
+        return trees
+
+    # -------------------------------------------------------------- predict
+    def flat(self, leaf_scale: float = 1.0) -> FlatEnsemble:
+        """The forest in the device node layout (leaves scaled by leaf_scale)."""
+        parts, offs, depths, off = [], [], [], 0
+        for est in self.estimators_:
+            t = est.tree_
+            arr = np.zeros(t.node_count, NODE_DT)
+            split = t.children_left >= 0
+            arr["v"] = np.where(split, t.threshold, t.value[:, 0, 0] * leaf_scale)
+            arr["feature"] = np.where(split, t.feature, -1)
+            arr["left"] = np.where(split, t.children_left, np.arange(t.node_count))
+            parts.append(arr)
+            offs.append(off)
+            depths.append(t.max_depth)
+            off += t.node_count
+        F = self.n_features_in_
+        return FlatEnsemble(nodes=np.concatenate(parts).astype(NODE_DT),
+                            tree_off=np.asarray(offs, np.int64), scale_lo=np.zeros(F),
+                            scale_hi=np.ones(F), base_score=0.0, max_depth=max(depths),
+                            manifest=tuple(f"f{i}" for i in range(F)),
+                            tree_depth=np.asarray(depths, np.int32))
+
+    def predict(self, X) -> np.ndarray:
+        """Mean of the trees' predictions on float32-cast X (sklearn semantics)."""
+        import torch
+
+        from .runtime import DeviceEnsemble, device, rf_predict
+
+        if getattr(self, "_flat", None) is None:
+            self._flat = DeviceEnsemble.upload(self.flat())
+        Xf = np.ascontiguousarray(np.asarray(X, dtype=np.float64).astype(np.float32), np.float64)
+        total, _ = rf_predict(self._flat, torch.from_numpy(Xf).to(device()))
+        return total.cpu().numpy() / len(self.estimators_)

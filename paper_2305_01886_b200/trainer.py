@@ -1,0 +1,193 @@
+"""Trainer face: ``train(dataset, "random_forest", ...)`` with the GPU forest.
+
+Mirrors ``gpukalc_trainer.training.train`` (``training.py:94-160``): canonical
+row order (mergesort by every feature, then the target; ``:82-91``), 5-fold
+``KFold(shuffle=True, random_state=seed)``, a ``MinMaxScaler`` fit per training
+fold, fold metrics (R^2, RMSE, MAE), then a final fit on all rows.  The forest
+(``_make_model``'s RandomForestRegressor, ``:73-76``) is
+:class:`paper_2305_01886_b200.forest.RandomForestRegressor` (GPU, K5).  Export
+follows ``export.py:26-83`` so the document loads in the reference's
+``load_ensemble`` and in this package's.
+
+Host glue here uses pandas / scikit-learn's KFold, MinMaxScaler and metrics
+exactly as the reference trainer does; tree fitting and prediction run on the
+device.  Like the reference, this module never imports the predictor face.
+"""
+
+from __future__ import annotations
+
+import json
+from dataclasses import dataclass, field
+from pathlib import Path
+from typing import Any
+
+import numpy as np
+
+from .errors import TrainerError
+from .forest import RandomForestRegressor
+
+FAMILIES = ("random_forest", "gradient_boosted")
+N_FOLDS = 5
+MIN_ROWS = 50
+
+
+@dataclass(frozen=True)
+class FoldMetrics:
+    r2: float
+    rmse: float
+    mae: float
+
+    def as_dict(self) -> dict:
+        return {"r2": self.r2, "rmse": self.rmse, "mae": self.mae}
+
+
+@dataclass
+class TrainResult:
+    family: str
+    seed: int
+    hyperparameters: dict[str, Any]
+    manifest: tuple
+    model: Any
+    scaler: Any
+    fold_metrics: list
+    mean_metrics: FoldMetrics
+    X: np.ndarray = field(repr=False)
+    y: np.ndarray = field(repr=False)
+    holdout_indices: np.ndarray = field(repr=False)
+    fold_mape_pct: list = field(default_factory=list)   # harness metric (not in the reference)
+
+    def metrics_doc(self) -> dict:
+        return {"family": self.family, "seed": self.seed,
+                "hyperparameters": self.hyperparameters, "n_rows": int(self.X.shape[0]),
+                "n_features": len(self.manifest), "feature_manifest": list(self.manifest),
+                "folds": [m.as_dict() for m in self.fold_metrics],
+                "mean": self.mean_metrics.as_dict()}
+
+
+def _make_model(family: str, n_estimators: int, learning_rate: float, max_depth, seed: int):
+    if family == "random_forest":
+        return RandomForestRegressor(n_estimators=n_estimators, max_depth=max_depth,
+                                     random_state=seed)
+    if family == "gradient_boosted":
+        raise TrainerError("the gradient-boosted family is not on the B200 path yet "
+                           "(SURVEY §8(f) #2); use family='random_forest'")
+    raise TrainerError(f"unsupported model family '{family}'; choose from {', '.join(FAMILIES)}")
+
+
+def canonical_rows(X, y, manifest) -> tuple[np.ndarray, np.ndarray]:
+    """Reference ``training.py:82-91``: stable sort by all features then target."""
+    import pandas as pd
+
+    frame = pd.DataFrame(np.asarray(X, dtype=float), columns=list(manifest))
+    target = "__target__"
+    frame[target] = np.asarray(y, dtype=float)
+    frame = frame.sort_values(by=list(manifest) + [target], kind="mergesort")
+    return frame[list(manifest)].to_numpy(dtype=float), frame[target].to_numpy(dtype=float)
+
+
+def train(dataset, family: str = "gradient_boosted", *, n_estimators: int = 500,
+          learning_rate: float = 0.05, max_depth: int | None = None, seed: int = 0) -> TrainResult:
+    """5-fold CV, then a final fit on all rows (reference ``training.py:94-160``).
+
+    `dataset` is the reference's Dataset (X DataFrame, y Series) or any object
+    with ``X``, ``y`` and ``manifest``; or an (X, y, manifest) tuple.
+    """
+    from sklearn.metrics import mean_absolute_error, mean_squared_error, r2_score
+    from sklearn.model_selection import KFold
+    from sklearn.preprocessing import MinMaxScaler
+
+    if family not in FAMILIES:
+        raise TrainerError(f"unsupported model family '{family}'; choose from " + ", ".join(FAMILIES))
+    if isinstance(dataset, tuple):
+        Xraw, yraw, manifest = dataset
+    else:
+        Xraw, yraw = dataset.X, dataset.y
+        manifest = tuple(getattr(dataset, "manifest", None) or list(dataset.X.columns))
+    n_rows = len(yraw)
+    if n_rows < MIN_ROWS:
+        raise TrainerError(f"need at least {MIN_ROWS} rows for {N_FOLDS}-fold CV, got {n_rows}")
+    X, y = canonical_rows(Xraw, yraw, manifest)
+    if np.ptp(y) == 0.0:
+        raise TrainerError("degenerate target: every row has the same value")
+    _make_model(family, n_estimators, learning_rate, max_depth, seed)  # family check
+    folds, mapes = [], []
+    holdout = np.empty(0, dtype=int)
+    for tr, te in KFold(n_splits=N_FOLDS, shuffle=True, random_state=seed).split(X):
+        scaler = MinMaxScaler().fit(X[tr])
+        model = _make_model(family, n_estimators, learning_rate, max_depth, seed)
+        model.fit(scaler.transform(X[tr]), y[tr])
+        pred = model.predict(scaler.transform(X[te]))
+        folds.append(FoldMetrics(r2=float(r2_score(y[te], pred)),
+                                 rmse=float(np.sqrt(mean_squared_error(y[te], pred))),
+                                 mae=float(mean_absolute_error(y[te], pred))))
+        mapes.append(float(np.mean(np.abs((y[te] - pred) / y[te])) * 100.0))
+        holdout = te
+    mean = FoldMetrics(r2=float(np.mean([m.r2 for m in folds])),
+                       rmse=float(np.mean([m.rmse for m in folds])),
+                       mae=float(np.mean([m.mae for m in folds])))
+    final_scaler = MinMaxScaler().fit(X)
+    final_model = _make_model(family, n_estimators, learning_rate, max_depth, seed)
+    final_model.fit(final_scaler.transform(X), y)
+    return TrainResult(family=family, seed=seed,
+                       hyperparameters={"n_estimators": n_estimators,
+                                        "learning_rate": learning_rate, "max_depth": max_depth},
+                       manifest=tuple(manifest), model=final_model, scaler=final_scaler,
+                       fold_metrics=folds, mean_metrics=mean, X=X, y=y, holdout_indices=holdout,
+                       fold_mape_pct=mapes)
+
+
+# ------------------------------------------------------------------ export
+
+
+def _tree_nodes(tree, leaf_scale: float) -> list:
+    """sklearn-style tree arrays -> node dicts (``export.py:26-39``)."""
+    nodes = []
+    for i in range(tree.node_count):
+        if tree.children_left[i] == -1:
+            nodes.append({"value": float(tree.value[i][0][0]) * leaf_scale})
+        else:
+            nodes.append({"feature": int(tree.feature[i]), "threshold": float(tree.threshold[i]),
+                          "left": int(tree.children_left[i]),
+                          "right": int(tree.children_right[i])})
+    return nodes
+
+
+def _accumulate_gains(tree, gains: np.ndarray) -> None:
+    """Weighted impurity decrease per feature (``export.py:42-50``)."""
+    w, imp = tree.weighted_n_node_samples, tree.impurity
+    for i in range(tree.node_count):
+        left, right = tree.children_left[i], tree.children_right[i]
+        if left == -1:
+            continue
+        dec = w[i] * imp[i] - w[left] * imp[left] - w[right] * imp[right]
+        gains[tree.feature[i]] += max(float(dec), 0.0)
+
+
+def ensemble_document(result: TrainResult) -> dict:
+    """Portable ensemble JSON (``export.py:53-83``); RF leaves x 1/n_trees."""
+    if result.family != "random_forest":
+        raise TrainerError(f"unsupported model family '{result.family}'")
+    estimators = list(result.model.estimators_)
+    leaf_scale = 1.0 / len(estimators)
+    gains = np.zeros(len(result.manifest))
+    trees = []
+    for est in estimators:
+        trees.append({"nodes": _tree_nodes(est.tree_, leaf_scale)})
+        _accumulate_gains(est.tree_, gains)
+    return {"schema_version": 1, "base_score": 0.0, "feature_manifest": list(result.manifest),
+            "scaling": {"min": [float(v) for v in result.scaler.data_min_],
+                        "max": [float(v) for v in result.scaler.data_max_]},
+            "trees": trees, "gains": [float(g) for g in gains]}
+
+
+def export_ensemble(result: TrainResult, out_dir, *, n_vectors: int = 20):
+    """ensemble.json (+ metrics.json) like ``export.py:150-175``."""
+    if n_vectors < 1:
+        raise TrainerError("need at least one test vector")
+    out = Path(out_dir)
+    out.mkdir(parents=True, exist_ok=True)
+    doc = ensemble_document(result)
+    p = out / "ensemble.json"
+    p.write_text(json.dumps(doc, indent=2) + "\n")
+    (out / "metrics.json").write_text(json.dumps(result.metrics_doc(), indent=2) + "\n")
+    return p

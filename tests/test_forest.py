@@ -1,0 +1,130 @@
+"""K5 random-forest training: seed exactness (CPU) and GPU fit parity.
+
+Bars (BASELINE.json): bootstrap counts seed-exact vs scikit-learn; trained-model
+R^2 within 0.005 and MAPE within 0.5 percentage points of the reference
+``train(..., "random_forest")`` over the same KFold folds (golden
+tests/golden/trainer_rf.json, produced by the reference with sklearn 1.9.0)."""
+
+import json
+
+import numpy as np
+import pytest
+
+from goldens import G
+from paper_2305_01886_b200.forest import bin_edges, tree_seeds
+
+
+def test_tree_seeds_match_sklearn():
+    b = np.load(G / "rf_bootstrap.npz")
+    for n in (1000, 4097):
+        for seed in (0, 1, 42):
+            assert np.array_equal(tree_seeds(seed, 5), b[f"n{n}_s{seed}_seeds"])
+
+
+def test_bin_edges_exact_for_few_distinct_values():
+    X = np.zeros((500, 2), np.float32)
+    X[:, 0] = np.arange(500) % 7
+    X[:, 1] = np.linspace(0, 1, 500)
+    e, ne = bin_edges(X)
+    assert ne[0] == 6 and list(e[0, :6]) == [0, 1, 2, 3, 4, 5]
+    assert ne[1] == 255
+
+
+def power_frame(n, seed):
+    """The reference trainer's synthetic generator (trainer/tests/conftest.py:8-32),
+    restated: power = 30 + 40 occ + 0.003 iic + 12 [loads > 50] + N(0, 1)."""
+    import pandas as pd
+
+    rng = np.random.default_rng(seed)
+    occ = rng.uniform(0.1, 1.0, n)
+    iic = rng.uniform(0.0, 20000.0, n)
+    loads = rng.integers(0, 200, n).astype(float)
+    frame = pd.DataFrame({
+        "kernel": [f"bench_{i}" for i in range(n)],
+        "occupancy": occ, "inst_issue_cycles": iic, "glob_load_sm": loads,
+        "block_size": rng.choice([64.0, 128.0, 256.0, 512.0, 1024.0], n),
+        "reg_thread": rng.integers(8, 64, n).astype(float),
+        "cache_penalty": rng.uniform(0.0, 500.0, n),
+        "power_w": (30.0 + 40.0 * occ + 0.003 * iic + 12.0 * (loads > 50)
+                    + rng.normal(0.0, 1.0, n)),
+    })
+    return frame
+
+
+@pytest.mark.gpu
+def test_device_bootstrap_matches_sklearn():
+    import ctypes
+
+    import torch
+
+    from paper_2305_01886_b200 import forest
+    from paper_2305_01886_b200.runtime import _ptr
+
+    L = forest._lib()
+    b = np.load(G / "rf_bootstrap.npz")
+    for n in (1000, 4097):
+        for seed in (0, 1, 42):
+            seeds = b[f"n{n}_s{seed}_seeds"]
+            want = b[f"n{n}_s{seed}_counts"]
+            sd = torch.tensor(seeds.astype(np.uint32).view(np.int32), device="cuda")
+            out = torch.empty(len(seeds) * n, dtype=torch.int32, device="cuda")
+            assert L.gk_rf_bootstrap(_ptr(sd), len(seeds), n, _ptr(out),
+                                     torch.cuda.current_stream().cuda_stream) == 0
+            got = out.view(len(seeds), n).cpu().numpy()
+            assert np.array_equal(got, want.astype(np.int32)), (n, seed)
+    _ = ctypes
+
+
+@pytest.mark.gpu
+def test_forest_fit_predict_and_export_roundtrip():
+    from paper_2305_01886_b200.ensemble import flatten, load_ensemble
+    from paper_2305_01886_b200.forest import RandomForestRegressor
+    from paper_2305_01886_b200.trainer import train, ensemble_document
+    import oracle as O
+
+    fr = power_frame(800, 11)
+    feats = [c for c in fr.columns if c not in ("kernel", "power_w")]
+    res = train((fr[feats].to_numpy(), fr["power_w"].to_numpy(), tuple(feats)), "random_forest",
+                n_estimators=24, max_depth=10, seed=3)
+    model = res.model
+    assert len(model.estimators_) == 24
+    for est in model.estimators_:
+        t = est.tree_
+        leaf = t.children_left == -1
+        assert (t.children_right[~leaf] == t.children_left[~leaf] + 1).all()
+        assert t.max_depth <= 10
+        assert np.all(t.n_node_samples[~leaf] ==
+                      t.n_node_samples[t.children_left[~leaf]] + t.n_node_samples[t.children_right[~leaf]])
+    # the exported document (export.py layout) walks to the model's predictions
+    # (training rows: their float64 scaled values and the float32 values the
+    # model compares sit on the same side of every midpoint threshold)
+    doc = ensemble_document(res)
+    flat = flatten(load_ensemble(doc))
+    pw, _ = O.rf_predict(flat, res.X[:200])
+    sk_like = model.predict(res.scaler.transform(res.X[:200]))
+    np.testing.assert_allclose(pw, sk_like, rtol=1e-6)
+    # determinism: same seed -> identical trees
+    m2 = RandomForestRegressor(n_estimators=4, max_depth=10, random_state=3).fit(
+        res.scaler.transform(res.X), res.y)
+    m3 = RandomForestRegressor(n_estimators=4, max_depth=10, random_state=3).fit(
+        res.scaler.transform(res.X), res.y)
+    for a, b in zip(m2.estimators_, m3.estimators_):
+        assert np.array_equal(a.tree_.feature, b.tree_.feature)
+        assert np.array_equal(a.tree_.threshold, b.tree_.threshold)
+        assert np.array_equal(a.tree_.value, b.tree_.value)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("key", ["n600_seed3_depth16", "n2000_seed5_depth12"])
+def test_train_r2_mape_parity_with_reference(key):
+    from paper_2305_01886_b200.trainer import train
+
+    ref = json.loads((G / "trainer_rf.json").read_text())[key]
+    fr = power_frame(ref["n_rows"], ref["frame_seed"])
+    feats = ref["features"]
+    res = train((fr[feats].to_numpy(), fr["power_w"].to_numpy(), tuple(feats)), "random_forest",
+                n_estimators=ref["n_estimators"], max_depth=ref["max_depth"], seed=0)
+    r2 = res.mean_metrics.r2
+    mape = float(np.mean(res.fold_mape_pct))
+    assert abs(r2 - ref["mean"]["r2"]) <= 0.005, (r2, ref["mean"]["r2"])
+    assert abs(mape - ref["mean_mape_pct"]) <= 0.5, (mape, ref["mean_mape_pct"])
