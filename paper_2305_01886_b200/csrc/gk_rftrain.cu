@@ -80,24 +80,19 @@ __global__ void __launch_bounds__(128) k5_bootstrap(const uint32_t *__restrict__
     while (accepted < n) {
         // twist in three dependency phases: [0,227) old operands, [227,454)
         // needs phase-1 results, [454,623) needs phase-2, 623 needs mt[0] new
-        for (int k = lane; k < 227; k += 32) {
-            const uint32_t v = twist(k);
-            __syncwarp(__activemask());
-            mt[k] = v;
+        // (warp-uniform trip counts + full-mask syncs: every lane reads its
+        // operands before any lane of the chunk overwrites them)
+        const int phase_lo[3] = {0, 227, 454}, phase_hi[3] = {227, 454, 623};
+        for (int ph = 0; ph < 3; ph++) {
+            for (int k0 = phase_lo[ph]; k0 < phase_hi[ph]; k0 += 32) {
+                const int k = k0 + lane;
+                const bool in = k < phase_hi[ph];
+                const uint32_t v = in ? twist(k) : 0u;
+                __syncwarp();
+                if (in) mt[k] = v;
+                __syncwarp();
+            }
         }
-        __syncwarp();
-        for (int k = 227 + lane; k < 454; k += 32) {
-            const uint32_t v = twist(k);
-            __syncwarp(__activemask());
-            mt[k] = v;
-        }
-        __syncwarp();
-        for (int k = 454 + lane; k < 623; k += 32) {
-            const uint32_t v = twist(k);
-            __syncwarp(__activemask());
-            mt[k] = v;
-        }
-        __syncwarp();
         if (lane == 0) mt[623] = twist(623);
         __syncwarp();
         for (int k0 = 0; k0 < 624 && accepted < n; k0 += 32) {
