@@ -253,10 +253,10 @@ int gk_rf_partition(const uint8_t *Xb, const int64_t *yfp, const double *y,
                     int32_t n_tasks, const void *split, const int32_t *ids, int32_t n_ids,
                     int32_t max_rows, int32_t *rows0, int32_t *rows1, int32_t *cursor,
                     void *stream);
-/* per leaf segment: {n, sum w, sum w*y, sum w*y^2} (fixed reduction order) */
-int gk_rf_leaf_stats(const uint32_t *counts, int64_t n_rows, const double *y, const void *leaves,
-                     int32_t n_leaves, const int32_t *rows0, const int32_t *rows1, double *out,
-                     void *stream);
+/* per leaf segment: int64 {n, sum w, sum w*yfp, sum w*y2fp} (exact fixed-point sums) */
+int gk_rf_leaf_stats(const uint32_t *counts, int64_t n_rows, const int64_t *yfp,
+                     const int64_t *y2fp, const void *leaves, int32_t n_leaves,
+                     const int32_t *rows0, const int32_t *rows1, int64_t *out, void *stream);
 
 int gk_set_stage_timing(int on);
 int gk_get_stage_ms(float *out3);

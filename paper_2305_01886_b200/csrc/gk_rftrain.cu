@@ -519,23 +519,26 @@ __global__ void __launch_bounds__(256) k5_partition(RfTrainData D, const RfTask 
 
 // ---------------------------------------------------------------- leaf stats
 
-// one warp per leaf segment: n, sum w, sum w*y, sum w*y^2 in a fixed order
-__global__ void k5_leaf_stats(RfTrainData D, const RfTask *__restrict__ leaves, int n_leaves,
+// one warp per leaf segment: n, sum w, sum w*y, sum w*y^2 as exact 64-bit
+// fixed-point integer sums (row order inside a segment is not deterministic,
+// integer sums are); y2fp = y^2 in its own fixed-point scale
+__global__ void k5_leaf_stats(RfTrainData D, const int64_t *__restrict__ y2fp,
+                              const RfTask *__restrict__ leaves, int n_leaves,
                               const int32_t *__restrict__ rows0, const int32_t *__restrict__ rows1,
-                              double *__restrict__ out /*[n_leaves][4]*/) {
+                              int64_t *__restrict__ out /*[n_leaves][4]*/) {
     const int lane = threadIdx.x & 31;
     const int li = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (li >= n_leaves) return;
     const RfTask T = leaves[li];
     const int32_t *rows = T.parity ? rows1 : rows0;
     const uint32_t *cnt = D.counts + (size_t)T.tree * D.n;
-    double w = 0.0, sy = 0.0, sy2 = 0.0;
+    long long w = 0, sy = 0, sy2 = 0;
     for (int p = T.begin + lane; p < T.end; p += 32) {
         const int32_t r = rows[p];
-        const double ww = (double)cnt[r], yy = D.y[r];
+        const long long ww = cnt[r];
         w += ww;
-        sy += ww * yy;
-        sy2 += ww * yy * yy;
+        sy += ww * D.yfp[r];
+        sy2 += ww * y2fp[r];
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
@@ -544,7 +547,7 @@ __global__ void k5_leaf_stats(RfTrainData D, const RfTask *__restrict__ leaves, 
         sy2 += __shfl_xor_sync(GK_FULL, sy2, o);
     }
     if (lane == 0) {
-        out[4 * li + 0] = (double)(T.end - T.begin);
+        out[4 * li + 0] = T.end - T.begin;
         out[4 * li + 1] = w;
         out[4 * li + 2] = sy;
         out[4 * li + 3] = sy2;
@@ -646,14 +649,14 @@ int gk_rf_partition(const uint8_t *Xb, const int64_t *yfp, const double *y,
     return gk_check_launch("k5_partition");
 }
 
-int gk_rf_leaf_stats(const uint32_t *counts, int64_t n_rows, const double *y, const void *leaves,
-                     int32_t n_leaves, const int32_t *rows0, const int32_t *rows1, double *out,
-                     void *stream) {
+int gk_rf_leaf_stats(const uint32_t *counts, int64_t n_rows, const int64_t *yfp,
+                     const int64_t *y2fp, const void *leaves, int32_t n_leaves,
+                     const int32_t *rows0, const int32_t *rows1, int64_t *out, void *stream) {
     if (n_leaves <= 0) return 0;
     const cudaStream_t st = (cudaStream_t)stream;
-    gk::RfTrainData D{nullptr, nullptr, y, counts, n_rows, 0};
+    gk::RfTrainData D{nullptr, yfp, nullptr, counts, n_rows, 0};
     gk::k5_leaf_stats<<<(n_leaves * 32 + 127) / 128, 128, 0, st>>>(
-        D, (const gk::RfTask *)leaves, n_leaves, rows0, rows1, out);
+        D, y2fp, (const gk::RfTask *)leaves, n_leaves, rows0, rows1, out);
     return gk_check_launch("k5_leaf_stats");
 }
 

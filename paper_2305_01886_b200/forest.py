@@ -53,7 +53,7 @@ def _lib():
         L.gk_rf_hist_bytes.restype = C.c_size_t
         L.gk_rf_partition.argtypes = [vp, vp, vp, vp, i64, i32, vp, i32, vp, vp, i32, i32, vp,
                                       vp, vp, vp]
-        L.gk_rf_leaf_stats.argtypes = [vp, i64, vp, vp, i32, vp, vp, vp, vp]
+        L.gk_rf_leaf_stats.argtypes = [vp, i64, vp, vp, vp, i32, vp, vp, vp, vp]
         L._rf_bound = True
     return L
 
@@ -164,8 +164,13 @@ class RandomForestRegressor:
         shift = int(np.floor(62 - np.log2(max(ymax, 1e-300) * n + 1e-300)))
         shift = max(min(shift, 60), -60)
         yfp = torch.from_numpy(np.rint(np.ldexp(y, shift)).astype(np.int64)).to(dev)
+        y2 = y * y
+        y2max = float(np.max(y2)) if n else 1.0
+        shift2 = int(np.floor(62 - np.log2(max(y2max, 1e-300) * n + 1e-300)))
+        shift2 = max(min(shift2, 60), -60)
+        y2fp = torch.from_numpy(np.rint(np.ldexp(y2, shift2)).astype(np.int64)).to(dev)
         yd = torch.from_numpy(y).to(dev)
-        self._dev = dict(Xb=Xb, yfp=yfp, y=yd, n=n, F=F)
+        self._dev = dict(Xb=Xb, yfp=yfp, y2fp=y2fp, y=yd, n=n, F=F, shift=shift, shift2=shift2)
 
         seeds = tree_seeds(self.random_state, self.n_estimators)
         todo = list(range(self.n_estimators))
@@ -330,13 +335,19 @@ class RandomForestRegressor:
         lv = np.zeros(len(lt), TASK_DT)
         lv["tree"], lv["begin"], lv["end"], lv["parity"] = lt, lb, le, lp
         lv_d = torch.from_numpy(lv.view(np.uint8)).to(dev)
-        stats_d = torch.empty(4 * len(lt), dtype=torch.float64, device=dev)
-        _check(L.gk_rf_leaf_stats(_ptr(counts), n, _ptr(D["y"]), _ptr(lv_d), len(lt), _ptr(rows0),
-                                  _ptr(rows1), _ptr(stats_d), st))
-        stats = np.zeros((n_nodes_tot, 4))
-        stats[node_base[lt] + ln] = stats_d.cpu().numpy().reshape(-1, 4)
+        stats_d = torch.empty(4 * len(lt), dtype=torch.int64, device=dev)
+        _check(L.gk_rf_leaf_stats(_ptr(counts), n, _ptr(D["yfp"]), _ptr(D["y2fp"]), _ptr(lv_d),
+                                  len(lt), _ptr(rows0), _ptr(rows1), _ptr(stats_d), st))
+        # exact integer sums bottom-up, converted to float64 once per node
+        istats = np.zeros((n_nodes_tot, 4), np.int64)
+        istats[node_base[lt] + ln] = stats_d.cpu().numpy().reshape(-1, 4)
         for gpar, glid in reversed(splits_by_level):
-            stats[gpar] = stats[glid] + stats[glid + 1]
+            istats[gpar] = istats[glid] + istats[glid + 1]
+        stats = np.empty((n_nodes_tot, 4))
+        stats[:, 0] = istats[:, 0]
+        stats[:, 1] = istats[:, 1]
+        stats[:, 2] = np.ldexp(istats[:, 2].astype(np.float64), -D["shift"])
+        stats[:, 3] = np.ldexp(istats[:, 3].astype(np.float64), -D["shift2"])
 
         trees = []
         for k in range(TB):
