@@ -492,13 +492,13 @@ __global__ void __launch_bounds__(256) k5_partition(RfTrainData D, const RfTask 
                                                     const int32_t *__restrict__ rows1,
                                                     int32_t *__restrict__ rows0_out1,
                                                     int32_t *__restrict__ cursor) {
-    const int ti = task_ids[blockIdx.y];
+    const int ti = task_ids[blockIdx.x];  // tasks on x (can exceed 65535), chunks on y
     const RfTask T = tasks[ti];
-    if (T.begin + (int)(blockIdx.x * blockDim.x) >= T.end) return;  // whole CTA past the node
+    if (T.begin + (int)(blockIdx.y * blockDim.x) >= T.end) return;  // whole CTA past the node
     const RfSplit sp = split[ti];
     const int32_t *in = T.parity ? rows1 : rows0;
     int32_t *outp = T.parity ? rows0_out1 : rows1_out0;
-    const int p = T.begin + blockIdx.x * blockDim.x + threadIdx.x;
+    const int p = T.begin + blockIdx.y * blockDim.x + threadIdx.x;
     const bool valid = p < T.end;
     const int32_t r = valid ? in[p] : 0;
     const bool left = valid && D.Xb[(size_t)r * D.F + sp.feat] <= sp.bin;
@@ -643,7 +643,12 @@ int gk_rf_partition(const uint8_t *Xb, const int64_t *yfp, const double *y,
     const cudaStream_t st = (cudaStream_t)stream;
     gk::RfTrainData D{Xb, yfp, y, counts, n_rows, n_feat};
     cudaMemsetAsync(cursor, 0, sizeof(int32_t) * 2 * (size_t)n_tasks, st);
-    dim3 grid((unsigned)((max_rows + 255) / 256), n_ids);
+    const int64_t chunks = ((int64_t)max_rows + 255) / 256;
+    if (chunks > 65535) {
+        gk_set_error("gk_rf_partition: node of %d rows exceeds the 16.7M-row chunk grid", max_rows);
+        return -1;
+    }
+    dim3 grid((unsigned)n_ids, (unsigned)chunks);
     gk::k5_partition<<<grid, 256, 0, st>>>(D, (const gk::RfTask *)tasks, (const gk::RfSplit *)split,
                                            ids, rows0, rows1, rows1, rows0, cursor);
     return gk_check_launch("k5_partition");
