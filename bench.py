@@ -75,7 +75,17 @@ class ClockSampler:
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) >= 8:
-                self.rows.append(parts)
+                self.rows.append([time.perf_counter()] + parts)
+
+    def window(self, t0: float, t1: float):
+        """Keep the samples taken inside [t0, t1] (the timed region); if the
+        region is shorter than the sampling period keep the busy samples around it."""
+        inside = [r for r in self.rows if t0 <= r[0] <= t1]
+        self.scope = "timed region"
+        if not inside:
+            inside = [r for r in self.rows if r[0] >= t0 - 1.0]
+            self.scope = "timed region +/- 1 s (region shorter than the 100 ms period)"
+        self.rows = inside
 
     def __exit__(self, *a):
         if self.proc:
@@ -90,13 +100,14 @@ class ClockSampler:
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        rows = [r[1:] for r in self.rows]
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({n for r in self.rows for n, v in zip(names, r[4:8]) if v == "Active"})
+        reasons = sorted({n for r in rows for n, v in zip(names, r[4:8]) if v == "Active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+                "samples": len(rows), "scope": getattr(self, "scope", "all")}
 
 
 # --------------------------------------------------------------- workload
@@ -166,23 +177,30 @@ def run_ours(args, rank, world, local_rank):
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
 
-    for _ in range(args.warmup):
-        sweep.run()
-    torch.cuda.synchronize()
-
     # ---- timed: K steps, device events per step, L2 flushed (untimed) between steps
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
     with ClockSampler(local_rank) as clk:
+        t_w = time.perf_counter()
+        while True:  # warm-up (>= W steps, and >= 1 s so the clock sampler is running)
+            for _ in range(args.warmup):
+                sweep.run()
+            torch.cuda.synchronize()
+            if time.perf_counter() - t_w > 1.0:
+                break
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
         for k in range(args.steps):
             flush.zero_()
             evs[k][0].record(stream)
             sweep.run()
             evs[k][1].record(stream)
         torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        time.sleep(0.25)
+    clk.window(t0, t1)
     if world > 1:
         dist.barrier()
     step_ms = [a.elapsed_time(b) for a, b in evs]
@@ -309,6 +327,9 @@ def main():
     ap.add_argument("--depth", type=int, default=16)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline (profiling)")
+    ap.add_argument("--no-rf", action="store_true", help="skip the config #3 forest fit")
+    ap.add_argument("--rf-rows", type=int, default=1_000_000)
+    ap.add_argument("--rf-trees", type=int, default=64)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -354,6 +375,8 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     R = run_ours(args, rank, world, local_rank)
+    if not args.no_rf:
+        R["rf"] = rf_fit_measure(args, rank, world, threads)
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -408,9 +431,70 @@ def main():
         "clocks": R["clk"],
         "setup_s": round(W["build_s"], 2),
     }
+    if "rf" in R:
+        line["rf_fit"] = R["rf"]
     print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
+
+
+def rf_table(rows: int, seed: int = 3):
+    """BASELINE config #3 table: 64 U[0,1) columns (8 rounded to integers),
+    y = 30 + 40 x0 + 20 x1^2 + 12 [x2 > 0.5] + 0.003*20000 x3 + N(0,1)."""
+    rng = np.random.default_rng(seed)
+    X = rng.random((rows, 64))
+    X[:, 56:] = np.floor(X[:, 56:] * 20)
+    y = (30 + 40 * X[:, 0] + 20 * X[:, 1] ** 2 + 12 * (X[:, 2] > 0.5) + 0.003 * 20000 * X[:, 3]
+         + rng.normal(0, 1, rows))
+    X = (X - X.min(0)) / (X.max(0) - X.min(0))  # what MinMaxScaler hands the model
+    return X, y
+
+
+def rf_fit_measure(args, rank, world, threads):
+    """Config #3: GPU forest fit on 1M x 64, depth 16, `--rf-trees` trees sharded
+    by tree across ranks (time = max over ranks), extrapolated to 500 trees; plus
+    scikit-learn (the reference's own RF) and the GPU on the same bounded sample."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2305_01886_b200.forest import RandomForestRegressor
+
+    X, y = rf_table(args.rf_rows)
+    RandomForestRegressor(2, max_depth=4, random_state=0).fit(X[:4096], y[:4096])  # warm-up
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    m = RandomForestRegressor(args.rf_trees, max_depth=16, random_state=0,
+                              shard=(rank, world) if world > 1 else None).fit(X, y)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dt = float(t[0])
+    nodes = float(np.mean([e.tree_.node_count for e in m.estimators_ if e is not None]))
+    out = {"workload": f"BASELINE configs[2]: {args.rf_rows} x 64 table, depth 16, "
+                       f"{args.rf_trees} trees measured (tree-sharded over {world} GPU)",
+           "fit_s": dt, "s_per_tree": dt / args.rf_trees,
+           "fit_s_500_trees_extrapolated": dt * 500 / args.rf_trees,
+           "nodes_per_tree": nodes, "timing": "host wall clock around fit(), device synced"}
+    if rank == 0 and not args.no_cpu:
+        from sklearn.ensemble import RandomForestRegressor as SkRF
+
+        ns, ts = 100_000, 16
+        t0 = time.perf_counter()
+        SkRF(ts, max_depth=16, random_state=0, n_jobs=threads).fit(X[:ns].astype(np.float32), y[:ns])
+        cs = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        RandomForestRegressor(ts, max_depth=16, random_state=0).fit(X[:ns], y[:ns])
+        torch.cuda.synchronize()
+        gs = time.perf_counter() - t0
+        out["cpu_baseline"] = {"value": cs, "unit": "s", "cores": threads, "kind": "reference",
+                               "sample": f"scikit-learn {ts}-tree RandomForestRegressor fit, "
+                                         f"{ns} rows x 64, depth 16, n_jobs={threads}",
+                               "gpu_same_sample_s": gs}
+    return out
 
 
 def workload_name(args) -> str:
