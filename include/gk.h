@@ -148,6 +148,11 @@ typedef struct {
      * a non-NaN gm_override[c] replaces the piecewise global latency. */
     const int64_t   *n_tw_override;
     const double    *gm_override;
+    /* optional processing order of the grid's kernels (n_k entries, a
+     * permutation of 0..n_k-1; NULL = 0..n_k-1).  Outputs stay indexed by
+     * point; the order only balances the device's dynamic work queue
+     * (largest kernels first). */
+    const uint32_t  *order;
     uint32_t n_k, n_cfg, n_arch, pad_;
 } gk_grid;
 

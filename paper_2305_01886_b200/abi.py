@@ -19,7 +19,8 @@ class GkCorpus(C.Structure):
 
 class GkGrid(C.Structure):
     _fields_ = [("kernel_ids", P), ("cfg", P), ("arch", P), ("lat", P),
-                ("n_tw_override", P), ("gm_override", P), ("n_k", C.c_uint32), ("n_cfg", C.c_uint32), ("n_arch", C.c_uint32),
+                ("n_tw_override", P), ("gm_override", P), ("order", P),
+                ("n_k", C.c_uint32), ("n_cfg", C.c_uint32), ("n_arch", C.c_uint32),
                 ("pad_", C.c_uint32)]
 
 
@@ -41,4 +42,4 @@ SF_NAMES = ("gm_latency", "d_kernel", "overhead_cycles", "gm_penalty", "sm_penal
             "cm_penalty", "d_total", "time_us", "cfg_delay")
 STATUS_OK, STATUS_INFEASIBLE_LAUNCH, STATUS_INFEASIBLE_OCCUPANCY = 0, 1, 2
 
-assert C.sizeof(GkCorpus) == 72 and C.sizeof(GkGrid) == 64 and C.sizeof(GkEnsemble) == 64
+assert C.sizeof(GkCorpus) == 72 and C.sizeof(GkGrid) == 72 and C.sizeof(GkEnsemble) == 64

@@ -460,7 +460,8 @@ __device__ __forceinline__ void finish_point(const gk_corpus &C, const gk_grid &
 __global__ void __launch_bounds__(kWarps * 32, GK_K23_MINB) k23_schedule(
     gk_corpus C, gk_grid G, const gk_kstat *__restrict__ ks, const double *__restrict__ latsum,
     PointOut O, uint64_t n_items, uint32_t items_per_kernel, uint32_t ns,
-    double *__restrict__ gscratch, uint32_t g_rows, uint32_t max_blk) {
+    double *__restrict__ gscratch, uint32_t g_rows, uint32_t max_blk,
+    unsigned long long *__restrict__ queue) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const uint32_t n_arch = G.n_arch, n_sig = C.n_sig;
     ArchSmem *arch_s = reinterpret_cast<ArchSmem *>(smem_raw);
@@ -495,8 +496,15 @@ __global__ void __launch_bounds__(kWarps * 32, GK_K23_MINB) k23_schedule(
     const uint32_t P_k = n_arch * G.n_cfg;
     const double NaN = __longlong_as_double(0x7ff8000000000000ll);
 
-    for (uint64_t item = gwarp; item < n_items; item += n_warps) {
-        const uint32_t ki = (uint32_t)(item / items_per_kernel);
+    // dynamic work queue (items differ widely in cost; G.order puts the most
+    // expensive kernels first so the tail is short)
+    (void)n_warps;
+    unsigned long long item = 0;
+    if (lane == 0) item = atomicAdd(queue, 1ull);
+    item = __shfl_sync(GK_FULL, item, 0);
+    for (; item < n_items;) {
+        const uint32_t kr = (uint32_t)(item / items_per_kernel);
+        const uint32_t ki = G.order ? G.order[kr] : kr;
         const uint32_t j0 = (uint32_t)(item % items_per_kernel) * 32;
         PointScalars P;
         P.active = j0 + lane < P_k;
@@ -583,6 +591,9 @@ __global__ void __launch_bounds__(kWarps * 32, GK_K23_MINB) k23_schedule(
                     for (uint32_t q = 0; q < O.n_sel; q++) O.sel[P.p * O.n_sel + q] = NaN;
             }
         }
+        __syncwarp();
+        if (lane == 0) item = atomicAdd(queue, 1ull);
+        item = __shfl_sync(GK_FULL, item, 0);
     }
 }
 
@@ -640,7 +651,7 @@ size_t gk_sched_scratch_bytes(const gk_grid *G, uint32_t max_n, uint32_t max_blk
     (void)G;
     const size_t warps = (size_t)sm_count() * kMaxCtaPerSm * gk::kWarps;
     const size_t slab = (3 * (size_t)global_rows(max_n) + 2 * (size_t)max_blk) * 32;
-    return warps * slab * sizeof(double);
+    return warps * slab * sizeof(double) + 256;  // + the work-queue counter
 }
 
 int gk_launch_sched(const gk_corpus *C, const gk_grid *G, const gk_kstat *ks, const double *latsum,
@@ -692,7 +703,12 @@ int gk_launch_sched(const gk_corpus *C, const gk_grid *G, const gk_kstat *ks, co
     uint64_t grid = (uint64_t)sm_count() * per_sm;
     const uint64_t need = (n_items + gk::kWarps - 1) / gk::kWarps;
     if (grid > need) grid = need;
+    // work-queue counter lives past the per-warp slabs
+    const size_t warps_cap = (size_t)sm_count() * kMaxCtaPerSm * gk::kWarps;
+    unsigned long long *queue = reinterpret_cast<unsigned long long *>(
+        gscratch + warps_cap * (3 * (size_t)global_rows(max_n) + 2 * (size_t)max_blk) * 32);
+    cudaMemsetAsync(queue, 0, sizeof(unsigned long long), st);
     gk::k23_schedule<<<(unsigned)grid, gk::kWarps * 32, smem, st>>>(
-        *C, *G, ks, latsum, O, n_items, ipk, ns, gscratch, global_rows(max_n), max_blk);
+        *C, *G, ks, latsum, O, n_items, ipk, ns, gscratch, global_rows(max_n), max_blk, queue);
     return gk_check_launch("k23_schedule");
 }

@@ -150,9 +150,21 @@ class DeviceGrid:
             g.bufs["n_tw"] = _dev(np.asarray(n_tw, dtype=np.int64))
         if gm is not None:
             g.bufs["gm"] = _dev(np.asarray(gm, dtype=np.float64))
+        if len(kid) > 1:
+            # largest-first processing order for the device work queue: a
+            # kernel's scheduling cost grows with sum over blocks of n^2
+            blk = corpus.blk
+            n = blk["n"].astype(np.int64)
+            per_block = n * n + n
+            cost_all = np.add.reduceat(per_block, corpus.ker["blk0"].astype(np.int64)) \
+                if len(blk) else np.zeros(corpus.n_ker, np.int64)
+            cost_all = np.where(corpus.ker["n_blk"] > 0, cost_all, 0)
+            order = np.argsort(-cost_all[kid], kind="stable").astype(np.uint32)
+            g.bufs["order"] = _dev(order)
         g.desc = abi.GkGrid(_ptr(g.bufs["kid"]), _ptr(g.bufs["cfg"]), _ptr(g.bufs["arch"]),
                             _ptr(g.bufs["lat"]), _ptr(g.bufs.get("n_tw")),
-                            _ptr(g.bufs.get("gm")), len(kid), len(cfg), len(arch), 0)
+                            _ptr(g.bufs.get("gm")), _ptr(g.bufs.get("order")), len(kid),
+                            len(cfg), len(arch), 0)
         return g
 
     @property
