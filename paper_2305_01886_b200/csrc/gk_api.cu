@@ -1,6 +1,7 @@
 // gk_api.cu -- the C-ABI of libgk (declared in include/gk.h).
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "gk_internal.cuh"
@@ -31,6 +32,20 @@ int gk_launch_sched(const gk_corpus *, const gk_grid *, const gk_kstat *, const 
                     const gk_trace *, uint32_t, uint32_t, double *, cudaStream_t);
 int gk_launch_rf(const gk_ensemble *, uint32_t, const double *, int64_t, int64_t, const uint8_t *,
                  const double *, double *, double *, uint32_t, uint32_t, cudaStream_t);
+int gk_launch_sweep_fused(const gk_corpus *, const gk_grid *, const gk_kstat *, const double *,
+                          const gk_ensemble *, uint32_t, const int32_t *, uint32_t, uint8_t *,
+                          double *, double *, double *, uint32_t, uint32_t, double *,
+                          cudaStream_t);
+
+// GK_SWEEP_FUSED=0 selects the two-kernel sweep (K3 then K4) for A/B measurements
+static bool sweep_fused() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("GK_SWEEP_FUSED");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
 
 namespace {
 
@@ -194,6 +209,16 @@ int gk_predict_energy_sweep(const gk_corpus *corpus, const gk_grid *grid,
     const uint32_t max_blk = corpus->max_blk ? corpus->max_blk : 1;
     void *ws = nullptr;
     if (int rc = scratch(gk_sched_scratch_bytes(grid, max_n, max_blk), &ws)) return rc;
+    if (sweep_fused()) {
+        // one kernel: schedule + features + ensemble walk + energy per warp of points
+        if (int rc = gk_launch_sweep_fused(corpus, grid, ks, latsum, ens_host, grid->n_arch,
+                                           sel_idx, n_sel, out_status, out_time_us, out_power,
+                                           out_energy, max_n, max_blk, (double *)ws, st))
+            return rc;
+        stage_mark(2, st);
+        stage_mark(3, st);
+        return 0;
+    }
     if (int rc = gk_launch_sched(corpus, grid, ks, latsum, out_status, nullptr, nullptr, nullptr,
                                  sel_idx, n_sel, sel, out_time_us, nullptr, max_n, max_blk,
                                  (double *)ws, st))

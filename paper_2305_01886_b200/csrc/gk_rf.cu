@@ -12,14 +12,11 @@
 // running total strictly in tree order, so the fp64 sum is bit-identical to
 // the reference's sequential `total += leaf`.
 #include "gk_internal.cuh"
+#include "gk_walk.cuh"
 
 namespace gk {
 
 constexpr int kRfThreads = 128;
-#ifndef GK_RF_ILP
-#define GK_RF_ILP 8  // trees walked in lock-step per thread (8 measured best on B200)
-#endif
-constexpr int kIlp = GK_RF_ILP;
 constexpr int kMaxFeat = 64;
 
 struct RfArgs {
@@ -93,57 +90,9 @@ __global__ void __launch_bounds__(kRfThreads) k4_rf_predict(RfArgs R) {
     // lane-varying f are then bank-conflict-free
     double *xr = xs + (size_t)threadIdx.x * nf;
     double *xt = xs + (size_t)kRfThreads * nf;
-    for (uint32_t f = 0; f < nf; f++) {
-        const double lo = E.scale_lo[f], hi = E.scale_hi[f];
-        xt[f * kRfThreads + threadIdx.x] =
-            hi > lo ? __ddiv_rn(__dsub_rn(xr[f], lo), __dsub_rn(hi, lo)) : 0.0;
-    }
-    const double *x = xt + threadIdx.x;
-#define XF(f) x[(size_t)(f) * kRfThreads]
-    // Branch-free descent: kIlp trees in lock-step for max(depth) steps; a
-    // leaf's `left` is itself so finished walks stay put.  Same comparisons
-    // (x <= threshold goes left) and the same leaves as the reference walk.
-    const gk_node *__restrict__ nodes = E.nodes;
-    double total = E.base_score;
-    uint32_t t = 0;
-    for (; t + kIlp <= E.n_trees; t += kIlp) {
-        const gk_node *base[kIlp];
-        int32_t idx[kIlp];
-        double v[kIlp];
-        int d = 0;
-#pragma unroll
-        for (int q = 0; q < kIlp; q++) {
-            base[q] = nodes + __ldg(E.tree_off + t + q);
-            idx[q] = 0;
-            d = max(d, __ldg(E.tree_depth + t + q));
-        }
-        for (int s = 0; s <= d; s++) {
-#pragma unroll
-            for (int q = 0; q < kIlp; q++) {
-                const double2 raw = __ldg(reinterpret_cast<const double2 *>(base[q] + idx[q]));
-                const int f = __double2loint(raw.y), l = __double2hiint(raw.y);
-                v[q] = raw.x;
-                const bool left = f < 0 || XF(f < 0 ? 0 : f) <= raw.x;
-                idx[q] = left ? l : l + 1;
-            }
-        }
-#pragma unroll
-        for (int q = 0; q < kIlp; q++) total = __dadd_rn(total, v[q]);  // tree order
-    }
-    for (; t < E.n_trees; t++) {
-        const gk_node *b = nodes + E.tree_off[t];
-        int32_t i = 0;
-        while (true) {
-            const double2 raw = __ldg(reinterpret_cast<const double2 *>(b + i));
-            const int f = __double2loint(raw.y), l = __double2hiint(raw.y);
-            if (f < 0) {
-                total = __dadd_rn(total, raw.x);
-                break;
-            }
-            i = XF(f) <= raw.x ? l : l + 1;
-        }
-    }
-#undef XF
+    for (uint32_t f = 0; f < nf; f++)
+        xt[f * kRfThreads + threadIdx.x] = scale_feature(xr[f], E.scale_lo[f], E.scale_hi[f]);
+    const double total = walk_ensemble(E, xt + threadIdx.x, kRfThreads);
     R.power[row] = total;
     if (R.energy) R.energy[row] = __dmul_rn(total, R.time_us[row]);
 }

@@ -17,6 +17,7 @@
 #include <stdlib.h>
 
 #include "gk_internal.cuh"
+#include "gk_walk.cuh"
 
 namespace gk {
 
@@ -28,6 +29,9 @@ constexpr int kWarps = 4;            // warps per CTA (each warp: 32 points of o
 // measured (tools/sweep_variants.sh, B200): 0% carveout (max L1 for the
 // reservation tables) beats a carveout sized for more resident CTAs
 #define GK_K23_CARVE 0  // >= 0: percent; -1: driver default; -2: just enough for the CTAs
+#endif
+#ifndef GK_K23_FUSED_CARVE
+#define GK_K23_FUSED_CARVE -1  // fused sweep carveout (percent); -1: computed like -2
 #endif
 
 // ------------------------------------------------------------------ K1
@@ -291,11 +295,16 @@ __device__ __forceinline__ double schedule_block(const gk_corpus &C, const gk_bl
     return delay;
 }
 
-__device__ __forceinline__ void finish_point(const gk_corpus &C, const gk_grid &G,
-                                             const gk_kstat *__restrict__ ks,
-                                             const double *__restrict__ latsum,
-                                             const gk_kernel &K, const PointScalars &P,
-                                             double cfg_delay, const PointOut &O) {
+// Returns time_us when the point is fully valid (status OK), else NaN.  In the
+// fused sweep, `xw` (this lane's column of the warp's feature tile, stride 32)
+// receives the manifest features already scaled by ensemble `E` (power.py:144).
+__device__ __forceinline__ double finish_point(const gk_corpus &C, const gk_grid &G,
+                                               const gk_kstat *__restrict__ ks,
+                                               const double *__restrict__ latsum,
+                                               const gk_kernel &K, const PointScalars &P,
+                                               double cfg_delay, const PointOut &O,
+                                               double *xw = nullptr,
+                                               const gk_ensemble *E = nullptr) {
     const gk_arch &A = G.arch[P.ai];
     const gk_config c = G.cfg[P.ci];
     const gk_kstat S = ks[P.ki];
@@ -360,15 +369,16 @@ __device__ __forceinline__ void finish_point(const gk_corpus &C, const gk_grid &
         sf[GK_SF_TIME_US] = __ddiv_rn(d_total, A.nu_gpu);
         sf[GK_SF_CFG_DELAY] = cfg_delay;
     }
-    if (O.time_us) O.time_us[p] = __ddiv_rn(d_total, A.nu_gpu);
-    if (!O.feat && !O.sel) return;
+    const double time_us = __ddiv_rn(d_total, A.nu_gpu);
+    if (O.time_us) O.time_us[p] = time_us;
     const double NaN = __longlong_as_double(0x7ff8000000000000ll);
+    if (!O.feat && !O.sel && !xw) return status == GK_OK ? time_us : NaN;
     if (status != GK_OK) {
         if (O.feat)
             for (int j = 0; j < GK_NFEAT; j++) O.feat[p * GK_NFEAT + j] = NaN;
         if (O.sel)
             for (uint32_t j = 0; j < O.n_sel; j++) O.sel[p * O.n_sel + j] = NaN;
-        return;
+        return NaN;
     }
     // extract_features (features.py:149-247)
     const double *ls = latsum + ((size_t)P.ai * G.n_k + P.ki) * 3;
@@ -450,18 +460,33 @@ __device__ __forceinline__ void finish_point(const gk_corpus &C, const gk_grid &
         double *o = O.sel + p * O.n_sel;
         for (uint32_t j = 0; j < O.n_sel; j++) o[j] = feature(O.sel_idx[j]);
     }
+    if (xw)
+        for (uint32_t j = 0; j < O.n_sel; j++)
+            xw[(size_t)j * 32] = scale_feature(feature(O.sel_idx[j]), E->scale_lo[j], E->scale_hi[j]);
+    return time_us;
 }
 
+
+// Fused sweep (K2/K3 -> K4 -> K6 in one kernel): after a warp's 32 points are
+// scheduled and their features composed, the same lanes walk their arch's
+// ensemble.  Warps in the latency-bound scheduling phase and warps in the
+// L1-bound walk phase then share each SM.
+struct FusedArgs {
+    gk_ensemble ens[4];
+    uint32_t n_ens;
+    double *power, *energy;
+};
 
 // Persistent warps over work items (kernel, up to 32 consecutive (arch, config) pairs).
 #ifndef GK_K23_MINB
 #define GK_K23_MINB 6
 #endif
+template <bool kFused>
 __global__ void __launch_bounds__(kWarps * 32, GK_K23_MINB) k23_schedule(
     gk_corpus C, gk_grid G, const gk_kstat *__restrict__ ks, const double *__restrict__ latsum,
     PointOut O, uint64_t n_items, uint32_t items_per_kernel, uint32_t ns,
     double *__restrict__ gscratch, uint32_t g_rows, uint32_t max_blk,
-    unsigned long long *__restrict__ queue) {
+    unsigned long long *__restrict__ queue, FusedArgs F) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const uint32_t n_arch = G.n_arch, n_sig = C.n_sig;
     ArchSmem *arch_s = reinterpret_cast<ArchSmem *>(smem_raw);
@@ -495,6 +520,8 @@ __global__ void __launch_bounds__(kWarps * 32, GK_K23_MINB) k23_schedule(
     double *blk_finish = blk_delay + (size_t)max_blk * 32;
     const uint32_t P_k = n_arch * G.n_cfg;
     const double NaN = __longlong_as_double(0x7ff8000000000000ll);
+    // fused: per-warp [n_sel][32] tile of scaled manifest features after the slabs
+    double *xw = slab_base + (size_t)kWarps * 3 * ns * 32 + (size_t)warp * O.n_sel * 32 + lane;
 
     // dynamic work queue (items differ widely in cost; G.order puts the most
     // expensive kernels first so the tail is short)
@@ -575,9 +602,11 @@ __global__ void __launch_bounds__(kWarps * 32, GK_K23_MINB) k23_schedule(
                 O.trace.blk_finish[P.p * K.n_blk + b] = ROW(blk_finish, b);
             }
         }
+        double t_ok = NaN;  // time_us of a fully valid point, else NaN
+        const gk_ensemble *Ep = kFused ? &F.ens[P.ai < F.n_ens ? P.ai : 0] : nullptr;
         if (P.active) {
             if (feasible) {
-                finish_point(C, G, ks, latsum, K, P, cfg_delay, O);
+                t_ok = finish_point(C, G, ks, latsum, K, P, cfg_delay, O, kFused ? xw : nullptr, Ep);
             } else {
                 if (O.status) O.status[P.p] = GK_INFEASIBLE_LAUNCH;
                 if (O.si)
@@ -589,6 +618,17 @@ __global__ void __launch_bounds__(kWarps * 32, GK_K23_MINB) k23_schedule(
                     for (int q = 0; q < GK_NFEAT; q++) O.feat[P.p * GK_NFEAT + q] = NaN;
                 if (O.sel)
                     for (uint32_t q = 0; q < O.n_sel; q++) O.sel[P.p * O.n_sel + q] = NaN;
+            }
+        }
+        if constexpr (kFused) {  // K4 + K6 for this lane's point
+            if (P.active) {
+                double pw = NaN, en = NaN;
+                if (!isnan(t_ok)) {
+                    pw = walk_ensemble(*Ep, xw, 32);
+                    en = __dmul_rn(pw, t_ok);
+                }
+                F.power[P.p] = pw;
+                F.energy[P.p] = en;
             }
         }
         __syncwarp();
@@ -654,10 +694,13 @@ size_t gk_sched_scratch_bytes(const gk_grid *G, uint32_t max_n, uint32_t max_blk
     return warps * slab * sizeof(double) + 256;  // + the work-queue counter
 }
 
-int gk_launch_sched(const gk_corpus *C, const gk_grid *G, const gk_kstat *ks, const double *latsum,
-                    uint8_t *status, int64_t *si, double *sf, double *feat, const int32_t *sel_idx,
-                    uint32_t n_sel, double *sel, double *time_us, const gk_trace *trace,
-                    uint32_t max_n, uint32_t max_blk, double *gscratch, cudaStream_t st) {
+template <bool kFused>
+static int launch_sched(const gk_corpus *C, const gk_grid *G, const gk_kstat *ks,
+                        const double *latsum, uint8_t *status, int64_t *si, double *sf,
+                        double *feat, const int32_t *sel_idx, uint32_t n_sel, double *sel,
+                        double *time_us, const gk_trace *trace, uint32_t max_n, uint32_t max_blk,
+                        double *gscratch, const gk::FusedArgs &F, cudaStream_t st) {
+    const auto kern = gk::k23_schedule<kFused>;
     const uint64_t P_k = (uint64_t)G->n_arch * G->n_cfg;
     if (G->n_k == 0 || P_k == 0) return 0;
     const uint32_t ipk = (uint32_t)((P_k + 31) / 32);
@@ -676,10 +719,10 @@ int gk_launch_sched(const gk_corpus *C, const gk_grid *G, const gk_kstat *ks, co
     else memset(&O.trace, 0, sizeof O.trace);
     const uint32_t ns = smem_rows(max_n);
     const size_t smem = G->n_arch * (sizeof(gk::ArchSmem) + (size_t)C->n_sig * sizeof(double)) +
-                        (size_t)gk::kWarps * 3 * ns * 32 * sizeof(double);
+                        (size_t)gk::kWarps * 3 * ns * 32 * sizeof(double) +
+                        (kFused ? (size_t)gk::kWarps * n_sel * 32 * sizeof(double) : 0);
     if (smem > 48 * 1024) {
-        cudaFuncSetAttribute(gk::k23_schedule, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     }
     // the reservation tables that do not fit the shared slab live in L1: prefer L1
     // (a 0% carveout caps resident CTAs at 5/SM even for ~1 KB of tables: ask
@@ -688,13 +731,15 @@ int gk_launch_sched(const gk_corpus *C, const gk_grid *G, const gk_kstat *ks, co
         const size_t per_sm_bytes = (smem + 1024) * 8;
         int carve = (int)((per_sm_bytes * 100 + 228 * 1024 - 1) / (228 * 1024));
         if (carve > 100) carve = 100;
+        const int computed = carve;
         if (GK_K23_CARVE >= 0) carve = GK_K23_CARVE;
-        if (GK_K23_CARVE != -1)
-            cudaFuncSetAttribute(gk::k23_schedule, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                 carve);
+        // the fused kernel needs shared memory for its feature tiles
+        if (kFused) carve = GK_K23_FUSED_CARVE >= 0 ? GK_K23_FUSED_CARVE : computed;
+        if (GK_K23_CARVE != -1 || kFused)
+            cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
     }
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gk::k23_schedule, gk::kWarps * 32, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, gk::kWarps * 32, smem);
     if (per_sm < 1) {
         gk_set_error("k23_schedule: %zu B shared memory per CTA does not fit", smem);
         return -1;
@@ -708,7 +753,45 @@ int gk_launch_sched(const gk_corpus *C, const gk_grid *G, const gk_kstat *ks, co
     unsigned long long *queue = reinterpret_cast<unsigned long long *>(
         gscratch + warps_cap * (3 * (size_t)global_rows(max_n) + 2 * (size_t)max_blk) * 32);
     cudaMemsetAsync(queue, 0, sizeof(unsigned long long), st);
-    gk::k23_schedule<<<(unsigned)grid, gk::kWarps * 32, smem, st>>>(
-        *C, *G, ks, latsum, O, n_items, ipk, ns, gscratch, global_rows(max_n), max_blk, queue);
-    return gk_check_launch("k23_schedule");
+    kern<<<(unsigned)grid, gk::kWarps * 32, smem, st>>>(*C, *G, ks, latsum, O, n_items, ipk, ns,
+                                                         gscratch, global_rows(max_n), max_blk,
+                                                         queue, F);
+    return gk_check_launch(kFused ? "k23_schedule<fused>" : "k23_schedule");
+}
+
+int gk_launch_sched(const gk_corpus *C, const gk_grid *G, const gk_kstat *ks, const double *latsum,
+                    uint8_t *status, int64_t *si, double *sf, double *feat, const int32_t *sel_idx,
+                    uint32_t n_sel, double *sel, double *time_us, const gk_trace *trace,
+                    uint32_t max_n, uint32_t max_blk, double *gscratch, cudaStream_t st) {
+    gk::FusedArgs F;
+    memset(&F, 0, sizeof F);
+    return launch_sched<false>(C, G, ks, latsum, status, si, sf, feat, sel_idx, n_sel, sel,
+                               time_us, trace, max_n, max_blk, gscratch, F, st);
+}
+
+// fused sweep: schedule + features + ensemble walk + energy in one kernel
+int gk_launch_sweep_fused(const gk_corpus *C, const gk_grid *G, const gk_kstat *ks,
+                          const double *latsum, const gk_ensemble *ens, uint32_t n_ens,
+                          const int32_t *sel_idx, uint32_t n_sel, uint8_t *status,
+                          double *time_us, double *power, double *energy, uint32_t max_n,
+                          uint32_t max_blk, double *gscratch, cudaStream_t st) {
+    if (n_ens < 1 || n_ens > 4 || n_sel < 1 || n_sel > 64) {
+        gk_set_error("fused sweep: 1..4 ensembles and 1..64 manifest features");
+        return -1;
+    }
+    gk::FusedArgs F;
+    memset(&F, 0, sizeof F);
+    for (uint32_t a = 0; a < n_ens; a++) {
+        if (ens[a].n_feat != n_sel) {
+            gk_set_error("fused sweep: ensemble %u has %u features, manifest has %u", a,
+                         ens[a].n_feat, n_sel);
+            return -1;
+        }
+        F.ens[a] = ens[a];
+    }
+    F.n_ens = n_ens;
+    F.power = power;
+    F.energy = energy;
+    return launch_sched<true>(C, G, ks, latsum, status, nullptr, nullptr, nullptr, sel_idx, n_sel,
+                              nullptr, time_us, nullptr, max_n, max_blk, gscratch, F, st);
 }

@@ -54,6 +54,17 @@ if os.environ.get("RF", "1") == "1":
     e1.record()
     torch.cuda.synchronize()
     res["k4"] = e0.elapsed_time(e1) / 5
+    sw = rt.Sweep(dc, dg, [de], sel)
+    for _ in range(2):
+        sw.run()
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(5):
+        sw.run()
+    e1.record()
+    torch.cuda.synchronize()
+    res["sweep"] = e0.elapsed_time(e1) / 5
+    res["fused"] = os.environ.get("GK_SWEEP_FUSED", "1")
 res["smem_rows"] = os.environ.get("GK_SMEM_ROWS", "default")
 res["points"] = dg.n_points
 print(json.dumps(res))
