@@ -158,9 +158,10 @@ typedef struct {
 
 /* Flattened tree ensemble (power.py:22-33).  Node = 16 B: for a split,
  * {threshold, feature, left} with right = left + 1; for a leaf,
- * {value, -1, self} -- a leaf's `left` is its own index, so a fixed number of
- * descent steps absorbs at the leaf.  Child indices are tree-local; trees are
- * contiguous from tree_off[t]; tree_depth[t] is the depth of tree t. */
+ * {value, -1, self - 1} -- the walk reads feature -1 as +inf, +inf <= value is
+ * false, so the step goes "right" to the leaf itself: a fixed number of descent
+ * steps absorbs at the leaf without a leaf test.  Child indices are tree-local;
+ * trees are contiguous from tree_off[t]; tree_depth[t] is the depth of tree t. */
 typedef struct { double v; int32_t feature; int32_t left; } gk_node;
 
 typedef struct {

@@ -89,7 +89,8 @@ __global__ void __launch_bounds__(kRfThreads) k4_rf_predict(RfArgs R) {
     // scale and transpose to [feature][thread]: the per-visit reads x[f] with a
     // lane-varying f are then bank-conflict-free
     double *xr = xs + (size_t)threadIdx.x * nf;
-    double *xt = xs + (size_t)kRfThreads * nf;
+    double *xt = xs + (size_t)kRfThreads * (nf + 1);  // row -1 of the tile = +inf (leaf slot)
+    xt[threadIdx.x - kRfThreads] = __longlong_as_double(0x7ff0000000000000ll);
     for (uint32_t f = 0; f < nf; f++)
         xt[f * kRfThreads + threadIdx.x] = scale_feature(xr[f], E.scale_lo[f], E.scale_hi[f]);
     const double total = walk_ensemble(E, xt + threadIdx.x, kRfThreads);
@@ -131,7 +132,8 @@ int gk_launch_rf(const gk_ensemble *ens, uint32_t n_ens, const double *X, int64_
     R.energy = energy;
     R.n_cfg = n_cfg;
     R.n_arch = n_arch ? n_arch : 1;
-    const size_t smem = 2 * (size_t)gk::kRfThreads * nf * sizeof(double);  // tile + transposed
+    // row tile + transposed tile with one leading +inf row
+    const size_t smem = (2 * (size_t)nf + 1) * gk::kRfThreads * sizeof(double);
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(gk::k4_rf_predict, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);

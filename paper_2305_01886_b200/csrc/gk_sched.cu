@@ -521,7 +521,10 @@ __global__ void __launch_bounds__(kWarps * 32, GK_K23_MINB) k23_schedule(
     const uint32_t P_k = n_arch * G.n_cfg;
     const double NaN = __longlong_as_double(0x7ff8000000000000ll);
     // fused: per-warp [n_sel][32] tile of scaled manifest features after the slabs
-    double *xw = slab_base + (size_t)kWarps * 3 * ns * 32 + (size_t)warp * O.n_sel * 32 + lane;
+    // (row 0 of each warp's tile is the +inf leaf slot; features start at row 1)
+    double *xw = slab_base + (size_t)kWarps * 3 * ns * 32 + (size_t)warp * (O.n_sel + 1) * 32 +
+                 32 + lane;
+    if (kFused) xw[-32] = __longlong_as_double(0x7ff0000000000000ll);
 
     // dynamic work queue (items differ widely in cost; G.order puts the most
     // expensive kernels first so the tail is short)
@@ -720,7 +723,7 @@ static int launch_sched(const gk_corpus *C, const gk_grid *G, const gk_kstat *ks
     const uint32_t ns = smem_rows(max_n);
     const size_t smem = G->n_arch * (sizeof(gk::ArchSmem) + (size_t)C->n_sig * sizeof(double)) +
                         (size_t)gk::kWarps * 3 * ns * 32 * sizeof(double) +
-                        (kFused ? (size_t)gk::kWarps * n_sel * 32 * sizeof(double) : 0);
+                        (kFused ? (size_t)gk::kWarps * (n_sel + 1) * 32 * sizeof(double) : 0);
     if (smem > 48 * 1024) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     }

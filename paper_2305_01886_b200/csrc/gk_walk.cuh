@@ -14,7 +14,9 @@
 
 namespace gk {
 
-// x: this row's scaled features, feature f at x[f * stride]
+// x: this row's scaled features, feature f at x[f * stride], and x[-stride]
+// must hold +inf: a leaf {value, -1, self - 1} then compares +inf <= value
+// (false) and steps "right" to itself, so walks absorb without a leaf test.
 __device__ __forceinline__ double walk_ensemble(const gk_ensemble &E, const double *x,
                                                 int stride) {
     constexpr int kIlp = GK_RF_ILP;
@@ -38,8 +40,7 @@ __device__ __forceinline__ double walk_ensemble(const gk_ensemble &E, const doub
                 const double2 raw = __ldg(reinterpret_cast<const double2 *>(base[q] + idx[q]));
                 const int f = __double2loint(raw.y), l = __double2hiint(raw.y);
                 v[q] = raw.x;
-                const bool left = f < 0 || x[(size_t)(f < 0 ? 0 : f) * stride] <= raw.x;
-                idx[q] = left ? l : l + 1;
+                idx[q] = x[f * stride] <= raw.x ? l : l + 1;
             }
         }
 #pragma unroll
@@ -55,7 +56,7 @@ __device__ __forceinline__ double walk_ensemble(const gk_ensemble &E, const doub
                 total = __dadd_rn(total, raw.x);
                 break;
             }
-            i = x[(size_t)f * stride] <= raw.x ? l : l + 1;
+            i = x[f * stride] <= raw.x ? l : l + 1;
         }
     }
     return total;

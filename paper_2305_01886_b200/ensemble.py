@@ -129,7 +129,7 @@ def load_ensemble(source) -> TreeEnsemble:
 class FlatEnsemble:
     """Device layout of one ensemble (host numpy arrays)."""
 
-    nodes: np.ndarray      # NODE_DT; a leaf's `left` is its own index (absorbing)
+    nodes: np.ndarray      # NODE_DT; a leaf is {value, -1, own index - 1} (absorbing)
     tree_off: np.ndarray   # int64 [n_trees]
     scale_lo: np.ndarray   # f64 [n_feat]
     scale_hi: np.ndarray
@@ -160,7 +160,7 @@ def _flatten_tree(nodes) -> tuple[np.ndarray, int]:
     while k < len(order):
         nd = nodes[order[k]]
         if "value" in nd:
-            out[k] = (float(nd["value"]), -1, k)   # absorbing leaf
+            out[k] = (float(nd["value"]), -1, k - 1)   # absorbing leaf: right = self
         else:
             left = len(order)
             order.append(nd["left"])
@@ -230,7 +230,7 @@ def random_forest_flat(n_trees: int, depth: int, manifest, scale_lo, scale_hi, s
             arr["left"][sp] = nxt + 2 * np.arange(len(sp))
             lf = idx[~split]
             arr["feature"][lf] = -1
-            arr["left"][lf] = lf                      # absorbing leaf
+            arr["left"][lf] = lf - 1                  # absorbing leaf: right = self
             arr["v"][lf] = (30.0 + 120.0 * rng.random(len(lf))) * scale
             base = nxt
         parts.append(arr)

@@ -380,7 +380,7 @@ class RandomForestRegressor:
             split = t.children_left >= 0
             arr["v"] = np.where(split, t.threshold, t.value[:, 0, 0] * leaf_scale)
             arr["feature"] = np.where(split, t.feature, -1)
-            arr["left"] = np.where(split, t.children_left, np.arange(t.node_count))
+            arr["left"] = np.where(split, t.children_left, np.arange(t.node_count) - 1)
             parts.append(arr)
             offs.append(off)
             depths.append(t.max_depth)
