@@ -481,8 +481,14 @@ struct FusedArgs {
 #ifndef GK_K23_MINB
 #define GK_K23_MINB 6
 #endif
+#ifndef GK_FUSED_MINB
+#define GK_FUSED_MINB 6
+#endif
+#ifndef GK_FUSED_ILP
+#define GK_FUSED_ILP 4  // trees walked in lock-step inside the fused sweep
+#endif
 template <bool kFused>
-__global__ void __launch_bounds__(kWarps * 32, GK_K23_MINB) k23_schedule(
+__global__ void __launch_bounds__(kWarps * 32, kFused ? GK_FUSED_MINB : GK_K23_MINB) k23_schedule(
     gk_corpus C, gk_grid G, const gk_kstat *__restrict__ ks, const double *__restrict__ latsum,
     PointOut O, uint64_t n_items, uint32_t items_per_kernel, uint32_t ns,
     double *__restrict__ gscratch, uint32_t g_rows, uint32_t max_blk,
@@ -627,7 +633,7 @@ __global__ void __launch_bounds__(kWarps * 32, GK_K23_MINB) k23_schedule(
             if (P.active) {
                 double pw = NaN, en = NaN;
                 if (!isnan(t_ok)) {
-                    pw = walk_ensemble(*Ep, xw, 32);
+                    pw = walk_ensemble<GK_FUSED_ILP>(*Ep, xw, 32);
                     en = __dmul_rn(pw, t_ok);
                 }
                 F.power[P.p] = pw;

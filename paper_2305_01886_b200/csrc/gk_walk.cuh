@@ -17,9 +17,9 @@ namespace gk {
 // x: this row's scaled features, feature f at x[f * stride], and x[-stride]
 // must hold +inf: a leaf {value, -1, self - 1} then compares +inf <= value
 // (false) and steps "right" to itself, so walks absorb without a leaf test.
+template <int kIlp = GK_RF_ILP>
 __device__ __forceinline__ double walk_ensemble(const gk_ensemble &E, const double *x,
                                                 int stride) {
-    constexpr int kIlp = GK_RF_ILP;
     const gk_node *__restrict__ nodes = E.nodes;
     double total = E.base_score;
     uint32_t t = 0;
