@@ -321,8 +321,9 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2", choices=["c2", "c5s"])
+    ap.add_argument("--workload", default="c2", choices=["c2", "c4", "c5s"])
     ap.add_argument("--kernels", type=int, default=0)
+    ap.add_argument("--rows", type=int, default=0, help="c4: total rows (default 100M)")
     ap.add_argument("--trees", type=int, default=500)
     ap.add_argument("--depth", type=int, default=16)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -374,6 +375,11 @@ def main():
 
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    if args.workload == "c4":
+        run_c4(args, rank, world, local_rank, threads)
+        if world > 1:
+            dist.destroy_process_group()
+        return
     R = run_ours(args, rank, world, local_rank)
     if not args.no_rf:
         R["rf"] = rf_fit_measure(args, rank, world, threads)
@@ -397,6 +403,9 @@ def main():
         "k1_static": R["dc_bytes"] + W["n_k"] * (64 + 24),
         "k23_schedule": R["dc_bytes"] + W["n_k"] * (64 + 24) + n_pts * (1 + 8 * 9 + 8 * nsel),
         "k4_rf_predict": ens_bytes * len(R["flats"]) + n_pts * (8 * nsel + 1 + 8 + 16),
+        # fused: corpus + configs once, ensemble once, status + time + power + energy out
+        "k23_schedule<fused>": R["dc_bytes"] + W["n_k"] * (64 + 24)
+        + ens_bytes * len(R["flats"]) + n_pts * (1 + 8 * 3),
     }
     peak, peak_kind = hbm_peak()
     achieved = alg[dom] / (split[dom] / 1e3) / 1e9
@@ -420,7 +429,7 @@ def main():
                    "infeasible_points": R["infeasible"], "parallelism": f"dp{world} (kernel shards)"},
         "e2e": {"value": e2e_value, "unit": "points/s", "h2d_bytes_per_step": R["e2e"]["h2d"],
                 "d2h_bytes_per_step": R["e2e"]["d2h"]},
-        "gpu_launches": 3 * args.steps,
+        "gpu_launches": len(split) * args.steps,
         "kernel_ms": split,
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
@@ -436,6 +445,90 @@ def main():
     print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_c4(args, rank, world, local_rank, threads):
+    """BASELINE configs[3]: batched inference of a 500-tree depth-16 ensemble over
+    100M feature rows x 64 (fp64, 51 GB resident in HBM), rows sharded over ranks.
+    Rows are generated on the device (U[0,1) like config #3's table); the ensemble
+    is the declared random one (~110k nodes/tree).  A step = one pass of K4 over
+    the GPU's rows; metric rows/s (+ HBM GB/s of the row stream)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2305_01886_b200 import runtime as rt
+    from paper_2305_01886_b200.ensemble import random_forest_flat
+
+    torch.cuda.set_device(local_rank)
+    n = (args.rows or 100_000_000) // world
+    F = 64
+    g = torch.Generator(device="cuda").manual_seed(4 + rank)
+    X = torch.rand((n, F), dtype=torch.float64, device="cuda", generator=g)
+    flat = random_forest_flat(args.trees, args.depth, [f"f{i}" for i in range(F)], np.zeros(F),
+                              np.ones(F), seed=11)
+    de = rt.DeviceEnsemble.upload(flat)
+    power = torch.empty(n, dtype=torch.float64, device="cuda")
+    L = rt.load_library()
+    import ctypes
+
+    def step():
+        rt._check(L.gk_rf_predict(ctypes.byref(de.desc), X.data_ptr(), F, n, None, None,
+                                  power.data_ptr(), None, torch.cuda.current_stream().cuda_stream))
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    with ClockSampler(local_rank) as clk:
+        t0 = time.perf_counter()
+        for k in range(args.steps):
+            evs[k][0].record()
+            step()
+            evs[k][1].record()
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        time.sleep(0.25)
+    clk.window(t0, t1)
+    ms = sum(a.elapsed_time(b) for a, b in evs)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t[0])
+    if rank != 0:
+        return
+    rows_total = n * world
+    value = rows_total * args.steps / (ms / 1e3)
+    alg = n * (8 * F + 8) + flat.nodes.nbytes  # rows in + power out + ensemble once
+    achieved = alg / (ms / args.steps / 1e3) / 1e9
+    peak, peak_kind = hbm_peak()
+    line = {"metric": "RF inference rows/sec", "value": value, "unit": "rows/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "BASELINE configs[3]: 500-tree depth-16 ensemble over "
+                                   f"{rows_total} rows x 64 fp64",
+                       "ensemble": f"{args.trees} trees depth {args.depth} "
+                                   f"({len(flat.nodes) // flat.n_trees} nodes/tree, declared random)",
+                       "rows_per_gpu": n, "l2": "rows (51 GB) >> L2"},
+            "gpu_launches": args.steps,
+            "roofline": {"bound": "hbm", "kernel": "k4_rf_predict", "achieved": achieved,
+                         "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                         "frac": achieved / peak, "algorithmic_bytes": alg, "traffic": None},
+            "clocks": clk.summary()}
+    if not args.no_cpu:
+        import oracle as O
+
+        ns = 20000
+        Xs = X[:ns].cpu().numpy()
+        t0 = time.perf_counter()
+        O.rf_predict(flat, Xs, threads=threads)
+        cs = time.perf_counter() - t0
+        line["cpu_baseline"] = {"value": ns / cs, "unit": "rows/s", "cores": threads,
+                                "kind": "port", "sample": f"{ns} rows, oracle walk"}
+    print(json.dumps(line))
 
 
 def rf_table(rows: int, seed: int = 3):

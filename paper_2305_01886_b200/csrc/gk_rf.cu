@@ -41,18 +41,26 @@ __device__ __forceinline__ void bulk_g2s(void *smem_dst, const void *gsrc, uint3
         : "memory");
 }
 
+// kMaxF: compile-time bound on the feature count for the in-place transpose
+// through registers (16 or 32); 0 = no staging, rows read straight from global.
+template <int kMaxF>
 __global__ void __launch_bounds__(kRfThreads) k4_rf_predict(RfArgs R) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t bar;
     const int64_t row0 = (int64_t)blockIdx.x * kRfThreads;
     const int64_t nr = min((int64_t)kRfThreads, R.n_rows - row0);
     const uint32_t nf = R.ens[0].n_feat;
-    double *xs = reinterpret_cast<double *>(smem_raw);  // [kRfThreads][ld] raw, then scaled
+    // one tile: row -1 = +inf (leaf slot), rows 0..nf-1 = [feature][thread]; the
+    // raw [thread][feature] rows are staged into rows 0.. and transposed in place
+    double *xt = reinterpret_cast<double *>(smem_raw) + kRfThreads;
+    double *xs = xt;
 
     // ---- stage the row tile (contiguous when ld == n_feat)
-    const bool bulk = (R.ld == (int64_t)nf) && ((nr * nf * 8) % 16 == 0) &&
+    const bool bulk = kMaxF > 0 && (R.ld == (int64_t)nf) && ((nr * nf * 8) % 16 == 0) &&
                       ((reinterpret_cast<uintptr_t>(R.X + row0 * R.ld) & 15) == 0);
-    if (bulk) {
+    if (kMaxF == 0) {
+        // no staging: each thread reads its own row below
+    } else if (bulk) {
         const uint32_t bytes = (uint32_t)(nr * nf * 8);
         if (threadIdx.x == 0) {
             const uint32_t b = (uint32_t)__cvta_generic_to_shared(&bar);
@@ -77,22 +85,34 @@ __global__ void __launch_bounds__(kRfThreads) k4_rf_predict(RfArgs R) {
         __syncthreads();
     }
     const int64_t row = row0 + threadIdx.x;
-    if (threadIdx.x >= nr) return;
-    const uint32_t ai = R.n_cfg ? (uint32_t)((row / R.n_cfg) % R.n_arch) : 0u;
+    const bool live = threadIdx.x < nr;
+    const uint32_t ai = (live && R.n_cfg) ? (uint32_t)((row / R.n_cfg) % R.n_arch) : 0u;
     const gk_ensemble &E = R.ens[ai < R.n_ens ? ai : 0];
+    // scale and transpose to [feature][thread]: the per-visit reads x[f] with a
+    // lane-varying f are then bank-conflict-free
+    xt[(int)threadIdx.x - kRfThreads] = __longlong_as_double(0x7ff0000000000000ll);
+    if (kMaxF > 0) {
+        double v[kMaxF > 0 ? kMaxF : 1];
+#pragma unroll
+        for (int f = 0; f < kMaxF; f++)
+            v[f] = (live && f < (int)nf) ? xs[threadIdx.x * nf + f] : 0.0;
+        __syncthreads();  // every raw row is in registers before the tile is overwritten
+#pragma unroll
+        for (int f = 0; f < kMaxF; f++)
+            if (live && f < (int)nf)
+                xt[f * kRfThreads + threadIdx.x] = scale_feature(v[f], E.scale_lo[f], E.scale_hi[f]);
+    } else if (live) {
+        for (uint32_t f = 0; f < nf; f++)
+            xt[f * kRfThreads + threadIdx.x] =
+                scale_feature(R.X[row * R.ld + f], E.scale_lo[f], E.scale_hi[f]);
+    }
+    if (!live) return;
     const double NaN = __longlong_as_double(0x7ff8000000000000ll);
     if (R.status && R.status[row]) {
         R.power[row] = NaN;
         if (R.energy) R.energy[row] = NaN;
         return;
     }
-    // scale and transpose to [feature][thread]: the per-visit reads x[f] with a
-    // lane-varying f are then bank-conflict-free
-    double *xr = xs + (size_t)threadIdx.x * nf;
-    double *xt = xs + (size_t)kRfThreads * (nf + 1);  // row -1 of the tile = +inf (leaf slot)
-    xt[threadIdx.x - kRfThreads] = __longlong_as_double(0x7ff0000000000000ll);
-    for (uint32_t f = 0; f < nf; f++)
-        xt[f * kRfThreads + threadIdx.x] = scale_feature(xr[f], E.scale_lo[f], E.scale_hi[f]);
     const double total = walk_ensemble(E, xt + threadIdx.x, kRfThreads);
     R.power[row] = total;
     if (R.energy) R.energy[row] = __dmul_rn(total, R.time_us[row]);
@@ -132,12 +152,23 @@ int gk_launch_rf(const gk_ensemble *ens, uint32_t n_ens, const double *X, int64_
     R.energy = energy;
     R.n_cfg = n_cfg;
     R.n_arch = n_arch ? n_arch : 1;
-    // row tile + transposed tile with one leading +inf row
-    const size_t smem = (2 * (size_t)nf + 1) * gk::kRfThreads * sizeof(double);
+    // one tile: leading +inf row + [feature][thread] (the staged raw rows are
+    // transposed in place through registers)
+    const size_t smem = ((size_t)nf + 1) * gk::kRfThreads * sizeof(double);
+    const auto kern = nf <= 16 ? gk::k4_rf_predict<16>
+                    : nf <= 32 ? gk::k4_rf_predict<32> : gk::k4_rf_predict<0>;
     if (smem > 48 * 1024)
-        cudaFuncSetAttribute(gk::k4_rf_predict, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // the node gathers live in L1: give shared memory only what resident CTAs need
+    {
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, gk::kRfThreads, smem);
+        const size_t need = (smem + 1024) * (per_sm > 0 ? per_sm : 1);
+        int carve = (int)((need * 100 + 228 * 1024 - 1) / (228 * 1024));
+        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             carve > 100 ? 100 : carve);
+    }
     const int64_t blocks = (n_rows + gk::kRfThreads - 1) / gk::kRfThreads;
-    gk::k4_rf_predict<<<(unsigned)blocks, gk::kRfThreads, smem, st>>>(R);
+    kern<<<(unsigned)blocks, gk::kRfThreads, smem, st>>>(R);
     return gk_check_launch("k4_rf_predict");
 }

@@ -485,7 +485,7 @@ struct FusedArgs {
 #define GK_FUSED_MINB 6
 #endif
 #ifndef GK_FUSED_ILP
-#define GK_FUSED_ILP 4  // trees walked in lock-step inside the fused sweep
+#define GK_FUSED_ILP 8  // trees walked in lock-step inside the fused sweep (8 measured best)
 #endif
 template <bool kFused>
 __global__ void __launch_bounds__(kWarps * 32, kFused ? GK_FUSED_MINB : GK_K23_MINB) k23_schedule(

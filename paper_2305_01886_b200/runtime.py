@@ -296,7 +296,16 @@ class Sweep:
             _check(L.gk_get_stage_ms(out))
         finally:
             L.gk_set_stage_timing(0)
+        if self.fused:
+            return {"k1_static": out[0], "k23_schedule<fused>": out[1]}
         return {"k1_static": out[0], "k23_schedule": out[1], "k4_rf_predict": out[2]}
+
+    @property
+    def fused(self) -> bool:
+        """libgk runs the sweep as one fused kernel unless GK_SWEEP_FUSED=0."""
+        import os
+
+        return os.environ.get("GK_SWEEP_FUSED", "1")[:1] != "0"
 
     def run(self, stream=None):
         _check(load_library().gk_predict_energy_sweep(
