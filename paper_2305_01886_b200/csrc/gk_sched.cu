@@ -23,7 +23,10 @@ namespace gk {
 
 constexpr int kWarps = 4;            // warps per CTA (each warp: 32 points of one kernel)
 #ifndef GK_PROBE
-#define GK_PROBE 4  // backward probe steps before the binary search for the first live span
+#define GK_PROBE 2  // backward probe steps before the binary search for the first live span
+#endif
+#ifndef GK_SCAN_UNROLL
+#define GK_SCAN_UNROLL 2  // spans loaded per first-fit scan iteration
 #endif
 #ifndef GK_K23_CARVE
 // measured (tools/sweep_variants.sh, B200): 0% carveout (max L1 for the
@@ -243,11 +246,27 @@ __device__ __forceinline__ double schedule_block(const gk_corpus &C, const gk_bl
             }
         }
         double t = ready;
-        for (; k < L; k++) {  // the reference's scan from there (2.9 spans on average)
-            const double s = ROW(m.ss, base + k), e = ROW(m.se, base + k);
-            if (e <= t) continue;
-            if (s >= __dadd_rn(t, len)) break;
-            t = e;
+        // the reference's scan from there (2.9 spans on average), GK_SCAN_UNROLL
+        // spans per iteration: independent loads, then the sequential decisions
+        bool hit = false;
+        for (; k < L && !hit; k += GK_SCAN_UNROLL) {
+            double s4[GK_SCAN_UNROLL], e4[GK_SCAN_UNROLL];
+#pragma unroll
+            for (int u = 0; u < GK_SCAN_UNROLL; u++) {
+                const bool in = k + u < L;
+                s4[u] = in ? ROW(m.ss, base + k + u) : 0.0;
+                e4[u] = in ? ROW(m.se, base + k + u) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < GK_SCAN_UNROLL; u++) {
+                if (hit || k + u >= L) continue;
+                if (e4[u] <= t) continue;
+                if (s4[u] >= __dadd_rn(t, len)) {
+                    hit = true;
+                    continue;
+                }
+                t = e4[u];
+            }
         }
         const double start = t;
         const double fin = __dadd_rn(start, d);
