@@ -26,7 +26,7 @@ constexpr int kWarps = 4;            // warps per CTA (each warp: 32 points of o
 #define GK_PROBE 2  // backward probe steps before the binary search for the first live span
 #endif
 #ifndef GK_SCAN_UNROLL
-#define GK_SCAN_UNROLL 2  // spans loaded per first-fit scan iteration
+#define GK_SCAN_UNROLL 4  // spans loaded per first-fit scan iteration (4 measured best)
 #endif
 #ifndef GK_K23_CARVE
 // measured (tools/sweep_variants.sh, B200): 0% carveout (max L1 for the
