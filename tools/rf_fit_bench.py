@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--trees", type=int, default=32)
     ap.add_argument("--depth", type=int, default=16)
     ap.add_argument("--batch", type=int, default=32)
+    ap.add_argument("--profile", action="store_true")
     a = ap.parse_args()
     import torch
 
@@ -40,11 +41,22 @@ def main():
     Xs = (X - X.min(0)) / (X.max(0) - X.min(0))
     RandomForestRegressor(2, max_depth=4, random_state=0).fit(Xs[:5000], y[:5000])  # warm-up
     torch.cuda.synchronize()
+    prof = None
+    if a.profile:
+        import cProfile
+
+        prof = cProfile.Profile()
+        prof.enable()
     t0 = time.perf_counter()
     m = RandomForestRegressor(a.trees, max_depth=a.depth, random_state=0,
                               trees_per_batch=a.batch).fit(Xs, y)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
+    if prof is not None:
+        import pstats
+
+        prof.disable()
+        pstats.Stats(prof).sort_stats("tottime").print_stats(18)
     nodes = np.mean([e.tree_.node_count for e in m.estimators_])
     p = m.predict(Xs[:100000])
     r2 = 1 - np.mean((p - y[:100000]) ** 2) / np.var(y[:100000])
