@@ -244,17 +244,12 @@ class RandomForestRegressor:
         _check(L.gk_rf_compact(_ptr(counts), TB, n, _ptr(base_d), _ptr(rows0), _ptr(fill), st))
         max_depth = self.max_depth if self.max_depth is not None else 1 << 30
 
-        # node storage per tree (BFS ids; children of one split are adjacent)
-        cap = [2 * int(mt) + 1 for mt in m]
-        node_base = np.concatenate([[0], np.cumsum(cap)[:-1]]).astype(np.int64)
-        n_nodes_tot = int(sum(cap))
-        feat = np.full(n_nodes_tot, TREE_UNDEFINED, np.int32)
-        nbin = np.zeros(n_nodes_tot, np.int32)
-        left = np.full(n_nodes_tot, TREE_LEAF, np.int32)
-        depth = np.zeros(n_nodes_tot, np.int32)
+        # nodes get BFS ids per tree (children of one split adjacent); records are
+        # kept per level and assembled into exactly-sized arrays at the end
         next_id = np.ones(TB, np.int64)
-        leaves = []           # (tree, node, parity, begin, end) arrays per level
-        splits_by_level = []  # (parent gidx, left gidx) arrays per level
+        tree_depth = np.zeros(TB, np.int32)
+        leaves = []    # (tree, node, parity, begin, end) arrays per level
+        splits = []    # (tree, node, feat, bin, left id) arrays per level
 
         # level 0 tasks: one root per tree
         t_tree = np.arange(TB, dtype=np.int32)
@@ -313,11 +308,7 @@ class RandomForestRegressor:
                 rank = np.arange(len(pt)) - np.repeat(starts, run_len)
             lid = next_id[pt] + 2 * rank
             next_id += 2 * np.bincount(pt, minlength=TB)
-            gpar = node_base[pt] + pn
-            feat[gpar] = sp["feat"][s]
-            nbin[gpar] = sp["bin"][s]
-            left[gpar] = lid
-            splits_by_level.append((gpar, node_base[pt] + lid))
+            splits.append((pt, pn, sp["feat"][s], sp["bin"][s], lid))
             nl = sp["n_left"][s].astype(np.int32)
             cb = np.empty(2 * len(pt), np.int32)
             ce = np.empty(2 * len(pt), np.int32)
@@ -328,7 +319,7 @@ class RandomForestRegressor:
             cn[0::2], cn[1::2] = lid, lid + 1
             cpar = np.repeat(1 - t_par[s], 2).astype(np.int32)
             t_depth += 1
-            depth[node_base[ct] + cn] = t_depth
+            tree_depth[pt] = t_depth
             elig = (ce - cb >= 2) & (t_depth < max_depth)
             if (~elig).any():
                 leaves.append((ct[~elig], cn[~elig], cpar[~elig], cb[~elig], ce[~elig]))
@@ -346,6 +337,19 @@ class RandomForestRegressor:
         stats_d = torch.empty(4 * len(lt), dtype=torch.int64, device=dev)
         _check(L.gk_rf_leaf_stats(_ptr(counts), n, _ptr(D["yfp"]), _ptr(D["y2fp"]), _ptr(lv_d),
                                   len(lt), _ptr(rows0), _ptr(rows1), _ptr(stats_d), st))
+        # exactly-sized node arrays
+        node_base = np.concatenate([[0], np.cumsum(next_id)[:-1]]).astype(np.int64)
+        n_nodes_tot = int(next_id.sum())
+        feat = np.full(n_nodes_tot, TREE_UNDEFINED, np.int32)
+        nbin = np.zeros(n_nodes_tot, np.int32)
+        left = np.full(n_nodes_tot, TREE_LEAF, np.int32)
+        splits_by_level = []
+        for pt, pn, fs, bs, lid in splits:
+            gpar = node_base[pt] + pn
+            feat[gpar] = fs
+            nbin[gpar] = bs
+            left[gpar] = lid
+            splits_by_level.append((gpar, node_base[pt] + lid))
         # exact integer sums bottom-up, converted to float64 once per node
         istats = np.zeros((n_nodes_tot, 4), np.int64)
         istats[node_base[lt] + ln] = stats_d.cpu().numpy().reshape(-1, 4)
@@ -375,7 +379,7 @@ class RandomForestRegressor:
             trees.append(Tree(node_count=cnt, children_left=cl.astype(np.int64), children_right=cr,
                               feature=f, threshold=thr, value=val.reshape(-1, 1, 1), impurity=imp,
                               n_node_samples=st_[:, 0].astype(np.int64), weighted_n_node_samples=w,
-                              max_depth=int(depth[g].max()) if cnt else 0))
+                              max_depth=int(tree_depth[k])))
         return trees
 
     # -------------------------------------------------------------- predict
