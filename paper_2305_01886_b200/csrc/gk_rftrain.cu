@@ -435,38 +435,32 @@ __global__ void __launch_bounds__(128) k5_split_small(RfTrainData D, const RfTas
         S += __shfl_xor_sync(GK_FULL, S, o);
     }
     const double parent = (double)S * (double)S / (double)W;
+    // per-warp 256-bin histogram, one feature at a time, evaluated by the same
+    // boundary scan as the larger nodes
+    __shared__ uint64_t hcw[4][kBins];
+    __shared__ int64_t hs[4][kBins];
+    uint64_t *cw = hcw[threadIdx.x >> 5];
+    int64_t *hsw = hs[threadIdx.x >> 5];
     BestSplit best{-1.0, 0x7fffffff, 0x7fffffff, 0};
     for (int f = 0; f < D.F; f++) {
-        int k[2];
 #pragma unroll
-        for (int h = 0; h < 2; h++) k[h] = r[h] >= 0 ? D.Xb[(size_t)r[h] * D.F + f] : 1 << 20;
-        uint32_t cl[2] = {0, 0}, wl[2] = {0, 0};
-        int64_t sl[2] = {0, 0};
-        for (int src = 0; src < 32; src++) {
-#pragma unroll
-            for (int h2 = 0; h2 < 2; h2++) {
-                const int kk = __shfl_sync(GK_FULL, k[h2], src);
-                const uint32_t ww = __shfl_sync(GK_FULL, w[h2], src);
-                const int64_t ss = __shfl_sync(GK_FULL, s[h2], src);
-                const bool valid = kk < (1 << 20);
-#pragma unroll
-                for (int h = 0; h < 2; h++) {
-                    if (valid && kk <= k[h]) {
-                        cl[h] += 1;
-                        wl[h] += ww;
-                        sl[h] += ss;
-                    }
-                }
-            }
+        for (int j = 0; j < kBins / 32; j++) {
+            cw[lane + 32 * j] = 0;
+            hsw[lane + 32 * j] = 0;
         }
+        __syncwarp();
 #pragma unroll
         for (int h = 0; h < 2; h++) {
-            if (r[h] < 0 || k[h] >= kBins - 1) continue;
-            if (cl[h] < 1 || (uint32_t)m - cl[h] < 1) continue;
-            const double SL = (double)sl[h], SR = (double)(S - sl[h]);
-            const double p = SL * SL / (double)wl[h] + SR * SR / (double)(W - wl[h]);
-            if (better(p, f, k[h], best)) best = BestSplit{p, f, k[h], cl[h]};
+            if (r[h] >= 0) {
+                const int b = D.Xb[(size_t)r[h] * D.F + f];
+                atomicAdd((unsigned long long *)&cw[b], (unsigned long long)((1ull << 32) | w[h]));
+                atomicAdd((unsigned long long *)&hsw[b], (unsigned long long)s[h]);
+            }
         }
+        __syncwarp();
+        const BestSplit b = eval_feature(cw, hsw, f, lane);
+        if (better(b.proxy, b.feat, b.bin, best)) best = b;
+        __syncwarp();
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {

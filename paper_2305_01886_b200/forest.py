@@ -82,7 +82,7 @@ def bin_edges(Xf: np.ndarray, n_bins: int = N_BINS, sample: int = 65_536):
         S = Xf[np.sort(idx)]
     else:
         S = Xf
-    S = np.sort(S, axis=0)
+    S = np.sort(S.astype(np.float32), axis=0)
     m = S.shape[0]
     edges = np.zeros((F, n_bins - 1), np.float32)
     n_edges = np.zeros(F, np.int32)
@@ -155,9 +155,8 @@ class RandomForestRegressor:
         self.n_features_in_ = F
         L = _lib()
         dev = device()
-        Xf = X.astype(np.float32)
-        edges, n_edges = bin_edges(Xf, self.n_bins)
-        Xd = torch.from_numpy(Xf.astype(np.float64)).to(dev)
+        edges, n_edges = bin_edges(X, self.n_bins)   # float32 sample inside
+        Xd = torch.from_numpy(X).to(dev)               # k5_bin casts to float32 (sklearn)
         Xb = torch.empty(n * F, dtype=torch.uint8, device=dev)
         bmin = torch.empty(F * N_BINS, dtype=torch.int32, device=dev)
         bmax = torch.empty(F * N_BINS, dtype=torch.int32, device=dev)
