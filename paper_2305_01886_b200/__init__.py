@@ -46,6 +46,7 @@ from .profiles import (
     us_from_cycles,
 )
 from .ptx import parse_ptx
+from .ptx_native import pack_ptx
 
 __version__ = "0.1.0"
 
@@ -55,7 +56,8 @@ __all__ = [
     "LaunchConfig", "ProfileError", "PtxInstruction", "PtxParseError", "Resource",
     "SELECTED_FEATURES", "ScheduleError", "TreeEnsemble", "cycles_from_us", "extract_features",
     "extract_features_batch", "global_mem_latency", "latency_of", "launch_overhead_us",
-    "list_shipped_profiles", "load_ensemble", "load_profile", "mem_throughput", "parse_ptx",
+    "list_shipped_profiles", "load_ensemble", "load_profile", "mem_throughput", "pack_ptx",
+    "parse_ptx",
     "predict_energy", "predict_launches", "predict_power", "predict_power_batch",
     "resolve_profile", "schedule_batch", "schedule_kernel", "us_from_cycles",
 ]

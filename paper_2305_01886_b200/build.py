@@ -20,6 +20,9 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libgk.so"
+PTX_LIB = PKG / "libgkptx.so"   # host-only native PTX front-end (g++, no CUDA)
+PTX_SOURCES = ["gk_ptx.cpp"]
+CXXFLAGS = ["-O2", "-std=c++17", "-fPIC", "-shared", "-pthread", "-Wall", "-Wextra"]
 SOURCES = ["gk_api.cu", "gk_sched.cu", "gk_rf.cu", "gk_rftrain.cu"]
 HEADERS = ["gk_internal.cuh", "gk_exp.h", "gk_exp_table.h", "gk_walk.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -42,7 +45,25 @@ def _stale() -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
+def build_ptx(force: bool = False) -> Path:
+    """libgkptx.so: the native PTX tokenizer / packer (include/gk_ptx.h)."""
+    hdr = PKG.parent / "include" / "gk_ptx.h"
+    srcs = [CSRC / s for s in PTX_SOURCES]
+    if not force and PTX_LIB.exists() and all(
+            d.stat().st_mtime <= PTX_LIB.stat().st_mtime for d in srcs + [hdr]):
+        return PTX_LIB
+    cxx = os.environ.get("CXX") or shutil.which("g++") or "g++"
+    tmp = PTX_LIB.with_suffix(".so.tmp")
+    cmd = [cxx, *CXXFLAGS, f"-I{hdr.parent}", *map(str, srcs), "-o", str(tmp)]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode:
+        raise RuntimeError(f"g++ failed on gk_ptx.cpp:\n{r.stdout}{r.stderr}")
+    tmp.replace(PTX_LIB)
+    return PTX_LIB
+
+
 def build(force: bool = False, verbose: bool = False) -> Path:
+    build_ptx(force)
     if not force and not _stale():
         return LIB
     objdir = PKG / "build"

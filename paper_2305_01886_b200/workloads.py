@@ -2,8 +2,9 @@
 
 Corpus generation + parsing is the host front-end: it runs
 once, outside any timed region, sharded over worker processes; each worker
-packs its shard and the shards are merged into one corpus with a single
-signature table.
+generates its shard's PTX text, parses + packs it with the native tokenizer
+(libgkptx, byte-identical to parse_ptx + pack_corpus), and the shards are
+merged into one corpus with a single signature table.
 """
 
 from __future__ import annotations
@@ -14,15 +15,12 @@ from concurrent.futures import ProcessPoolExecutor
 import numpy as np
 
 from . import corpus as CG
-from . import pack, ptx
+from . import pack, ptx_native
 
 
 def _shard(args):
     n, seed, prefix = args
-    b = pack.CorpusBuilder()
-    for name, text, loops in CG.synth_corpus(n, seed, prefix):
-        b.add(ptx.parse_ptx(text, name, loop_counts=loops))
-    return b.build()
+    return ptx_native.pack_ptx(CG.synth_corpus(n, seed, prefix), threads=1)
 
 
 def merge_corpora(parts: list) -> pack.Corpus:
