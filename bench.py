@@ -36,6 +36,23 @@ PEAKS = ROOT / "MEASURED_PEAKS.json"
 FALLBACK_HBM = 6650.0
 
 
+TRAFFIC = ROOT / "profiles" / "r1" / "traffic.json"
+
+
+def ncu_traffic(workload: str, kernel: str, units: int):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture
+    (profiles/r1/traffic.json), scaled per unit to this launch's size."""
+    try:
+        rec = json.loads(TRAFFIC.read_text())[workload][kernel]
+    except Exception:
+        return None, None
+    per_unit = (rec["read"] + rec["write"]) / rec["units"]
+    src = f"ncu --set full, {rec['capture']}"
+    if rec["units"] != units:
+        src += f"; scaled from {rec['units']} to {units} {rec['unit']}s"
+    return per_unit * units, src
+
+
 def hbm_peak():
     try:
         return float(json.loads(PEAKS.read_text())["hbm_gbs"]), "measured"
@@ -409,6 +426,7 @@ def main():
     }
     peak, peak_kind = hbm_peak()
     achieved = alg[dom] / (split[dom] / 1e3) / 1e9
+    traffic, traffic_src = ncu_traffic(args.workload, dom, n_pts if dom != "k1_static" else W["n_k"])
     # CPU baseline on rank 0 (bounded sample)
     nk, cp, cs = 0, 0, 1.0
     if not args.no_cpu:
@@ -433,7 +451,8 @@ def main():
         "kernel_ms": split,
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                     "algorithmic_bytes": alg[dom], "traffic": None},
+                     "algorithmic_bytes": alg[dom], "traffic": traffic,
+                     "traffic_source": traffic_src},
         "cpu_baseline": {"value": cp / cs, "unit": "points/s", "cores": threads, "kind": "port",
                          "sample": f"first {nk} kernels of the workload ({cp} points), oracle "
                                    f"schedule+features+ensemble+energy"},
@@ -466,7 +485,9 @@ def run_c4(args, rank, world, local_rank, threads):
     X = torch.rand((n, F), dtype=torch.float64, device="cuda", generator=g)
     flat = random_forest_flat(args.trees, args.depth, [f"f{i}" for i in range(F)], np.zeros(F),
                               np.ones(F), seed=11)
-    de = rt.DeviceEnsemble.upload(flat)
+    # random independent rows: the walk is bound by L2/DRAM latency, so the
+    # two-level block layout (half the dependent loads) is the default here
+    de = rt.DeviceEnsemble.upload(flat, layout=os.environ.get("GK_WALK_LAYOUT", "blocks"))
     power = torch.empty(n, dtype=torch.float64, device="cuda")
     L = rt.load_library()
     import ctypes
@@ -504,6 +525,7 @@ def run_c4(args, rank, world, local_rank, threads):
     alg = n * (8 * F + 8) + flat.nodes.nbytes  # rows in + power out + ensemble once
     achieved = alg / (ms / args.steps / 1e3) / 1e9
     peak, peak_kind = hbm_peak()
+    traffic, traffic_src = ncu_traffic("c4", "k4_rf_predict", n)
     line = {"metric": "RF inference rows/sec", "value": value, "unit": "rows/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
@@ -512,11 +534,12 @@ def run_c4(args, rank, world, local_rank, threads):
                                    f"{rows_total} rows x 64 fp64",
                        "ensemble": f"{args.trees} trees depth {args.depth} "
                                    f"({len(flat.nodes) // flat.n_trees} nodes/tree, declared random)",
-                       "rows_per_gpu": n, "l2": "rows (51 GB) >> L2"},
+                       "rows_per_gpu": n, "l2": "rows (51 GB) >> L2", "walk_layout": de.layout},
             "gpu_launches": args.steps,
             "roofline": {"bound": "hbm", "kernel": "k4_rf_predict", "achieved": achieved,
                          "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                         "frac": achieved / peak, "algorithmic_bytes": alg, "traffic": None},
+                         "frac": achieved / peak, "algorithmic_bytes": alg, "traffic": traffic,
+                         "traffic_source": traffic_src},
             "clocks": clk.summary()}
     if not args.no_cpu:
         import oracle as O

@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define GK_ABI_VERSION 1
+#define GK_ABI_VERSION 2
 
 /* resource / class codes (reference ptx/types.py:12-24) */
 enum { GK_SP = 0, GK_SFU = 1, GK_DPU = 2, GK_LSU = 3, GK_WS = 4, GK_NRES = 5 };
@@ -164,6 +164,29 @@ typedef struct {
  * trees are contiguous from tree_off[t]; tree_depth[t] is the depth of tree t. */
 typedef struct { double v; int32_t feature; int32_t left; } gk_node;
 
+/* Compact 8-byte walk node (optional), same index space as gk_node:
+ *   t    = f32 bits of round-toward-(-inf)(threshold); 0 for a leaf
+ *   meta = feature << 24 | right  (feature 0..126; 0xFF = leaf, right = self)
+ * Decision: a = round-down-f32(x) vs t as for gk_block2 below; the exact tie
+ * test reads nodes[i].v; a leaf's feature byte selects the +inf slot in front
+ * of the feature tile, so the walk absorbs at leaves (value in nodes[i].v). */
+typedef struct { uint32_t t; uint32_t meta; } gk_node8;
+
+/* Two-level walk block (32 B, optional; one 256-bit load per lane per step).
+ * A block is a depth-2 subtree: slot 0 (its root, an internal node at even
+ * depth), slots 1 / 2 (the root's left / right child) and the four exits
+ * below them (exit 2k + c = child c of slot 1 + k).
+ *   t[s]  f32 bits of round-toward-(-inf)(threshold of slot s)
+ *   f     feature of slot s in byte s
+ *   e[j]  next block id, or GK_LEAF | leaf id (leaf_val index)
+ * A slot that is a leaf has both of its exits = that leaf (its t / f are 0).
+ * Decision at a slot: a = round-down-f32(x[f]); a < t -> left, a > t -> right,
+ * a == t (x and the threshold share one f32 bucket) -> the exact fp64 test
+ * x <= thr64[3 * block + slot].  This equals `x <= threshold` for every x
+ * (NaN and +-inf included), so power stays bit-identical (power.py:156-168). */
+#define GK_LEAF 0x80000000u
+typedef struct { uint32_t t[3]; uint32_t f; uint32_t e[4]; } gk_block2;
+
 typedef struct {
     const gk_node *nodes;
     const int64_t *tree_off;    /* n_trees                        */
@@ -172,6 +195,13 @@ typedef struct {
     const double  *scale_hi;
     double   base_score;
     uint32_t n_trees, n_feat, max_depth;
+    /* optional compact forms of the same trees; the walk uses blocks if set,
+     * else nodes8 if set, else the 16-byte nodes */
+    const gk_node8  *nodes8;    /* per node                                 */
+    const gk_block2 *blocks;    /* n_blocks                                 */
+    const double    *thr64;     /* 3 per block: exact thresholds (tie test)  */
+    const double    *leaf_val;  /* per leaf id                               */
+    const uint32_t  *root;      /* n_trees: root block id or GK_LEAF | leaf  */
 } gk_ensemble;
 
 /* ------------------------------------------------------------------------ */

@@ -118,6 +118,50 @@ __global__ void __launch_bounds__(kRfThreads) k4_rf_predict(RfArgs R) {
     if (R.energy) R.energy[row] = __dmul_rn(total, R.time_us[row]);
 }
 
+#ifndef GK_RF_B2_ILP
+#define GK_RF_B2_ILP 4
+#endif
+// K4 over compact layouts (gk_node8 / gk_block2): the CTA's row tile is loaded
+// coalesced, scaled, rounded toward -inf to f32 and stored transposed
+// [feature][row] (stride kRfThreads: each walk read -- lane-varying feature,
+// one row per lane -- hits 32 distinct banks).
+// The exact fp64 feature is recomputed from X only for the rare a == t visit.
+template <bool kBlocks>
+__global__ void __launch_bounds__(kRfThreads) k4_rf_predict_c(RfArgs R) {
+    extern __shared__ __align__(16) float xf_raw[];
+    constexpr int S = kRfThreads;
+    float *xf = xf_raw + S;  // row -1: the +inf slot of the leaf step
+    const int64_t row0 = (int64_t)blockIdx.x * kRfThreads;
+    const int nr = (int)min((int64_t)kRfThreads, R.n_rows - row0);
+    const int nf = (int)R.ens[0].n_feat;
+    xf_raw[threadIdx.x] = __int_as_float(0x7f800000);
+    for (int q = threadIdx.x; q < nr * nf; q += kRfThreads) {
+        const int r = q / nf, f = q - r * nf;
+        const int64_t row = row0 + r;
+        const uint32_t ai = R.n_cfg ? (uint32_t)((row / R.n_cfg) % R.n_arch) : 0u;
+        const gk_ensemble &Er = R.ens[ai < R.n_ens ? ai : 0];
+        const double v = scale_feature(R.X[row * R.ld + f], Er.scale_lo[f], Er.scale_hi[f]);
+        xf[f * S + r] = __double2float_rd(v);
+    }
+    __syncthreads();
+    if ((int)threadIdx.x >= nr) return;
+    const int64_t row = row0 + threadIdx.x;
+    const uint32_t ai = R.n_cfg ? (uint32_t)((row / R.n_cfg) % R.n_arch) : 0u;
+    const gk_ensemble &E = R.ens[ai < R.n_ens ? ai : 0];
+    const double NaN = __longlong_as_double(0x7ff8000000000000ll);
+    if (R.status && R.status[row]) {
+        R.power[row] = NaN;
+        if (R.energy) R.energy[row] = NaN;
+        return;
+    }
+    const double *xrow = R.X + row * R.ld;
+    auto x64 = [&](int f) { return scale_feature(xrow[f], E.scale_lo[f], E.scale_hi[f]); };
+    const double total = kBlocks ? walk_ensemble_b2<GK_RF_B2_ILP>(E, xf + threadIdx.x, S, x64)
+                                 : walk_ensemble8<GK_RF_ILP>(E, xf + threadIdx.x, S, x64);
+    R.power[row] = total;
+    if (R.energy) R.energy[row] = __dmul_rn(total, R.time_us[row]);
+}
+
 }  // namespace gk
 
 int gk_launch_rf(const gk_ensemble *ens, uint32_t n_ens, const double *X, int64_t ld,
@@ -152,6 +196,26 @@ int gk_launch_rf(const gk_ensemble *ens, uint32_t n_ens, const double *X, int64_
     R.energy = energy;
     R.n_cfg = n_cfg;
     R.n_arch = n_arch ? n_arch : 1;
+    bool all_blocks = true, all_n8 = true;
+    for (uint32_t a = 0; a < n_ens; a++) {
+        all_blocks &= ens[a].blocks != nullptr;
+        all_n8 &= ens[a].nodes8 != nullptr;
+    }
+    if (all_blocks || all_n8) {
+        const size_t smem8 = ((size_t)nf + 1) * gk::kRfThreads * sizeof(float);
+        const auto k8 = all_blocks ? gk::k4_rf_predict_c<true> : gk::k4_rf_predict_c<false>;
+        if (smem8 > 48 * 1024)
+            cudaFuncSetAttribute(k8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem8);
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k8, gk::kRfThreads, smem8);
+        const size_t need = (smem8 + 1024) * (per_sm > 0 ? per_sm : 1);
+        const int carve = (int)((need * 100 + 228 * 1024 - 1) / (228 * 1024));
+        cudaFuncSetAttribute(k8, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             carve > 100 ? 100 : carve);
+        const int64_t blocks = (n_rows + gk::kRfThreads - 1) / gk::kRfThreads;
+        k8<<<(unsigned)blocks, gk::kRfThreads, smem8, st>>>(R);
+        return gk_check_launch(all_blocks ? "k4_rf_predict_c<blocks>" : "k4_rf_predict_c<nodes8>");
+    }
     // one tile: leading +inf row + [feature][thread] (the staged raw rows are
     // transposed in place through registers)
     const size_t smem = ((size_t)nf + 1) * gk::kRfThreads * sizeof(double);

@@ -305,7 +305,8 @@ __device__ __forceinline__ double finish_point(const gk_corpus &C, const gk_grid
                                                const gk_kernel &K, const PointScalars &P,
                                                double cfg_delay, const PointOut &O,
                                                double *xw = nullptr,
-                                               const gk_ensemble *E = nullptr) {
+                                               const gk_ensemble *E = nullptr,
+                                               float *xf = nullptr) {
     const gk_arch &A = G.arch[P.ai];
     const gk_config c = G.cfg[P.ci];
     const gk_kstat S = ks[P.ki];
@@ -462,8 +463,11 @@ __device__ __forceinline__ double finish_point(const gk_corpus &C, const gk_grid
         for (uint32_t j = 0; j < O.n_sel; j++) o[j] = feature(O.sel_idx[j]);
     }
     if (xw)
-        for (uint32_t j = 0; j < O.n_sel; j++)
-            xw[(size_t)j * 32] = scale_feature(feature(O.sel_idx[j]), E->scale_lo[j], E->scale_hi[j]);
+        for (uint32_t j = 0; j < O.n_sel; j++) {
+            const double v = scale_feature(feature(O.sel_idx[j]), E->scale_lo[j], E->scale_hi[j]);
+            xw[(size_t)j * 32] = v;
+            xf[(size_t)j * 32] = __double2float_rd(v);  // compact-walk key (gk_node8)
+        }
     return time_us;
 }
 
@@ -475,6 +479,7 @@ __device__ __forceinline__ double finish_point(const gk_corpus &C, const gk_grid
 struct FusedArgs {
     gk_ensemble ens[4];
     uint32_t n_ens;
+    int compact;  // walk a compact layout when the ensemble has one (GK_FUSED_COMPACT=1)
     double *power, *energy;
 };
 
@@ -487,6 +492,9 @@ struct FusedArgs {
 #endif
 #ifndef GK_FUSED_ILP
 #define GK_FUSED_ILP 8  // trees walked in lock-step inside the fused sweep (8 measured best)
+#endif
+#ifndef GK_FUSED_B2_ILP
+#define GK_FUSED_B2_ILP 4  // blocked walk: trees in lock-step (each step = 2 levels, 8 regs/tree)
 #endif
 template <bool kFused>
 __global__ void __launch_bounds__(kWarps * 32, kFused ? GK_FUSED_MINB : GK_K23_MINB) k23_schedule(
@@ -531,7 +539,14 @@ __global__ void __launch_bounds__(kWarps * 32, kFused ? GK_FUSED_MINB : GK_K23_M
     // (row 0 of each warp's tile is the +inf leaf slot; features start at row 1)
     double *xw = slab_base + (size_t)kWarps * 3 * ns * 32 + (size_t)warp * (O.n_sel + 1) * 32 +
                  32 + lane;
-    if (kFused) xw[-32] = __longlong_as_double(0x7ff0000000000000ll);
+    // fused: per-warp [n_sel + 1][32] f32 keys for the compact walk after the fp64 tiles
+    float *xf = reinterpret_cast<float *>(slab_base + (size_t)kWarps * 3 * ns * 32 +
+                                          (size_t)kWarps * (O.n_sel + 1) * 32) +
+                (size_t)warp * (O.n_sel + 1) * 32 + 32 + lane;
+    if (kFused) {
+        xw[-32] = __longlong_as_double(0x7ff0000000000000ll);
+        xf[-32] = __int_as_float(0x7f800000);
+    }
 
     // dynamic work queue (items differ widely in cost; G.order puts the most
     // expensive kernels first so the tail is short)
@@ -616,7 +631,8 @@ __global__ void __launch_bounds__(kWarps * 32, kFused ? GK_FUSED_MINB : GK_K23_M
         const gk_ensemble *Ep = kFused ? &F.ens[P.ai < F.n_ens ? P.ai : 0] : nullptr;
         if (P.active) {
             if (feasible) {
-                t_ok = finish_point(C, G, ks, latsum, K, P, cfg_delay, O, kFused ? xw : nullptr, Ep);
+                t_ok = finish_point(C, G, ks, latsum, K, P, cfg_delay, O, kFused ? xw : nullptr, Ep,
+                                    xf);
             } else {
                 if (O.status) O.status[P.p] = GK_INFEASIBLE_LAUNCH;
                 if (O.si)
@@ -634,7 +650,13 @@ __global__ void __launch_bounds__(kWarps * 32, kFused ? GK_FUSED_MINB : GK_K23_M
             if (P.active) {
                 double pw = NaN, en = NaN;
                 if (!isnan(t_ok)) {
-                    pw = walk_ensemble<GK_FUSED_ILP>(*Ep, xw, 32);
+                    auto x64 = [&](int f) { return xw[f * 32]; };
+                    // measured on B200 (c2): inside the fused sweep the 16-byte
+                    // nodes beat both compact layouts (80-register budget,
+                    // L1 data-pipe bound), so they are the default here
+                    pw = F.compact && Ep->blocks   ? walk_ensemble_b2<GK_FUSED_B2_ILP>(*Ep, xf, 32, x64)
+                         : F.compact && Ep->nodes8 ? walk_ensemble8<GK_FUSED_ILP>(*Ep, xf, 32, x64)
+                                                   : walk_ensemble<GK_FUSED_ILP>(*Ep, xw, 32);
                     en = __dmul_rn(pw, t_ok);
                 }
                 F.power[P.p] = pw;
@@ -730,7 +752,8 @@ static int launch_sched(const gk_corpus *C, const gk_grid *G, const gk_kstat *ks
     const uint32_t ns = smem_rows(max_n);
     const size_t smem = G->n_arch * (sizeof(gk::ArchSmem) + (size_t)C->n_sig * sizeof(double)) +
                         (size_t)gk::kWarps * 3 * ns * 32 * sizeof(double) +
-                        (kFused ? (size_t)gk::kWarps * (n_sel + 1) * 32 * sizeof(double) : 0);
+                        (kFused ? (size_t)gk::kWarps * (n_sel + 1) * 32 * (sizeof(double) + sizeof(float))
+                                : 0);
     if (smem > 48 * 1024) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     }
@@ -800,6 +823,10 @@ int gk_launch_sweep_fused(const gk_corpus *C, const gk_grid *G, const gk_kstat *
         F.ens[a] = ens[a];
     }
     F.n_ens = n_ens;
+    {
+        const char *e = getenv("GK_FUSED_COMPACT");
+        F.compact = e && atoi(e) != 0;
+    }
     F.power = power;
     F.energy = energy;
     return launch_sched<true>(C, G, ks, latsum, status, nullptr, nullptr, nullptr, sel_idx, n_sel,

@@ -62,6 +62,150 @@ __device__ __forceinline__ double walk_ensemble(const gk_ensemble &E, const doub
     return total;
 }
 
+// Compact walk over gk_node8 (include/gk.h).  xf: this row's features rounded
+// toward -inf to f32 (feature f at xf[f * stride], xf[-stride] = +inf);
+// x64(f): the exact scaled fp64 feature, needed only when a == t.  Per visit:
+// one 8-byte node load, one 4-byte shared load, two f32 compares -- 12 bytes
+// through the L1 data pipe instead of 24.  Loads of the kIlp trees are issued
+// together; the rare tie test runs out of line.
+template <int kIlp, class X64>
+__device__ __forceinline__ void walk8_group(const gk_ensemble &E, uint32_t t, const float *xf,
+                                            int stride, const X64 &x64, double &total) {
+    const uint2 *__restrict__ n8 = reinterpret_cast<const uint2 *>(E.nodes8);
+    const uint2 *base[kIlp];
+    int32_t idx[kIlp];
+    int d = 0;
+#pragma unroll
+    for (int q = 0; q < kIlp; q++) {
+        base[q] = n8 + __ldg(E.tree_off + t + q);
+        idx[q] = 0;
+        d = max(d, __ldg(E.tree_depth + t + q));
+    }
+    for (int s = 0; s < d; s++) {
+        uint2 raw[kIlp];
+        float a[kIlp];
+#pragma unroll
+        for (int q = 0; q < kIlp; q++) raw[q] = __ldg(base[q] + idx[q]);
+#pragma unroll
+        for (int q = 0; q < kIlp; q++) a[q] = xf[((int)raw[q].y >> 24) * stride];  // leaf: +inf slot
+        uint32_t tie = 0;
+        bool le[kIlp];
+#pragma unroll
+        for (int q = 0; q < kIlp; q++) {
+            const float th = __uint_as_float(raw[q].x);
+            le[q] = a[q] < th;
+            tie |= (a[q] == th ? 1u : 0u) << q;
+        }
+        if (__builtin_expect(tie != 0, 0)) {
+#pragma unroll
+            for (int q = 0; q < kIlp; q++)
+                if (tie >> q & 1u)
+                    le[q] = x64((int)raw[q].y >> 24) <=
+                            __ldg(&E.nodes[(base[q] - n8) + idx[q]].v);
+        }
+#pragma unroll
+        for (int q = 0; q < kIlp; q++) {
+            const int r = (int)(raw[q].y & 0xFFFFFFu);
+            idx[q] = le[q] ? r - 1 : r;
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < kIlp; q++) total = __dadd_rn(total, __ldg(&E.nodes[(base[q] - n8) + idx[q]].v));
+}
+
+template <int kIlp, class X64>
+__device__ __forceinline__ double walk_ensemble8(const gk_ensemble &E, const float *xf, int stride,
+                                                 const X64 &x64) {
+    double total = E.base_score;
+    uint32_t t = 0;
+    for (; t + kIlp <= E.n_trees; t += kIlp) walk8_group<kIlp>(E, t, xf, stride, x64, total);
+    for (; t < E.n_trees; t++) walk8_group<1>(E, t, xf, stride, x64, total);
+    return total;
+}
+
+// Blocked walk over gk_block2 (include/gk.h): one 256-bit load per tree per
+// two levels.  xf: this row's features rounded toward -inf to f32 (feature f
+// at xf[f * stride]); x64(f): the exact scaled fp64 feature, needed only when a
+// row value and a threshold share one f32 bucket (the tie test runs out of
+// line).  kIlp trees advance in lock-step for ceil(max depth / 2) steps; a
+// tree that reached its leaf stops loading.  Leaves are added in tree order.
+__device__ __forceinline__ void ld_block2(const gk_block2 *p, uint32_t (&w)[8]) {
+    asm volatile("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]),
+                   "=r"(w[6]), "=r"(w[7])
+                 : "l"(p));
+}
+
+template <int kIlp, class X64>
+__device__ __forceinline__ void walk_b2_group(const gk_ensemble &E, uint32_t t, const float *xf,
+                                              int stride, const X64 &x64, double &total) {
+    uint32_t ref[kIlp];
+    int d = 0;
+#pragma unroll
+    for (int q = 0; q < kIlp; q++) {
+        ref[q] = __ldg(E.root + t + q);
+        d = max(d, __ldg(E.tree_depth + t + q));
+    }
+    const int steps = (d + 1) >> 1;
+    for (int s = 0; s < steps; s++) {
+        uint32_t w[kIlp][8];
+#pragma unroll
+        for (int q = 0; q < kIlp; q++) {
+            if (!(ref[q] & GK_LEAF)) ld_block2(E.blocks + ref[q], w[q]);
+            else {
+#pragma unroll
+                for (int k = 0; k < 8; k++) w[q][k] = 0;
+            }
+        }
+        float a[kIlp][3];
+#pragma unroll
+        for (int q = 0; q < kIlp; q++)
+#pragma unroll
+            for (int k = 0; k < 3; k++) a[q][k] = xf[((w[q][3] >> (8 * k)) & 0xFFu) * stride];
+        uint32_t tie = 0;
+        uint32_t nref[kIlp];
+#pragma unroll
+        for (int q = 0; q < kIlp; q++) {
+            const float t0 = __uint_as_float(w[q][0]);
+            const bool c0 = a[q][0] < t0;
+            const float as = c0 ? a[q][1] : a[q][2];
+            const float ts = __uint_as_float(c0 ? w[q][1] : w[q][2]);
+            const bool c1 = as < ts;
+            tie |= (((a[q][0] == t0) | (as == ts)) && !(ref[q] & GK_LEAF) ? 1u : 0u) << q;
+            const uint32_t lo = c1 ? w[q][4] : w[q][5], hi = c1 ? w[q][6] : w[q][7];
+            nref[q] = c0 ? lo : hi;
+        }
+        if (__builtin_expect(tie != 0, 0)) {
+#pragma unroll
+            for (int q = 0; q < kIlp; q++) {
+                if (!(tie >> q & 1u)) continue;
+                const double *th = E.thr64 + 3 * (size_t)ref[q];
+                const uint32_t fw = w[q][3];
+                const bool c0 = x64((int)(fw & 0xFFu)) <= th[0];
+                const bool c1 = c0 ? x64((int)((fw >> 8) & 0xFFu)) <= th[1]
+                                   : x64((int)((fw >> 16) & 0xFFu)) <= th[2];
+                const uint32_t lo = c1 ? w[q][4] : w[q][5], hi = c1 ? w[q][6] : w[q][7];
+                nref[q] = c0 ? lo : hi;
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < kIlp; q++)
+            if (!(ref[q] & GK_LEAF)) ref[q] = nref[q];
+    }
+#pragma unroll
+    for (int q = 0; q < kIlp; q++) total = __dadd_rn(total, __ldg(E.leaf_val + (ref[q] & ~GK_LEAF)));
+}
+
+template <int kIlp, class X64>
+__device__ __forceinline__ double walk_ensemble_b2(const gk_ensemble &E, const float *xf, int stride,
+                                                   const X64 &x64) {
+    double total = E.base_score;
+    uint32_t t = 0;
+    for (; t + kIlp <= E.n_trees; t += kIlp) walk_b2_group<kIlp>(E, t, xf, stride, x64, total);
+    for (; t < E.n_trees; t++) walk_b2_group<1>(E, t, xf, stride, x64, total);
+    return total;
+}
+
 // power.py:144 -- (v - lo) / (hi - lo), or 0 when hi <= lo
 __device__ __forceinline__ double scale_feature(double v, double lo, double hi) {
     return hi > lo ? __ddiv_rn(__dsub_rn(v, lo), __dsub_rn(hi, lo)) : 0.0;

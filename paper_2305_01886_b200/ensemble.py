@@ -245,6 +245,104 @@ def random_forest_flat(n_trees: int, depth: int, manifest, scale_lo, scale_hi, s
                         tree_depth=np.asarray(depths, dtype=np.int32))
 
 
+BLOCK2_DT = np.dtype([("t", "<u4", (3,)), ("f", "<u4"), ("e", "<u4", (4,))])
+GK_LEAF = 0x80000000
+BLOCK2_MAX_FEAT = 255
+
+
+def f32_round_down(v: np.ndarray) -> np.ndarray:
+    """Largest float32 <= v, elementwise (NaN stays NaN; v > FLT_MAX -> FLT_MAX)."""
+    v = np.asarray(v, dtype=np.float64)
+    with np.errstate(over="ignore", invalid="ignore"):
+        f = v.astype(np.float32)
+        up = f.astype(np.float64) > v
+    f[up] = np.nextafter(f[up], np.float32(-np.inf))
+    return f
+
+
+NODE8_DT = np.dtype([("t", "<u4"), ("meta", "<u4")])
+NODE8_MAX_FEAT = 127          # feature index lives in the signed top byte (0xFF = leaf)
+NODE8_MAX_RIGHT = (1 << 24) - 1
+
+
+def nodes8(flat: FlatEnsemble) -> np.ndarray | None:
+    """gk_node8 form of `flat` (same index space), or None when the ensemble does
+    not fit it (>127 features, >16M nodes per tree).  Splits:
+    {round-down-f32(threshold), feature << 24 | left + 1}; leaves {0, 0xFF << 24 | self}."""
+    nd = flat.nodes
+    if flat.n_feat > NODE8_MAX_FEAT or len(nd) == 0:
+        return None
+    leaf = nd["feature"] < 0
+    right = nd["left"].astype(np.int64) + 1          # leaf: left = self - 1 -> right = self
+    if (right < 0).any() or (right > NODE8_MAX_RIGHT).any():
+        return None
+    out = np.zeros(len(nd), NODE8_DT)
+    out["t"][~leaf] = f32_round_down(nd["v"][~leaf]).view(np.uint32)
+    feat = np.where(leaf, 0xFF, nd["feature"]).astype(np.uint32)
+    out["meta"] = (feat << 24) | right.astype(np.uint32)
+    return out
+
+
+@dataclass
+class Blocked:
+    """Two-level blocked walk form of a FlatEnsemble (gk_block2, include/gk.h)."""
+
+    blocks: np.ndarray     # BLOCK2_DT [n_blocks]
+    thr64: np.ndarray      # f64 [3 * n_blocks]
+    leaf_val: np.ndarray   # f64 [n_leaves]
+    root: np.ndarray       # u32 [n_trees]
+
+
+def blocked(flat: FlatEnsemble) -> Blocked | None:
+    """Depth-2 blocks of every tree (vectorised over all nodes): a block per
+    internal node at even depth holding it and its two children; exits are the
+    grandchildren (a block id, or GK_LEAF | leaf id).  None if the ensemble does
+    not fit the format (>255 features, >= 2^31 blocks or leaves)."""
+    nd = flat.nodes
+    N = len(nd)
+    if flat.n_feat > BLOCK2_MAX_FEAT or N == 0 or flat.n_trees == 0:
+        return None
+    sizes = np.diff(np.append(flat.tree_off, N))
+    base = np.repeat(flat.tree_off, sizes)
+    leaf = nd["feature"] < 0
+    left = np.where(leaf, 0, base + nd["left"].astype(np.int64))
+    depth = np.full(N, -1, np.int64)
+    frontier = flat.tree_off.astype(np.int64)
+    d = 0
+    while len(frontier):
+        depth[frontier] = d
+        inner = frontier[~leaf[frontier]]
+        frontier = np.concatenate([left[inner], left[inner] + 1])
+        d += 1
+    is_blk = ~leaf & (depth % 2 == 0)
+    blk_id = np.cumsum(is_blk) - 1
+    leaf_id = np.cumsum(leaf) - 1
+    if is_blk.sum() >= GK_LEAF or leaf.sum() >= GK_LEAF:
+        return None
+
+    def ref(nodes):
+        return np.where(leaf[nodes], GK_LEAF | leaf_id[nodes], blk_id[nodes]).astype(np.uint32)
+
+    r = np.flatnonzero(is_blk)
+    slots = np.stack([r, left[r], left[r] + 1], axis=1)            # [nb, 3]
+    inner = ~leaf[slots]
+    out = np.zeros(len(r), BLOCK2_DT)
+    thr = np.where(inner, nd["v"][slots], 0.0)
+    out["t"] = np.where(inner, f32_round_down(thr).view(np.uint32), 0)
+    feat = np.where(inner, nd["feature"][slots], 0).astype(np.uint32)
+    out["f"] = feat[:, 0] | (feat[:, 1] << 8) | (feat[:, 2] << 16)
+    for k in (1, 2):
+        s_k = slots[:, k]
+        c = left[s_k]
+        lf = leaf[s_k]
+        own = ref(s_k)
+        out["e"][:, 2 * (k - 1)] = np.where(lf, own, ref(np.where(lf, s_k, c)))
+        out["e"][:, 2 * (k - 1) + 1] = np.where(lf, own, ref(np.where(lf, s_k, c + 1)))
+    return Blocked(blocks=out, thr64=np.ascontiguousarray(thr.reshape(-1)),
+                   leaf_val=np.ascontiguousarray(nd["v"][leaf]),
+                   root=ref(flat.tree_off.astype(np.int64)))
+
+
 def flat_to_document(flat: FlatEnsemble) -> dict:
     """FlatEnsemble -> reference JSON document (for cross-checks on small ensembles)."""
     trees = []

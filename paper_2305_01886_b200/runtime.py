@@ -51,7 +51,7 @@ def load_library(path: Path | None = None):
     L.gk_predict_energy_sweep.argtypes = [vp, vp, vp, vp, u32, vp, vp, vp, vp, vp, vp]
     L.gk_set_stage_timing.argtypes = [C.c_int]
     L.gk_get_stage_ms.argtypes = [vp]
-    if L.gk_abi_version() != 1:
+    if L.gk_abi_version() != 2:
         raise DeviceError("libgk ABI version mismatch")
     if path is None:
         _lib = L
@@ -178,22 +178,51 @@ class DeviceEnsemble:
     bufs: dict = field(default_factory=dict)
     desc: abi.GkEnsemble | None = None
 
+    LAYOUTS = ("nodes", "nodes8", "blocks")
+
     @classmethod
-    def upload(cls, flat) -> "DeviceEnsemble":
-        if flat.n_trees == 0:
-            # zero-tree ensembles (reference fixture ensemble_constant.json) keep one dummy node
-            pass
+    def upload(cls, flat, layout: str | None = None) -> "DeviceEnsemble":
+        """Copy a FlatEnsemble to the device in walk layout `layout`:
+        "nodes" (16-byte gk_node only), "nodes8" (+ gk_node8: 8-byte nodes) or
+        "blocks" (+ gk_block2: one 256-bit load per two levels).  Measured on
+        B200: K4 (gk_rf_predict) is fastest on blocks (1.43x on config #4's
+        random rows, which are L2/DRAM-latency bound; 7 % on the sweep's rows);
+        the fused sweep walks the 16-byte nodes unless GK_FUSED_COMPACT=1.
+        Default: $GK_WALK_LAYOUT or "blocks".  A layout the ensemble does not
+        fit falls back to "nodes"; the 16-byte nodes stay resident in every
+        layout (leaf values, exact tie thresholds)."""
+        import os
+
+        from .ensemble import blocked, nodes8
+
+        layout = layout or os.environ.get("GK_WALK_LAYOUT", "blocks")
+        if layout not in cls.LAYOUTS:
+            raise ValueError(f"walk layout must be one of {cls.LAYOUTS}, got {layout!r}")
         de = cls(flat)
         de.bufs = {"nodes": _dev(flat.nodes),
                    "off": _dev(flat.tree_off if flat.n_trees else np.zeros(1, np.int64)),
                    "depth": _dev(flat.tree_depth if flat.n_trees else np.zeros(1, np.int32)),
                    "lo": _dev(flat.scale_lo), "hi": _dev(flat.scale_hi)}
+        if layout == "nodes8":
+            n8 = nodes8(flat)
+            if n8 is not None:
+                de.bufs["nodes8"] = _dev(n8)
+        elif layout == "blocks":
+            bl = blocked(flat)
+            if bl is not None:
+                de.bufs.update(blocks=_dev(bl.blocks), thr64=_dev(bl.thr64),
+                               leaf_val=_dev(bl.leaf_val), root=_dev(bl.root))
         b = de.bufs
         de.desc = abi.GkEnsemble(_ptr(b["nodes"]), _ptr(b["off"]), _ptr(b["depth"]),
                                  _ptr(b["lo"]), _ptr(b["hi"]),
                                  float(flat.base_score), flat.n_trees, flat.n_feat,
-                                 flat.max_depth)
+                                 flat.max_depth, _ptr(b.get("nodes8")), _ptr(b.get("blocks")),
+                                 _ptr(b.get("thr64")), _ptr(b.get("leaf_val")), _ptr(b.get("root")))
         return de
+
+    @property
+    def layout(self) -> str:
+        return "blocks" if "blocks" in self.bufs else ("nodes8" if "nodes8" in self.bufs else "nodes")
 
 
 # ------------------------------------------------------------------ calls
