@@ -11,8 +11,12 @@
 // thread walks kIlp trees concurrently for its row.  Leaves are added to the
 // running total strictly in tree order, so the fp64 sum is bit-identical to
 // the reference's sequential `total += leaf`.
+#include <cooperative_groups.h>
+
 #include "gk_internal.cuh"
 #include "gk_walk.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace gk {
 
@@ -127,11 +131,10 @@ __global__ void __launch_bounds__(kRfThreads) k4_rf_predict(RfArgs R) {
 // one row per lane -- hits 32 distinct banks).
 // The exact fp64 feature is recomputed from X only for the rare a == t visit.
 template <bool kBlocks>
-__global__ void __launch_bounds__(kRfThreads) k4_rf_predict_c(RfArgs R) {
-    extern __shared__ __align__(16) float xf_raw[];
+__device__ __forceinline__ void rf_tile_c(const RfArgs &R, int64_t tile, float *xf_raw) {
     constexpr int S = kRfThreads;
     float *xf = xf_raw + S;  // row -1: the +inf slot of the leaf step
-    const int64_t row0 = (int64_t)blockIdx.x * kRfThreads;
+    const int64_t row0 = tile * kRfThreads;
     const int nr = (int)min((int64_t)kRfThreads, R.n_rows - row0);
     const int nf = (int)R.ens[0].n_feat;
     xf_raw[threadIdx.x] = __int_as_float(0x7f800000);
@@ -160,6 +163,29 @@ __global__ void __launch_bounds__(kRfThreads) k4_rf_predict_c(RfArgs R) {
                                  : walk_ensemble8<GK_RF_ILP>(E, xf + threadIdx.x, S, x64);
     R.power[row] = total;
     if (R.energy) R.energy[row] = __dmul_rn(total, R.time_us[row]);
+}
+
+template <bool kBlocks>
+__global__ void __launch_bounds__(kRfThreads) k4_rf_predict_c(RfArgs R) {
+    extern __shared__ __align__(16) float xf_raw[];
+    rf_tile_c<kBlocks>(R, blockIdx.x, xf_raw);
+}
+
+// Persistent form for large row tables: every resident CTA takes one tile per
+// round and all CTAs cross a grid barrier between rounds, so the whole GPU
+// walks the same few trees at any time -- the working set is a handful of
+// trees (L2-resident) instead of the entire ensemble (> L2), which turns the
+// deep-level node gathers from DRAM into L2 hits.
+template <bool kBlocks>
+__global__ void __launch_bounds__(kRfThreads) k4_rf_predict_rounds(RfArgs R, int64_t n_tiles) {
+    extern __shared__ __align__(16) float xf_raw[];
+    cg::grid_group grid = cg::this_grid();
+    const int64_t rounds = (n_tiles + gridDim.x - 1) / gridDim.x;
+    for (int64_t k = 0; k < rounds; k++) {
+        const int64_t tile = k * gridDim.x + blockIdx.x;
+        if (tile < n_tiles) rf_tile_c<kBlocks>(R, tile, xf_raw);
+        grid.sync();
+    }
 }
 
 }  // namespace gk
@@ -212,8 +238,35 @@ int gk_launch_rf(const gk_ensemble *ens, uint32_t n_ens, const double *X, int64_
         const int carve = (int)((need * 100 + 228 * 1024 - 1) / (228 * 1024));
         cudaFuncSetAttribute(k8, cudaFuncAttributePreferredSharedMemoryCarveout,
                              carve > 100 ? 100 : carve);
-        const int64_t blocks = (n_rows + gk::kRfThreads - 1) / gk::kRfThreads;
-        k8<<<(unsigned)blocks, gk::kRfThreads, smem8, st>>>(R);
+        const int64_t tiles = (n_rows + gk::kRfThreads - 1) / gk::kRfThreads;
+        // persistent rounds once the table spans several waves of resident CTAs
+        int dev = 0, n_sm = 0, coop = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+        const auto kp = all_blocks ? gk::k4_rf_predict_rounds<true> : gk::k4_rf_predict_rounds<false>;
+        int per_sm_p = 0;
+        if (smem8 > 48 * 1024)
+            cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem8);
+        cudaFuncSetAttribute(kp, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             carve > 100 ? 100 : carve);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_p, kp, gk::kRfThreads, smem8);
+        const int64_t resident = (int64_t)per_sm_p * n_sm;
+        const char *pe = getenv("GK_RF_ROUNDS");
+        const bool rounds_on = (pe ? atoi(pe) != 0 : true) && coop && resident > 0 &&
+                               tiles >= 4 * resident;
+        if (rounds_on) {
+            int64_t nt = tiles;
+            void *args[] = {&R, &nt};
+            cudaError_t e = cudaLaunchCooperativeKernel((const void *)kp, dim3((unsigned)resident),
+                                                        dim3(gk::kRfThreads), args, smem8, st);
+            if (e != cudaSuccess) {
+                gk_set_error("k4_rf_predict_rounds: %s", cudaGetErrorString(e));
+                return -1;
+            }
+            return gk_check_launch("k4_rf_predict_rounds");
+        }
+        k8<<<(unsigned)tiles, gk::kRfThreads, smem8, st>>>(R);
         return gk_check_launch(all_blocks ? "k4_rf_predict_c<blocks>" : "k4_rf_predict_c<nodes8>");
     }
     // one tile: leading +inf row + [feature][thread] (the staged raw rows are

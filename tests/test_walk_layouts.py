@@ -240,3 +240,33 @@ def test_fused_sweep_compact_layouts_tie_heavy_match_oracle():
             m = ok & (arch_of == a)
             assert bits_equal(power[m], want[a][0]), (layout, a)
             assert bits_equal(energy[m], want[a][1]), (layout, a)
+
+
+@pytest.mark.gpu
+def test_k4_persistent_rounds_match_oracle():
+    """Tables spanning several waves of resident CTAs take the grid-synchronised
+    persistent path (k4_rf_predict_rounds); same bits as the oracle and as the
+    one-tile-per-CTA launch."""
+    import os
+
+    import torch
+
+    import oracle as O
+    from paper_2305_01886_b200 import runtime as rt
+
+    nf, n = 15, 700_000
+    rng = np.random.default_rng(11)
+    X = rng.random((n, nf))
+    flat = random_forest_flat(30, 10, [f"f{i}" for i in range(nf)], np.zeros(nf), np.ones(nf), seed=4)
+    flat = _tie_heavy(flat, X[:5000], rng)
+    Xd = torch.tensor(X, device="cuda")
+    de = rt.DeviceEnsemble.upload(flat, layout="blocks")
+    p_rounds, _ = rt.rf_predict(de, Xd)
+    os.environ["GK_RF_ROUNDS"] = "0"
+    try:
+        p_tiles, _ = rt.rf_predict(de, Xd)
+    finally:
+        del os.environ["GK_RF_ROUNDS"]
+    want, _ = O.rf_predict(flat, X)
+    assert bits_equal(p_rounds.cpu().numpy(), want)
+    assert bits_equal(p_tiles.cpu().numpy(), want)
