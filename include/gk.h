@@ -294,6 +294,17 @@ int gk_rf_leaf_stats(const uint32_t *counts, int64_t n_rows, const int64_t *yfp,
                      const int64_t *y2fp, const void *leaves, int32_t n_leaves,
                      const int32_t *rows0, const int32_t *rows1, int64_t *out, void *stream);
 
+/* One gradient-boosting update (sklearn GradientBoostingRegressor, squared
+ * error; reference training.py:67-72 via _make_model("gradient_boosted")):
+ * rows of leaf k (tasks as for gk_rf_leaf_stats) get F += leaf_val[k]
+ * (learning_rate * leaf mean), then yfp / y2fp = the next stage's residual
+ * y - F (and its square) in fixed point 2^shift / 2^shift2, and *absmax =
+ * max(*absmax, max |y - F|) as the bit pattern of a non-negative double. */
+int gk_gb_step(const void *leaves, int32_t n_leaves, const double *leaf_val,
+               const int32_t *rows0, const int32_t *rows1, const double *y, double *F,
+               int64_t *yfp, int64_t *y2fp, int32_t shift, int32_t shift2,
+               uint64_t *absmax, int32_t max_leaf_rows, void *stream);
+
 int gk_set_stage_timing(int on);
 int gk_get_stage_ms(float *out3);
 

@@ -548,6 +548,41 @@ __global__ void k5_leaf_stats(RfTrainData D, const int64_t *__restrict__ y2fp,
     }
 }
 
+// ---------------------------------------------------------- gradient boosting
+
+// One boosting update (sklearn GradientBoostingRegressor, squared error): for
+// every row of every leaf of the stage's tree, F += leaf_val (= learning_rate *
+// leaf mean, computed like sklearn's `learning_rate * value`), then the next
+// stage's negative gradient r = y - F in fixed point (yfp = rint(r * 2^shift),
+// y2fp = rint(r^2 * 2^shift2), the K5 histogram targets) and max |r| (the
+// bits of a non-negative double order like the double) for the next shift.
+__global__ void __launch_bounds__(256) k5_gb_step(const RfTask *__restrict__ leaves,
+                                                  const double *__restrict__ leaf_val,
+                                                  const int32_t *__restrict__ rows0,
+                                                  const int32_t *__restrict__ rows1,
+                                                  const double *__restrict__ y,
+                                                  double *__restrict__ F, int64_t *__restrict__ yfp,
+                                                  int64_t *__restrict__ y2fp, int shift, int shift2,
+                                                  unsigned long long *__restrict__ absmax) {
+    const RfTask T = leaves[blockIdx.x];
+    const int32_t *rows = T.parity ? rows1 : rows0;
+    const double v = leaf_val[blockIdx.x];
+    double m = 0.0;
+    for (int p = T.begin + (int)(blockIdx.y * blockDim.x + threadIdx.x); p < T.end;
+         p += (int)(gridDim.y * blockDim.x)) {
+        const int32_t r = rows[p];
+        const double f = __dadd_rn(F[r], v);
+        F[r] = f;
+        const double g = __dsub_rn(y[r], f);
+        yfp[r] = __double2ll_rn(ldexp(g, shift));
+        y2fp[r] = __double2ll_rn(ldexp(__dmul_rn(g, g), shift2));
+        m = fmax(m, fabs(g));
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(GK_FULL, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(absmax, (unsigned long long)__double_as_longlong(m));
+}
+
 }  // namespace gk
 
 // ------------------------------------------------------------------ C-ABI
@@ -657,6 +692,26 @@ int gk_rf_leaf_stats(const uint32_t *counts, int64_t n_rows, const int64_t *yfp,
     gk::k5_leaf_stats<<<(n_leaves * 32 + 127) / 128, 128, 0, st>>>(
         D, y2fp, (const gk::RfTask *)leaves, n_leaves, rows0, rows1, out);
     return gk_check_launch("k5_leaf_stats");
+}
+
+int gk_gb_step(const void *leaves, int32_t n_leaves, const double *leaf_val,
+               const int32_t *rows0, const int32_t *rows1, const double *y, double *F,
+               int64_t *yfp, int64_t *y2fp, int32_t shift, int32_t shift2,
+               uint64_t *absmax, int32_t max_leaf_rows, void *stream) {
+    if (n_leaves <= 0) return 0;
+    if (shift < -1000 || shift > 1000 || shift2 < -1000 || shift2 > 1000) {
+        gk_set_error("gk_gb_step: fixed-point shift out of range");
+        return -1;
+    }
+    const cudaStream_t st = (cudaStream_t)stream;
+    int64_t chunks = ((int64_t)max_leaf_rows + 255) / 256;
+    if (chunks > 1024) chunks = 1024;
+    if (chunks < 1) chunks = 1;
+    dim3 grid((unsigned)n_leaves, (unsigned)chunks);
+    gk::k5_gb_step<<<grid, 256, 0, st>>>((const gk::RfTask *)leaves, leaf_val, rows0, rows1, y, F,
+                                        yfp, y2fp, shift, shift2,
+                                        (unsigned long long *)absmax);
+    return gk_check_launch("k5_gb_step");
 }
 
 }  // extern "C"

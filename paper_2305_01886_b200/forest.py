@@ -125,34 +125,20 @@ class TreeEstimator:
     random_state: int
 
 
-class RandomForestRegressor:
-    """GPU-trained random forest with scikit-learn's constructor/fit/predict."""
+class _LevelGrower:
+    """Shared K5 machinery: device binning + midpoint threshold tables
+    (`_prepare_bins`, `_thr_tables`) and level-wise growth of a batch of trees
+    over row lists (`_grow`).  Used by the random forest and by gradient
+    boosting (boosting.py)."""
 
-    def __init__(self, n_estimators: int = 100, *, max_depth: int | None = None,
-                 random_state=None, n_bins: int = N_BINS, trees_per_batch: int = 32,
-                 shard: tuple[int, int] | None = None):
-        self.n_estimators = n_estimators
-        self.max_depth = max_depth
-        self.random_state = random_state
-        self.n_bins = n_bins
-        self.trees_per_batch = trees_per_batch
-        self.shard = shard  # (rank, world): build trees t with t % world == rank
-        self.estimators_: list = []
-
-    # ------------------------------------------------------------------ fit
-    def fit(self, X, y, sample_weight=None):
+    def _prepare_bins(self, X):
+        """Bin X on the device (float32 cast like sklearn) and build the
+        midpoint threshold table; returns the [n][F] u8 bin matrix."""
         import torch
 
         from .runtime import _ptr, device
 
-        if sample_weight is not None:
-            raise NotImplementedError("sample_weight is not supported (training.py never passes it)")
-        X = np.ascontiguousarray(X, dtype=np.float64)
-        y = np.ascontiguousarray(y, dtype=np.float64).reshape(-1)
         n, F = X.shape
-        if F > 64 * 1024 or n >= 2 ** 31:
-            raise ValueError("too many rows / features")
-        self.n_features_in_ = F
         L = _lib()
         dev = device()
         edges, n_edges = bin_edges(X, self.n_bins)   # float32 sample inside
@@ -167,32 +153,7 @@ class RandomForestRegressor:
         del Xd
         self._thr_tables(bmin.cpu().numpy().view(np.uint32).reshape(F, N_BINS),
                          bmax.cpu().numpy().view(np.uint32).reshape(F, N_BINS))
-        ymax = float(np.max(np.abs(y))) if n else 1.0
-        shift = int(np.floor(62 - np.log2(max(ymax, 1e-300) * n + 1e-300)))
-        shift = max(min(shift, 60), -60)
-        yfp = torch.from_numpy(np.rint(np.ldexp(y, shift)).astype(np.int64)).to(dev)
-        y2 = y * y
-        y2max = float(np.max(y2)) if n else 1.0
-        shift2 = int(np.floor(62 - np.log2(max(y2max, 1e-300) * n + 1e-300)))
-        shift2 = max(min(shift2, 60), -60)
-        y2fp = torch.from_numpy(np.rint(np.ldexp(y2, shift2)).astype(np.int64)).to(dev)
-        yd = torch.from_numpy(y).to(dev)
-        self._dev = dict(Xb=Xb, yfp=yfp, y2fp=y2fp, y=yd, n=n, F=F, shift=shift, shift2=shift2)
-
-        seeds = tree_seeds(self.random_state, self.n_estimators)
-        todo = list(range(self.n_estimators))
-        if self.shard is not None:
-            rank, world = self.shard
-            todo = [t for t in todo if t % world == rank]
-        self.estimators_ = [None] * self.n_estimators
-        for b0 in range(0, len(todo), self.trees_per_batch):
-            batch = todo[b0: b0 + self.trees_per_batch]
-            for t, tree in zip(batch, self._grow_batch(seeds[batch])):
-                self.estimators_[t] = TreeEstimator(tree_=tree, random_state=int(seeds[t]))
-        if self.shard is None:
-            self._flat = None
-        del self._dev
-        return self
+        return Xb
 
     def _thr_tables(self, bmin_ord, bmax_ord):
         def ord2f(u):
@@ -219,7 +180,10 @@ class RandomForestRegressor:
         bad = (thr == hi) | ~np.isfinite(thr)
         self._thr = np.where(bad, lo, thr)
 
-    def _grow_batch(self, seeds):
+    def _grow(self, counts, base, m, rows0, rows1, TB):
+        """Grow TB trees level-wise over the row lists rows0[base[t] .. +m[t]]
+        (weights counts[t][row]); returns (sklearn-shaped trees, leaf records)
+        where the leaf records are (TASK_DT tasks, per-leaf node value)."""
         import torch
 
         from .runtime import _ptr, device
@@ -229,18 +193,6 @@ class RandomForestRegressor:
         D = self._dev
         n, F = D["n"], D["F"]
         st = torch.cuda.current_stream().cuda_stream
-        TB = len(seeds)
-        seeds_d = torch.from_numpy(seeds.astype(np.uint32)).to(dev)
-        counts = torch.empty(TB * n, dtype=torch.int32, device=dev)
-        _check(L.gk_rf_bootstrap(_ptr(seeds_d), TB, n, _ptr(counts), st))
-        m = (counts.view(TB, n) > 0).sum(dim=1).cpu().numpy().astype(np.int64)
-        base = np.concatenate([[0], np.cumsum(m)[:-1]]).astype(np.int64)
-        total = int(m.sum())
-        base_d = torch.from_numpy(base).to(dev)
-        rows0 = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
-        rows1 = torch.empty_like(rows0)
-        fill = torch.empty(TB, dtype=torch.int32, device=dev)
-        _check(L.gk_rf_compact(_ptr(counts), TB, n, _ptr(base_d), _ptr(rows0), _ptr(fill), st))
         max_depth = self.max_depth if self.max_depth is not None else 1 << 30
 
         # nodes get BFS ids per tree (children of one split adjacent); records are
@@ -379,7 +331,91 @@ class RandomForestRegressor:
                               feature=f, threshold=thr, value=val.reshape(-1, 1, 1), impurity=imp,
                               n_node_samples=st_[:, 0].astype(np.int64), weighted_n_node_samples=w,
                               max_depth=int(tree_depth[k])))
-        return trees
+        leaf_value = stats[node_base[lt] + ln, 2] / stats[node_base[lt] + ln, 1]
+        return trees, (lv, lv_d, leaf_value)
+
+
+
+class RandomForestRegressor(_LevelGrower):
+    """GPU-trained random forest with scikit-learn's constructor/fit/predict."""
+
+    def __init__(self, n_estimators: int = 100, *, max_depth: int | None = None,
+                 random_state=None, n_bins: int = N_BINS, trees_per_batch: int = 32,
+                 shard: tuple[int, int] | None = None):
+        self.n_estimators = n_estimators
+        self.max_depth = max_depth
+        self.random_state = random_state
+        self.n_bins = n_bins
+        self.trees_per_batch = trees_per_batch
+        self.shard = shard  # (rank, world): build trees t with t % world == rank
+        self.estimators_: list = []
+
+    # ------------------------------------------------------------------ fit
+    def fit(self, X, y, sample_weight=None):
+        import torch
+
+        from .runtime import _ptr, device
+
+        if sample_weight is not None:
+            raise NotImplementedError("sample_weight is not supported (training.py never passes it)")
+        X = np.ascontiguousarray(X, dtype=np.float64)
+        y = np.ascontiguousarray(y, dtype=np.float64).reshape(-1)
+        n, F = X.shape
+        if F > 64 * 1024 or n >= 2 ** 31:
+            raise ValueError("too many rows / features")
+        self.n_features_in_ = F
+        Xb = self._prepare_bins(X)
+        dev = device()
+        ymax = float(np.max(np.abs(y))) if n else 1.0
+        shift = int(np.floor(62 - np.log2(max(ymax, 1e-300) * n + 1e-300)))
+        shift = max(min(shift, 60), -60)
+        yfp = torch.from_numpy(np.rint(np.ldexp(y, shift)).astype(np.int64)).to(dev)
+        y2 = y * y
+        y2max = float(np.max(y2)) if n else 1.0
+        shift2 = int(np.floor(62 - np.log2(max(y2max, 1e-300) * n + 1e-300)))
+        shift2 = max(min(shift2, 60), -60)
+        y2fp = torch.from_numpy(np.rint(np.ldexp(y2, shift2)).astype(np.int64)).to(dev)
+        yd = torch.from_numpy(y).to(dev)
+        self._dev = dict(Xb=Xb, yfp=yfp, y2fp=y2fp, y=yd, n=n, F=F, shift=shift, shift2=shift2)
+
+        seeds = tree_seeds(self.random_state, self.n_estimators)
+        todo = list(range(self.n_estimators))
+        if self.shard is not None:
+            rank, world = self.shard
+            todo = [t for t in todo if t % world == rank]
+        self.estimators_ = [None] * self.n_estimators
+        for b0 in range(0, len(todo), self.trees_per_batch):
+            batch = todo[b0: b0 + self.trees_per_batch]
+            for t, tree in zip(batch, self._grow_batch(seeds[batch])):
+                self.estimators_[t] = TreeEstimator(tree_=tree, random_state=int(seeds[t]))
+        if self.shard is None:
+            self._flat = None
+        del self._dev
+        return self
+
+    def _grow_batch(self, seeds):
+        import torch
+
+        from .runtime import _ptr, device
+
+        L = _lib()
+        dev = device()
+        D = self._dev
+        n, F = D["n"], D["F"]
+        st = torch.cuda.current_stream().cuda_stream
+        TB = len(seeds)
+        seeds_d = torch.from_numpy(seeds.astype(np.uint32)).to(dev)
+        counts = torch.empty(TB * n, dtype=torch.int32, device=dev)
+        _check(L.gk_rf_bootstrap(_ptr(seeds_d), TB, n, _ptr(counts), st))
+        m = (counts.view(TB, n) > 0).sum(dim=1).cpu().numpy().astype(np.int64)
+        base = np.concatenate([[0], np.cumsum(m)[:-1]]).astype(np.int64)
+        total = int(m.sum())
+        base_d = torch.from_numpy(base).to(dev)
+        rows0 = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
+        rows1 = torch.empty_like(rows0)
+        fill = torch.empty(TB, dtype=torch.int32, device=dev)
+        _check(L.gk_rf_compact(_ptr(counts), TB, n, _ptr(base_d), _ptr(rows0), _ptr(fill), st))
+        return self._grow(counts, base, m, rows0, rows1, TB)[0]
 
     # -------------------------------------------------------------- predict
     def flat(self, leaf_scale: float = 1.0) -> FlatEnsemble:

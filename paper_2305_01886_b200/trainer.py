@@ -1,11 +1,14 @@
-"""Trainer face: ``train(dataset, "random_forest", ...)`` with the GPU forest.
+"""Trainer face: ``train(dataset, family, ...)`` with the GPU forest / GPU boosting.
 
 Mirrors ``gpukalc_trainer.training.train`` (``training.py:94-160``): canonical
 row order (mergesort by every feature, then the target; ``:82-91``), 5-fold
 ``KFold(shuffle=True, random_state=seed)``, a ``MinMaxScaler`` fit per training
 fold, fold metrics (R^2, RMSE, MAE), then a final fit on all rows.  The forest
 (``_make_model``'s RandomForestRegressor, ``:73-76``) is
-:class:`paper_2305_01886_b200.forest.RandomForestRegressor` (GPU, K5).  Export
+:class:`paper_2305_01886_b200.forest.RandomForestRegressor` (GPU, K5); the
+default family's GradientBoostingRegressor (``:67-72``) is
+:class:`paper_2305_01886_b200.boosting.GradientBoostingRegressor` (GPU, K5 +
+gk_gb_step).  Export
 follows ``export.py:26-83`` so the document loads in the reference's
 ``load_ensemble`` and in this package's.
 
@@ -23,6 +26,7 @@ from typing import Any
 
 import numpy as np
 
+from .boosting import GradientBoostingRegressor
 from .errors import TrainerError
 from .forest import RandomForestRegressor
 
@@ -68,9 +72,10 @@ def _make_model(family: str, n_estimators: int, learning_rate: float, max_depth,
     if family == "random_forest":
         return RandomForestRegressor(n_estimators=n_estimators, max_depth=max_depth,
                                      random_state=seed)
-    if family == "gradient_boosted":
-        raise TrainerError("the gradient-boosted family is not on the B200 path yet "
-                           "(SURVEY §8(f) #2); use family='random_forest'")
+    if family == "gradient_boosted":   # training.py:67-72 (GPU boosting, boosting.py)
+        kwargs = {} if max_depth is None else {"max_depth": max_depth}
+        return GradientBoostingRegressor(n_estimators=n_estimators, learning_rate=learning_rate,
+                                         random_state=seed, **kwargs)
     raise TrainerError(f"unsupported model family '{family}'; choose from {', '.join(FAMILIES)}")
 
 
@@ -164,17 +169,24 @@ def _accumulate_gains(tree, gains: np.ndarray) -> None:
 
 
 def ensemble_document(result: TrainResult) -> dict:
-    """Portable ensemble JSON (``export.py:53-83``); RF leaves x 1/n_trees."""
-    if result.family != "random_forest":
+    """Portable ensemble JSON (``export.py:53-83``): RF leaves x 1/n_trees,
+    boosted leaves x learning_rate with base_score = the init prediction."""
+    if result.family == "gradient_boosted":
+        estimators = [est[0] for est in result.model.estimators_]
+        leaf_scale = float(result.model.learning_rate)
+        base_score = float(result.model.init_.predict(np.zeros((1, len(result.manifest))))[0])
+    elif result.family == "random_forest":
+        estimators = list(result.model.estimators_)
+        leaf_scale = 1.0 / len(estimators)
+        base_score = 0.0
+    else:
         raise TrainerError(f"unsupported model family '{result.family}'")
-    estimators = list(result.model.estimators_)
-    leaf_scale = 1.0 / len(estimators)
     gains = np.zeros(len(result.manifest))
     trees = []
     for est in estimators:
         trees.append({"nodes": _tree_nodes(est.tree_, leaf_scale)})
         _accumulate_gains(est.tree_, gains)
-    return {"schema_version": 1, "base_score": 0.0, "feature_manifest": list(result.manifest),
+    return {"schema_version": 1, "base_score": base_score, "feature_manifest": list(result.manifest),
             "scaling": {"min": [float(v) for v in result.scaler.data_min_],
                         "max": [float(v) for v in result.scaler.data_max_]},
             "trees": trees, "gains": [float(g) for g in gains]}

@@ -13,6 +13,8 @@ Outputs (all small, committed):
                       predict_energy outputs on real feature rows
   rf_bootstrap.npz    sklearn RandomForestRegressor per-tree seeds + bootstrap counts
   trainer_rf.json     reference train(random_forest) fold metrics (+ harness MAPE)
+  trainer_gbt.json    reference train(gradient_boosted) fold metrics (+ harness MAPE),
+                      and the exported ensemble's test vectors of one final model
 """
 
 from __future__ import annotations
@@ -260,6 +262,50 @@ def make_trainer_metrics():
     print("trainer metrics")
 
 
+def make_trainer_gbt():
+    """Reference train(..., 'gradient_boosted') -- the trainer's DEFAULT family
+    (training.py:67-72, sklearn GradientBoostingRegressor) -- on its own
+    synthetic frame, with the same harness MAPE over the same KFold folds."""
+    from gpukalc_trainer import train
+    from gpukalc_trainer.dataset import Dataset
+    from sklearn.ensemble import GradientBoostingRegressor
+    from sklearn.model_selection import KFold
+    from sklearn.preprocessing import MinMaxScaler
+
+    sys.path.insert(0, str(REF / "trainer" / "tests"))
+    from conftest import power_frame  # the reference trainer's own generator
+
+    out = {}
+    for n, seed, n_est, lr, depth in ((600, 3, 200, 0.05, None), (2000, 5, 150, 0.1, 4),
+                                      (3000, 7, 100, 0.1, None)):
+        fr = power_frame(n, seed=seed)
+        feats = [c for c in fr.columns if c not in ("kernel", "power_w")]
+        ds = Dataset(X=fr[feats].astype(float), y=fr["power_w"].astype(float),
+                     provenance=fr[["kernel"]])
+        res = train(ds, "gradient_boosted", n_estimators=n_est, learning_rate=lr,
+                    max_depth=depth, seed=0)
+        kw = {} if depth is None else {"max_depth": depth}
+        mapes = []
+        for tr, te in KFold(5, shuffle=True, random_state=0).split(res.X):
+            sc = MinMaxScaler().fit(res.X[tr])
+            m = GradientBoostingRegressor(n_estimators=n_est, learning_rate=lr, random_state=0, **kw)
+            m.fit(sc.transform(res.X[tr]), res.y[tr])
+            pred = m.predict(sc.transform(res.X[te]))
+            mapes.append(float(np.mean(np.abs((res.y[te] - pred) / res.y[te])) * 100))
+        out[f"n{n}_seed{seed}_est{n_est}_lr{lr}_depth{depth}"] = {
+            "n_rows": n, "frame_seed": seed, "n_estimators": n_est, "learning_rate": lr,
+            "max_depth": depth, "folds": [m.as_dict() for m in res.fold_metrics],
+            "mean": res.mean_metrics.as_dict(), "fold_mape_pct": mapes,
+            "mean_mape_pct": float(np.mean(mapes)), "features": feats,
+            "init": float(res.model.init_.predict(np.zeros((1, len(feats))))[0]),
+        }
+    import sklearn
+
+    out["sklearn_version"] = sklearn.__version__
+    (HERE / "trainer_gbt.json").write_text(json.dumps(out, indent=1) + "\n")
+    print("trainer gbt metrics")
+
+
 if __name__ == "__main__":
     only = set(sys.argv[1:])
     if not only or "sched" in only:
@@ -267,6 +313,9 @@ if __name__ == "__main__":
         for name, args in SETS.items():
             make_set(name, *args)
         make_trace()
-    make_power()
-    make_bootstrap()
-    make_trainer_metrics()
+    if not only:
+        make_power()
+        make_bootstrap()
+        make_trainer_metrics()
+    if not only or "gbt" in only:
+        make_trainer_gbt()
