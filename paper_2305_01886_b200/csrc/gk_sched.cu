@@ -466,7 +466,7 @@ __device__ __forceinline__ double finish_point(const gk_corpus &C, const gk_grid
         for (uint32_t j = 0; j < O.n_sel; j++) {
             const double v = scale_feature(feature(O.sel_idx[j]), E->scale_lo[j], E->scale_hi[j]);
             xw[(size_t)j * 32] = v;
-            xf[(size_t)j * 32] = __double2float_rd(v);  // compact-walk key (gk_node8)
+            if (xf) xf[(size_t)j * 32] = __double2float_rd(v);  // compact-walk key
         }
     return time_us;
 }
@@ -540,12 +540,15 @@ __global__ void __launch_bounds__(kWarps * 32, kFused ? GK_FUSED_MINB : GK_K23_M
     double *xw = slab_base + (size_t)kWarps * 3 * ns * 32 + (size_t)warp * (O.n_sel + 1) * 32 +
                  32 + lane;
     // fused: per-warp [n_sel + 1][32] f32 keys for the compact walk after the fp64 tiles
-    float *xf = reinterpret_cast<float *>(slab_base + (size_t)kWarps * 3 * ns * 32 +
-                                          (size_t)kWarps * (O.n_sel + 1) * 32) +
-                (size_t)warp * (O.n_sel + 1) * 32 + 32 + lane;
+    // (only allocated when the fused walk uses a compact layout, F.compact)
+    float *xf = (kFused && F.compact)
+                    ? reinterpret_cast<float *>(slab_base + (size_t)kWarps * 3 * ns * 32 +
+                                                (size_t)kWarps * (O.n_sel + 1) * 32) +
+                          (size_t)warp * (O.n_sel + 1) * 32 + 32 + lane
+                    : nullptr;
     if (kFused) {
         xw[-32] = __longlong_as_double(0x7ff0000000000000ll);
-        xf[-32] = __int_as_float(0x7f800000);
+        if (xf) xf[-32] = __int_as_float(0x7f800000);
     }
 
     // dynamic work queue (items differ widely in cost; G.order puts the most
@@ -752,7 +755,8 @@ static int launch_sched(const gk_corpus *C, const gk_grid *G, const gk_kstat *ks
     const uint32_t ns = smem_rows(max_n);
     const size_t smem = G->n_arch * (sizeof(gk::ArchSmem) + (size_t)C->n_sig * sizeof(double)) +
                         (size_t)gk::kWarps * 3 * ns * 32 * sizeof(double) +
-                        (kFused ? (size_t)gk::kWarps * (n_sel + 1) * 32 * (sizeof(double) + sizeof(float))
+                        (kFused ? (size_t)gk::kWarps * (n_sel + 1) * 32 *
+                                      (sizeof(double) + (F.compact ? sizeof(float) : 0))
                                 : 0);
     if (smem > 48 * 1024) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

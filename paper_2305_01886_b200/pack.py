@@ -101,6 +101,38 @@ class Corpus:
             raise ValueError("corpus index arrays have the wrong dtype")
         return self
 
+    def slice(self, k0: int, k1: int) -> "Corpus":
+        """Kernels [k0, k1) as a self-contained corpus (offsets rebased; the
+        signature table is kept whole so latency tables stay identical)."""
+        k0, k1 = max(0, k0), min(self.n_ker, k1)
+        ker = self.ker[k0:k1].copy()
+        if k1 <= k0:
+            return Corpus(tok=np.zeros(1, TOKEN_DT), preds=np.zeros(0, np.uint16),
+                          blk=np.zeros(0, BLOCK_DT), fpreds=np.zeros(0, np.uint32),
+                          topo=np.zeros(0, np.uint32), ker=ker, sigs=list(self.sigs), names=[])
+        b0 = int(ker["blk0"][0])
+        b1 = int(ker["blk0"][-1] + ker["n_blk"][-1])
+        t0 = int(ker["tok0"][0])
+        t1 = int(ker["tok0"][-1] + ker["n_tok"][-1])
+        o0 = int(ker["topo0"][0])
+        o1 = int(ker["topo0"][-1] + ker["n_blk"][-1])
+        blk = self.blk[b0:b1].copy()
+        f0 = int(blk["fpred0"][0]) if len(blk) else 0
+        f1 = int(blk["fpred0"][-1] + blk["n_fpred"][-1]) if len(blk) else 0
+        p0, p1 = int(self.tok["pred0"][t0]), int(self.tok["pred0"][t1])
+        tok = self.tok[t0:t1 + 1].copy()          # + the sentinel (its pred0 = p1)
+        tok["pred0"] -= p0
+        tok[-1] = np.zeros((), TOKEN_DT)
+        tok["pred0"][-1] = p1 - p0
+        blk["tok0"] -= t0
+        blk["fpred0"] -= f0
+        ker["blk0"] -= b0
+        ker["topo0"] -= o0
+        ker["tok0"] -= t0
+        return Corpus(tok=tok, preds=self.preds[p0:p1].copy(), blk=blk,
+                      fpreds=self.fpreds[f0:f1].copy(), topo=self.topo[o0:o1].copy(), ker=ker,
+                      sigs=list(self.sigs), names=list(self.names[k0:k1]))
+
     def kernel_tokens(self, k: int) -> tuple[int, int]:
         return int(self.ker[k]["tok0"]), int(self.ker[k]["n_tok"])
 

@@ -342,3 +342,131 @@ class Sweep:
             self.n_sel, _ptr(self.work), _ptr(self.status), _ptr(self.time_us), _ptr(self.power),
             _ptr(self.energy), _stream(stream)))
         return self.status, self.time_us, self.power, self.energy
+
+
+class HostSweep:
+    """The energy sweep from HOST buffers to HOST results -- the reference-facing
+    batch call (cli.py:184-197's per-launch loop as one call).
+
+    Every `submit()` is one full step: the packed corpus is copied from pinned
+    host memory to the device (copy stream 1), the fused sweep runs (compute
+    stream), and (status, time_us, power_w, energy_uj) are copied back to
+    pinned host memory (copy stream 2).  Device inputs and host outputs are
+    multi-buffered (`depth` slots), so successive steps pipeline: step s + 1's
+    H2D and step s - 1's D2H run on the B200's copy engines while step s
+    computes.  `run()` = one submitted step, synchronised.
+
+    `n_chunks` > 1 additionally splits one step into kernel chunks (each a
+    self-contained sub-corpus); measured on B200 this does NOT pay for a
+    single step, because one fused launch cannot finish faster than its
+    longest work item (~2.5 ms on config #2), so it is off by default."""
+
+    def __init__(self, corpus: Corpus, profiles, configs, ensembles, sel_idx, n_chunks: int = 1,
+                 depth: int = 2):
+        t = _torch()
+        dev = device()
+        n_k = corpus.n_ker
+        n_chunks = max(1, min(n_chunks, n_k)) if n_k else 1
+        blk = corpus.blk
+        n = blk["n"].astype(np.int64)
+        if n_k and n_chunks > 1:
+            kc = np.add.reduceat(n * n + n + 1, corpus.ker["blk0"].astype(np.int64)) \
+                if len(blk) else np.ones(n_k, np.int64)
+            kc = np.where(corpus.ker["n_blk"] > 0, kc, 1)
+            cum = np.cumsum(kc)
+            cuts = [0] + [int(np.searchsorted(cum, cum[-1] * i / n_chunks)) + 1
+                          for i in range(1, n_chunks)] + [n_k]
+            cuts = sorted(set(min(max(c, 0), n_k) for c in cuts))
+        else:
+            cuts = [0, n_k]
+        self.n_cfg, self.n_arch = len(configs), len(profiles)
+        P_k = self.n_cfg * self.n_arch
+        self.n_points = n_k * P_k
+        self.depth = max(1, depth)
+        # host inputs (pinned, shared by every slot) and per-slot device state
+        self.chunks = []
+        for k0, k1 in zip(cuts[:-1], cuts[1:]):
+            if k1 <= k0 and n_k:
+                continue
+            sub = corpus.slice(k0, k1) if (k0, k1) != (0, n_k) else corpus
+            host = {}
+            for k in ("tok", "preds", "blk", "fpreds", "topo", "ker"):
+                a = np.ascontiguousarray(getattr(sub, k))
+                if len(a) == 0:
+                    a = np.zeros(1, a.dtype)
+                host[k] = t.from_numpy(a.view(np.uint8).reshape(-1) if a.dtype.fields else a) \
+                    .pin_memory()
+            slots = []
+            for _ in range(self.depth):
+                dc = DeviceCorpus.upload(sub)
+                dg = DeviceGrid.build(dc, profiles, configs)
+                slots.append({"dc": dc, "sweep": Sweep(dc, dg, ensembles, sel_idx)})
+            self.chunks.append({"host": host, "slots": slots, "p0": k0 * P_k, "p1": k1 * P_k})
+        self.h2d_bytes = sum(h.numel() * h.element_size() for c in self.chunks
+                             for h in c["host"].values())
+        self.d2h_bytes = self.n_points * (1 + 3 * 8)
+        self.outs = [{"status": t.empty(self.n_points, dtype=t.uint8).pin_memory(),
+                      "time_us": t.empty(self.n_points, dtype=t.float64).pin_memory(),
+                      "power_w": t.empty(self.n_points, dtype=t.float64).pin_memory(),
+                      "energy_uj": t.empty(self.n_points, dtype=t.float64).pin_memory()}
+                     for _ in range(self.depth)]
+        self.s_h2d = t.cuda.Stream(device=dev)
+        self.s_d2h = t.cuda.Stream(device=dev)
+        self.ev_free = [t.cuda.Event() for _ in range(self.depth)]   # slot's D2H done
+        self.n_submitted = 0
+
+    @property
+    def out(self) -> dict:
+        """Host results of the most recently submitted step."""
+        return self.outs[(self.n_submitted - 1) % self.depth]
+
+    def submit(self, stream=None) -> dict:
+        """Enqueue one step (H2D -> sweep -> D2H) on `stream` (default: the
+        current stream) and the two copy streams; returns that step's host
+        output dict (valid after synchronisation)."""
+        t = _torch()
+        cs = stream or t.cuda.current_stream()
+        k = self.n_submitted % self.depth
+        first = self.n_submitted < self.depth
+        self.n_submitted += 1
+        # the slot's previous step must have finished its D2H (which follows its compute)
+        self.s_h2d.wait_stream(cs) if first else self.s_h2d.wait_event(self.ev_free[k])
+        ev_in = []
+        with t.cuda.stream(self.s_h2d):
+            for c in self.chunks:
+                dc = c["slots"][k]["dc"]
+                for name, h in c["host"].items():
+                    dc.bufs[name].copy_(h, non_blocking=True)
+                e = t.cuda.Event()
+                e.record(self.s_h2d)
+                ev_in.append(e)
+        ev_done = []
+        for c, e in zip(self.chunks, ev_in):
+            cs.wait_event(e)
+            c["slots"][k]["sweep"].run(cs)
+            d = t.cuda.Event()
+            d.record(cs)
+            ev_done.append(d)
+        out = self.outs[k]
+        with t.cuda.stream(self.s_d2h):
+            for c, d in zip(self.chunks, ev_done):
+                self.s_d2h.wait_event(d)
+                sw, p0, p1 = c["slots"][k]["sweep"], c["p0"], c["p1"]
+                out["status"][p0:p1].copy_(sw.status, non_blocking=True)
+                out["time_us"][p0:p1].copy_(sw.time_us, non_blocking=True)
+                out["power_w"][p0:p1].copy_(sw.power, non_blocking=True)
+                out["energy_uj"][p0:p1].copy_(sw.energy, non_blocking=True)
+            self.ev_free[k].record(self.s_d2h)
+        return out
+
+    def finish(self, stream=None):
+        """Make `stream` (default: current) wait for every submitted step."""
+        t = _torch()
+        cs = stream or t.cuda.current_stream()
+        cs.wait_stream(self.s_d2h)
+        cs.wait_stream(self.s_h2d)
+
+    def run(self, stream=None) -> dict:
+        out = self.submit(stream)
+        self.finish(stream)
+        return out
