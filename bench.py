@@ -349,6 +349,7 @@ def main():
     ap.add_argument("--no-rf", action="store_true", help="skip the config #3 forest fit")
     ap.add_argument("--rf-rows", type=int, default=1_000_000)
     ap.add_argument("--rf-trees", type=int, default=64)
+    ap.add_argument("--gbt-stages", type=int, default=100)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -614,6 +615,40 @@ def rf_fit_measure(args, rank, world, threads):
                                "sample": f"scikit-learn {ts}-tree RandomForestRegressor fit, "
                                          f"{ns} rows x 64, depth 16, n_jobs={threads}",
                                "gpu_same_sample_s": gs}
+    out["gbt_fit"] = gbt_fit_measure(args, X, y, rank, world, threads)
+    return out
+
+
+def gbt_fit_measure(args, X, y, rank, world, threads):
+    """The trainer's default family (gradient boosting, training.py:67-72) on
+    the same 1M x 64 table: `--gbt-stages` depth-3 stages on the GPU (stages
+    are sequential; replicas only under torchrun), next to scikit-learn's
+    GradientBoostingRegressor (single-threaded by design) on a bounded sample."""
+    import torch
+
+    from paper_2305_01886_b200.boosting import GradientBoostingRegressor
+
+    GradientBoostingRegressor(2, random_state=0).fit(X[:4096], y[:4096])
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    GradientBoostingRegressor(args.gbt_stages, learning_rate=0.1, random_state=0).fit(X, y)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    out = {"workload": f"{len(y)} x {X.shape[1]} table, {args.gbt_stages} stages, depth 3, lr 0.1",
+           "fit_s": dt, "ms_per_stage": dt / args.gbt_stages * 1e3,
+           "timing": "host wall clock around fit(), device synced"}
+    if rank == 0 and not args.no_cpu:
+        from sklearn.ensemble import GradientBoostingRegressor as SkGBR
+
+        ns, ss = 50_000, 4
+        t0 = time.perf_counter()
+        SkGBR(n_estimators=ss, learning_rate=0.1, random_state=0).fit(X[:ns].astype(np.float32), y[:ns])
+        cs = time.perf_counter() - t0
+        out["cpu_baseline"] = {"value": cs / ss * 1e3, "unit": "ms/stage", "cores": 1,
+                               "kind": "reference",
+                               "sample": f"scikit-learn GradientBoostingRegressor, {ns} rows x "
+                                         f"{X.shape[1]}, {ss} stages (sklearn boosting is "
+                                         "single-threaded)"}
     return out
 
 
