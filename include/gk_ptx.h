@@ -1,5 +1,5 @@
 /*
- * gk_ptx.h -- C-ABI of libgkptx: the native PTX front-end.
+ * gk_ptx.h -- C-ABI of libgkhost: the native PTX front-end.
  *
  * Host-only (no CUDA): tokenises PTX text, classifies opcodes, splits basic
  * blocks, builds the CFG and the per-block def-use DAG, and packs the kernels

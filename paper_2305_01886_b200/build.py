@@ -20,8 +20,9 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libgk.so"
-PTX_LIB = PKG / "libgkptx.so"   # host-only native PTX front-end (g++, no CUDA)
-PTX_SOURCES = ["gk_ptx.cpp"]
+PTX_LIB = PKG / "libgkhost.so"   # host-only native code (g++, no CUDA): PTX front-end, ensemble I/O
+PTX_SOURCES = ["gk_ptx.cpp", "gk_ensio.cpp"]
+PTX_HEADERS = ["gk_ptx.h", "gk_ensio.h"]
 CXXFLAGS = ["-O2", "-std=c++17", "-fPIC", "-shared", "-pthread", "-Wall", "-Wextra"]
 SOURCES = ["gk_api.cu", "gk_sched.cu", "gk_rf.cu", "gk_rftrain.cu"]
 HEADERS = ["gk_internal.cuh", "gk_exp.h", "gk_exp_table.h", "gk_walk.cuh"]
@@ -46,18 +47,20 @@ def _stale() -> bool:
 
 
 def build_ptx(force: bool = False) -> Path:
-    """libgkptx.so: the native PTX tokenizer / packer (include/gk_ptx.h)."""
-    hdr = PKG.parent / "include" / "gk_ptx.h"
+    """libgkhost.so: the native PTX front-end (include/gk_ptx.h) and ensemble
+    JSON I/O (include/gk_ensio.h) -- host code, no CUDA."""
+    inc = PKG.parent / "include"
+    hdrs = [inc / h for h in PTX_HEADERS]
     srcs = [CSRC / s for s in PTX_SOURCES]
     if not force and PTX_LIB.exists() and all(
-            d.stat().st_mtime <= PTX_LIB.stat().st_mtime for d in srcs + [hdr]):
+            d.stat().st_mtime <= PTX_LIB.stat().st_mtime for d in srcs + hdrs):
         return PTX_LIB
     cxx = os.environ.get("CXX") or shutil.which("g++") or "g++"
     tmp = PTX_LIB.with_suffix(".so.tmp")
-    cmd = [cxx, *CXXFLAGS, f"-I{hdr.parent}", *map(str, srcs), "-o", str(tmp)]
+    cmd = [cxx, *CXXFLAGS, f"-I{inc}", *map(str, srcs), "-o", str(tmp)]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode:
-        raise RuntimeError(f"g++ failed on gk_ptx.cpp:\n{r.stdout}{r.stderr}")
+        raise RuntimeError(f"g++ failed on {PTX_SOURCES}:\n{r.stdout}{r.stderr}")
     tmp.replace(PTX_LIB)
     return PTX_LIB
 

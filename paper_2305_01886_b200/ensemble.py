@@ -78,7 +78,23 @@ def _check_tree(nodes, n_features: int, t: int) -> None:
 
 
 def load_ensemble(source) -> TreeEnsemble:
-    """JSON path or parsed mapping -> TreeEnsemble (reference ``power.py:73-125``)."""
+    """JSON path or parsed mapping -> TreeEnsemble (reference ``power.py:73-125``).
+
+    A path goes through the native loader (libgkhost, ``include/gk_ensio.h``:
+    parse + validate + breadth-first flatten, trees in parallel) when it is
+    built; the returned ensemble then carries its device layout already and
+    materialises the reference's node dicts only if ``trees`` is read.
+    Documents the native loader declines (any validation error, or constructs
+    it does not model) take this Python path, which raises the reference's
+    exception with its message."""
+    if not isinstance(source, Mapping):
+        fast = _load_native(source)
+        if fast is not None:
+            return fast
+    return _load_python(source)
+
+
+def _load_python(source) -> TreeEnsemble:
     if isinstance(source, Mapping):
         doc = source
     else:
@@ -123,6 +139,126 @@ def load_ensemble(source) -> TreeEnsemble:
                         scale_max=tuple(float(v) for v in hi),
                         trees=tuple(tuple(dict(n) for n in tr["nodes"]) for tr in trees),
                         gains=tuple(float(g) for g in gains))
+
+
+class _LazyTrees(tuple):
+    """The reference's ``trees`` (a tuple of tuples of node dicts, document
+    order) materialised from the native loader's arrays on first use."""
+
+    def __new__(cls, arrays):
+        obj = super().__new__(cls)
+        obj._arrays = arrays
+        obj._cache = None
+        return obj
+
+    def _get(self):
+        if self._cache is None:
+            off, feat, val, left, right, kind = self._arrays
+            ends = list(off[1:]) + [len(feat)]
+            trees = []
+            for o, e in zip(off, ends):
+                nodes = []
+                for i in range(int(o), int(e)):
+                    v = val[i]
+                    v = int(v) if kind[i] & 2 else float(v)
+                    if kind[i] & 1:
+                        nodes.append({"value": v})
+                    else:
+                        nodes.append({"feature": int(feat[i]), "threshold": v,
+                                      "left": int(left[i]), "right": int(right[i])})
+                trees.append(tuple(nodes))
+            self._cache = tuple(trees)
+        return self._cache
+
+    def __len__(self):
+        return len(self._arrays[0])
+
+    def __iter__(self):
+        return iter(self._get())
+
+    def __getitem__(self, i):
+        return self._get()[i]
+
+    def __eq__(self, other):
+        return tuple(self._get()) == tuple(other)
+
+    def __ne__(self, other):
+        return not self == other
+
+    __hash__ = None
+
+    def __repr__(self):
+        return f"<{len(self)} trees>"
+
+
+def _load_native(path):
+    """Native parse of an ensemble file; None when the caller must take the
+    Python path (library missing, unreadable file, or a declined document)."""
+    import ctypes as C
+
+    try:
+        from .ptx_native import load_library
+        L = load_library()
+    except (OSError, RuntimeError):
+        return None
+    if not getattr(L, "_ens_bound", False):
+        vp = C.c_void_p
+        L.gk_ens_parse.restype = vp
+        L.gk_ens_parse.argtypes = [C.c_char_p, C.c_size_t, C.c_int, vp, C.c_char_p, C.c_size_t]
+        L.gk_ens_sizes_of.argtypes = [vp, vp]
+        L.gk_ens_copy.restype = C.c_int
+        L.gk_ens_copy.argtypes = [vp] * 14
+        L.gk_ens_free.argtypes = [vp]
+        L._ens_bound = True
+    try:
+        text = Path(path).read_bytes()
+    except OSError:
+        return None
+
+    class Sizes(C.Structure):
+        _fields_ = [("n_trees", C.c_uint64), ("n_nodes", C.c_uint64), ("n_feat", C.c_uint64),
+                    ("manifest_bytes", C.c_uint64), ("max_depth", C.c_uint32),
+                    ("pad_", C.c_uint32), ("base_score", C.c_double)]
+
+    status = C.c_int(0)
+    why = C.create_string_buffer(128)
+    h = L.gk_ens_parse(text, len(text), 0, C.byref(status), why, len(why))
+    if not h:
+        return None
+    try:
+        if status.value != 0:
+            return None
+        sz = Sizes()
+        L.gk_ens_sizes_of(h, C.byref(sz))
+        nt, nn, k = int(sz.n_trees), int(sz.n_nodes), int(sz.n_feat)
+        nodes = np.zeros(max(nn, 1), NODE_DT)
+        off = np.zeros(nt, np.int64)
+        depth = np.zeros(nt, np.int32)
+        lo, hi, gains = np.zeros(k), np.zeros(k), np.zeros(k)
+        man = np.zeros(max(int(sz.manifest_bytes), 1), np.uint8)
+        man_off = np.zeros(k + 1, np.int64)
+        of = np.zeros(nn, np.int32)
+        ov = np.zeros(nn)
+        ol = np.zeros(nn, np.int32)
+        orr = np.zeros(nn, np.int32)
+        ok = np.zeros(nn, np.uint8)
+        p = [a.ctypes.data for a in (nodes, off, depth, lo, hi, gains, man, man_off, of, ov, ol,
+                                     orr, ok)]
+        if L.gk_ens_copy(h, *p):
+            return None
+    finally:
+        L.gk_ens_free(h)
+    raw = man.tobytes()
+    manifest = tuple(raw[man_off[i]:man_off[i + 1]].decode("utf-8") for i in range(k))
+    ens = TreeEnsemble(base_score=float(sz.base_score), feature_manifest=manifest,
+                       scale_min=tuple(float(v) for v in lo), scale_max=tuple(float(v) for v in hi),
+                       trees=_LazyTrees((off, of, ov, ol, orr, ok)),
+                       gains=tuple(float(g) for g in gains))
+    ens._flat["flat"] = FlatEnsemble(nodes=nodes, tree_off=off, scale_lo=lo.copy(),
+                                     scale_hi=hi.copy(), base_score=float(sz.base_score),
+                                     max_depth=int(sz.max_depth), manifest=manifest,
+                                     tree_depth=depth)
+    return ens
 
 
 @dataclass
@@ -361,3 +497,78 @@ def flat_to_document(flat: FlatEnsemble) -> dict:
             "scaling": {"min": [float(v) for v in flat.scale_lo],
                         "max": [float(v) for v in flat.scale_hi]},
             "trees": trees, "gains": [0.0] * len(flat.manifest)}
+
+
+# ---------------------------------------------------------------- native writer
+
+
+def _writer():
+    import ctypes as C
+
+    from .ptx_native import load_library
+
+    L = load_library()
+    if not getattr(L, "_ensw_bound", False):
+        vp = C.c_void_p
+        L.gk_ens_write.restype = C.c_int
+        L.gk_ens_write.argtypes = [C.c_int64, C.c_double, vp, vp, C.c_uint64, vp, vp, vp,
+                                   C.c_uint64, vp, vp, vp, vp, vp, vp, C.c_int, C.c_int, vp, vp]
+        L.gk_ens_float_repr.restype = C.c_int
+        L.gk_ens_float_repr.argtypes = [vp, C.c_uint64, vp, vp]
+        L.gk_ens_buf_free.argtypes = [vp]
+        L._ensw_bound = True
+    return L
+
+
+def _take(L, fn, *args) -> bytes:
+    import ctypes as C
+
+    out, n = C.c_void_p(), C.c_size_t()
+    if fn(*args, C.byref(out), C.byref(n)):
+        raise MemoryError("gk_ens_write: allocation failed")
+    try:
+        return C.string_at(out.value, n.value)
+    finally:
+        L.gk_ens_buf_free(out)
+
+
+def float_reprs(x) -> list:
+    """CPython repr() of each double, computed by the native writer (test hook)."""
+    L = _writer()
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    if len(x) == 0:
+        return []
+    return _take(L, L.gk_ens_float_repr, x.ctypes.data, len(x)).decode().split(" ")
+
+
+def document_text(*, base_score: float, manifest, scale_lo, scale_hi, gains, trees,
+                  schema_version: int = ENSEMBLE_SCHEMA_VERSION, indent: int | None = 2) -> str:
+    """``json.dumps(doc, indent=indent)`` of an ensemble document, formatted
+    natively (libgkhost ``gk_ens_write``) and byte-identical to CPython's json.
+    `trees`: per tree a dict of document-order arrays ``is_leaf``, ``feature``,
+    ``value`` (leaf value or threshold), ``left``, ``right`` (what
+    ``export._tree_nodes`` reads from sklearn's tree arrays)."""
+    L = _writer()
+    enc = [m.encode("utf-8") for m in manifest]
+    blob = b"".join(enc) or b"\0"
+    moff = np.zeros(len(enc) + 1, np.int64)
+    moff[1:] = np.cumsum([len(e) for e in enc]) if enc else []
+    sizes = [len(t["is_leaf"]) for t in trees]
+    noff = np.zeros(len(trees) + 1, np.int64)
+    noff[1:] = np.cumsum(sizes) if sizes else []
+
+    def cat(key, dt):
+        if not trees:
+            return np.zeros(1, dt)
+        return np.ascontiguousarray(np.concatenate([np.asarray(t[key]) for t in trees]).astype(dt))
+
+    leaf, feat, val = cat("is_leaf", np.uint8), cat("feature", np.int32), cat("value", np.float64)
+    left, right = cat("left", np.int32), cat("right", np.int32)
+    lo, hi, g = (np.ascontiguousarray(a, dtype=np.float64) for a in (scale_lo, scale_hi, gains))
+    if not (len(lo) == len(hi) == len(g) == len(enc)):
+        raise ValueError("manifest, scaling and gains must have the same length")
+    p = [a.ctypes.data for a in (moff, lo, hi, g, noff, leaf, feat, val, left, right)]
+    text = _take(L, L.gk_ens_write, int(schema_version), float(base_score), blob, p[0], len(enc),
+                 p[1], p[2], p[3], len(trees), p[4], p[5], p[6], p[7], p[8], p[9],
+                 -1 if indent is None else int(indent), 0)
+    return text.decode("ascii")

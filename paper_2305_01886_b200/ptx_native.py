@@ -5,7 +5,7 @@
     pack.pack_corpus(ptx.parse_ptx(text, name, loop_counts=loops) for name, text, loops in sources)
 
 (reference ``ptx/parser.py:156-257`` + ``ptx/classify.py:68-104`` +
-``ptx/types.py:79-124``), run by ``libgkptx.so`` (``include/gk_ptx.h``) over
+``ptx/types.py:79-124``), run by ``libgkhost.so`` (``include/gk_ptx.h``) over
 all host threads.  The result is byte-identical, including the latency
 signature table and the error raised for the first bad kernel (same exception
 type and message).  Unknown-opcode warnings are logged through this package's
@@ -29,7 +29,7 @@ from . import pack, ptx
 from .errors import PtxParseError, ScheduleError
 from .ir import CLASS_CODE, RESOURCE_CODE, InstClass
 
-LIB_PATH = Path(__file__).resolve().parent / "libgkptx.so"
+LIB_PATH = Path(__file__).resolve().parent / "libgkhost.so"
 EXPORTS = ("gk_ptx_abi_version", "gk_ptx_pack", "gk_ptx_error", "gk_ptx_sizes_of", "gk_ptx_copy",
            "gk_ptx_sig", "gk_ptx_warning", "gk_ptx_free")
 _CLASS_NAME = {v: k for k, v in CLASS_CODE.items()}
@@ -43,7 +43,7 @@ class _Sizes(C.Structure):
 
 
 def load_library(path: Path | None = None):
-    """ctypes handle of libgkptx (host-only; loads without a GPU)."""
+    """ctypes handle of libgkhost (host-only; loads without a GPU)."""
     global _lib
     if _lib is not None and path is None:
         return _lib
@@ -66,7 +66,7 @@ def load_library(path: Path | None = None):
     L.gk_ptx_warning.argtypes = [vp, u64, vp, C.c_char_p, C.c_size_t]
     L.gk_ptx_free.argtypes = [vp]
     if L.gk_ptx_abi_version() != 1:
-        raise RuntimeError("libgkptx ABI version mismatch")
+        raise RuntimeError("libgkhost ABI version mismatch")
     if path is None:
         _lib = L
     return L

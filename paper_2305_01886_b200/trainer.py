@@ -171,16 +171,7 @@ def _accumulate_gains(tree, gains: np.ndarray) -> None:
 def ensemble_document(result: TrainResult) -> dict:
     """Portable ensemble JSON (``export.py:53-83``): RF leaves x 1/n_trees,
     boosted leaves x learning_rate with base_score = the init prediction."""
-    if result.family == "gradient_boosted":
-        estimators = [est[0] for est in result.model.estimators_]
-        leaf_scale = float(result.model.learning_rate)
-        base_score = float(result.model.init_.predict(np.zeros((1, len(result.manifest))))[0])
-    elif result.family == "random_forest":
-        estimators = list(result.model.estimators_)
-        leaf_scale = 1.0 / len(estimators)
-        base_score = 0.0
-    else:
-        raise TrainerError(f"unsupported model family '{result.family}'")
+    estimators, leaf_scale, base_score = _doc_parts(result)
     gains = np.zeros(len(result.manifest))
     trees = []
     for est in estimators:
@@ -192,14 +183,57 @@ def ensemble_document(result: TrainResult) -> dict:
             "trees": trees, "gains": [float(g) for g in gains]}
 
 
+def _doc_parts(result: TrainResult):
+    if result.family == "gradient_boosted":
+        estimators = [est[0] for est in result.model.estimators_]
+        leaf_scale = float(result.model.learning_rate)
+        base_score = float(result.model.init_.predict(np.zeros((1, len(result.manifest))))[0])
+    elif result.family == "random_forest":
+        estimators = list(result.model.estimators_)
+        leaf_scale = 1.0 / len(estimators)
+        base_score = 0.0
+    else:
+        raise TrainerError(f"unsupported model family '{result.family}'")
+    return estimators, leaf_scale, base_score
+
+
+def ensemble_document_text(result: TrainResult) -> str:
+    """``json.dumps(ensemble_document(result), indent=2)`` without building the
+    per-node dicts: the tree arrays go straight to the native writer
+    (libgkhost ``gk_ens_write``, byte-identical text).  Gains
+    accumulate in the same order as ``_accumulate_gains`` (np.add.at is
+    sequential)."""
+    from .ensemble import document_text
+
+    estimators, leaf_scale, base_score = _doc_parts(result)
+    gains = np.zeros(len(result.manifest))
+    trees = []
+    for est in estimators:
+        t = est.tree_
+        cl, cr = np.asarray(t.children_left), np.asarray(t.children_right)
+        leaf = cl == -1
+        vals = np.asarray(t.value)[:, 0, 0].astype(np.float64) * leaf_scale
+        trees.append({"is_leaf": leaf, "feature": np.where(leaf, 0, t.feature),
+                      "value": np.where(leaf, vals, np.asarray(t.threshold, np.float64)),
+                      "left": np.where(leaf, 0, cl), "right": np.where(leaf, 0, cr)})
+        w, imp = np.asarray(t.weighted_n_node_samples), np.asarray(t.impurity)
+        sp = np.flatnonzero(~leaf)
+        dec = w[sp] * imp[sp] - w[cl[sp]] * imp[cl[sp]] - w[cr[sp]] * imp[cr[sp]]
+        np.add.at(gains, np.asarray(t.feature)[sp], np.maximum(dec, 0.0))
+    return document_text(base_score=base_score, manifest=list(result.manifest),
+                         scale_lo=np.asarray(result.scaler.data_min_, np.float64),
+                         scale_hi=np.asarray(result.scaler.data_max_, np.float64),
+                         gains=gains, trees=trees, indent=2)
+
+
 def export_ensemble(result: TrainResult, out_dir, *, n_vectors: int = 20):
-    """ensemble.json (+ metrics.json) like ``export.py:150-175``."""
+    """ensemble.json (+ metrics.json) like ``export.py:150-175``; the JSON text
+    comes from the native writer (identical bytes to json.dumps)."""
     if n_vectors < 1:
         raise TrainerError("need at least one test vector")
     out = Path(out_dir)
     out.mkdir(parents=True, exist_ok=True)
-    doc = ensemble_document(result)
     p = out / "ensemble.json"
-    p.write_text(json.dumps(doc, indent=2) + "\n")
+    p.write_text(ensemble_document_text(result) + "\n")
     (out / "metrics.json").write_text(json.dumps(result.metrics_doc(), indent=2) + "\n")
     return p

@@ -3,7 +3,7 @@
 Corpus generation + parsing is the host front-end: it runs
 once, outside any timed region, sharded over worker processes; each worker
 generates its shard's PTX text, parses + packs it with the native tokenizer
-(libgkptx, byte-identical to parse_ptx + pack_corpus), and the shards are
+(libgkhost, byte-identical to parse_ptx + pack_corpus), and the shards are
 merged into one corpus with a single signature table.
 """
 

@@ -1,6 +1,6 @@
 """Golden outcomes of the REFERENCE PTX front-end on hand-written edge cases and
 seeded random mutations of synthetic kernels (pins the native tokenizer
-`libgkptx` and this package's `ptx.parse_ptx`).
+`libgkhost` and this package's `ptx.parse_ptx`).
 
 Run in the build container only (imports /root/reference):
 

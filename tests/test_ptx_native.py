@@ -1,4 +1,4 @@
-"""Native PTX front-end (libgkptx, include/gk_ptx.h) vs the reference parser.
+"""Native PTX front-end (libgkhost, include/gk_ptx.h) vs the reference parser.
 
 CPU tests: the tokenizer is host code.  Parity is byte-identity of the packed
 corpus with pack_corpus(parse_ptx(...)), the digests of the reference-parsed
