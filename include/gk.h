@@ -305,6 +305,27 @@ int gk_gb_step(const void *leaves, int32_t n_leaves, const double *leaf_val,
                int64_t *yfp, int64_t *y2fp, int32_t shift, int32_t shift2,
                uint64_t *absmax, int32_t max_leaf_rows, void *stream);
 
+/* ---- correlation pruning statistics (gk_corr.cu) -------
+ * Reference: gpukalc_trainer/dataset.py:138-193 -> DataFrame.corr("pearson")
+ * and DataFrame.corr("kendall") (scipy.stats.kendalltau tau-b per pair).
+ * X is [n][ld] row-major fp64 on the device, finite values.  Workspaces are
+ * caller-allocated device memory of the *_workspace() size. */
+size_t gk_corr_ranks_workspace(int64_t n);
+/* dense ranks (ranks[c * n + row]), unique counts and tie sums per column */
+int gk_corr_ranks(const double *X, int64_t n, int32_t K, int64_t ld, uint32_t *ranks,
+                  uint32_t *n_unique, int64_t *ties, void *ws, size_t ws_bytes, void *stream);
+size_t gk_corr_kendall_workspace(int64_t n, int32_t max_pairs);
+/* per pair p (x = column pa[p], y = column pb[p]): strictly discordant pairs
+ * and joint ties -- the exact integers of scipy's tau-b */
+int gk_corr_kendall(const uint32_t *ranks, int64_t n, int32_t K, const uint32_t *n_unique_host,
+                    const int32_t *pa, const int32_t *pb, const int32_t *pa_d, const int32_t *pb_d,
+                    int32_t P, int64_t *dis, int64_t *ntie, void *ws, size_t ws_bytes,
+                    void *stream);
+size_t gk_corr_pearson_workspace(int64_t n, int32_t K);
+/* column means and centred co-moments (upper triangle, row-major), fixed-order sums */
+int gk_corr_pearson(const double *X, int64_t n, int32_t K, int64_t ld, double *mean,
+                    double *comoment, void *ws, size_t ws_bytes, void *stream);
+
 int gk_set_stage_timing(int on);
 int gk_get_stage_ms(float *out3);
 

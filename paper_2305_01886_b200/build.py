@@ -24,7 +24,7 @@ PTX_LIB = PKG / "libgkhost.so"   # host-only native code (g++, no CUDA): PTX fro
 PTX_SOURCES = ["gk_ptx.cpp", "gk_ensio.cpp"]
 PTX_HEADERS = ["gk_ptx.h", "gk_ensio.h"]
 CXXFLAGS = ["-O2", "-std=c++17", "-fPIC", "-shared", "-pthread", "-Wall", "-Wextra"]
-SOURCES = ["gk_api.cu", "gk_sched.cu", "gk_rf.cu", "gk_rftrain.cu"]
+SOURCES = ["gk_api.cu", "gk_sched.cu", "gk_rf.cu", "gk_rftrain.cu", "gk_corr.cu"]
 HEADERS = ["gk_internal.cuh", "gk_exp.h", "gk_exp_table.h", "gk_walk.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ["-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
