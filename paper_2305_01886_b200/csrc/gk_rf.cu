@@ -254,7 +254,7 @@ int gk_launch_rf(const gk_ensemble *ens, uint32_t n_ens, const double *X, int64_
         const int64_t resident = (int64_t)per_sm_p * n_sm;
         const char *pe = getenv("GK_RF_ROUNDS");
         const bool rounds_on = (pe ? atoi(pe) != 0 : true) && coop && resident > 0 &&
-                               tiles >= 4 * resident;
+                               tiles >= 32 * resident;
         if (rounds_on) {
             int64_t nt = tiles;
             void *args[] = {&R, &nt};
