@@ -289,10 +289,12 @@ int gk_rf_partition(const uint8_t *Xb, const int64_t *yfp, const double *y,
                     int32_t n_tasks, const void *split, const int32_t *ids, int32_t n_ids,
                     int32_t max_rows, int32_t *rows0, int32_t *rows1, int32_t *cursor,
                     void *stream);
-/* per leaf segment: int64 {n, sum w, sum w*yfp, sum w*y2fp} (exact fixed-point sums) */
+/* per leaf segment: int64 {n, sum w, sum w*yfp, sum w*y2fp} (exact fixed-point
+ * sums); max_leaf_rows (the largest segment) sizes the row-chunk grid */
 int gk_rf_leaf_stats(const uint32_t *counts, int64_t n_rows, const int64_t *yfp,
                      const int64_t *y2fp, const void *leaves, int32_t n_leaves,
-                     const int32_t *rows0, const int32_t *rows1, int64_t *out, void *stream);
+                     const int32_t *rows0, const int32_t *rows1, int64_t *out,
+                     int32_t max_leaf_rows, void *stream);
 
 /* One gradient-boosting update (sklearn GradientBoostingRegressor, squared
  * error; reference training.py:67-72 via _make_model("gradient_boosted")):

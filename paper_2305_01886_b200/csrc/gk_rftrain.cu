@@ -208,6 +208,9 @@ __device__ __forceinline__ BestSplit eval_feature(const uint64_t *cw, const int6
     for (int j = 0; j < 8; j++) {
         const int b = lane * 8 + j;
         if (b >= kBins - 1) continue;
+        // an empty bin repeats the previous boundary's split, whose proxy ties
+        // and wins (lower bin): only non-empty bins are candidates (exact)
+        if (c8[j] == (j ? c8[j - 1] : 0ull)) continue;
         const uint64_t cl = cpre + c8[j];
         const uint32_t CL = (uint32_t)(cl >> 32), WL = (uint32_t)cl;
         if (CL < 1 || C - CL < 1) continue;
@@ -442,24 +445,33 @@ __global__ void __launch_bounds__(128) k5_split_small(RfTrainData D, const RfTas
     uint64_t *cw = hcw[threadIdx.x >> 5];
     int64_t *hsw = hs[threadIdx.x >> 5];
     BestSplit best{-1.0, 0x7fffffff, 0x7fffffff, 0};
-    for (int f = 0; f < D.F; f++) {
+    // zero once; after each feature every lane clears only the bins it filled
 #pragma unroll
-        for (int j = 0; j < kBins / 32; j++) {
-            cw[lane + 32 * j] = 0;
-            hsw[lane + 32 * j] = 0;
-        }
-        __syncwarp();
+    for (int j = 0; j < kBins / 32; j++) {
+        cw[lane + 32 * j] = 0;
+        hsw[lane + 32 * j] = 0;
+    }
+    __syncwarp();
+    for (int f = 0; f < D.F; f++) {
+        int bin[2];
 #pragma unroll
         for (int h = 0; h < 2; h++) {
-            if (r[h] >= 0) {
-                const int b = D.Xb[(size_t)r[h] * D.F + f];
-                atomicAdd((unsigned long long *)&cw[b], (unsigned long long)((1ull << 32) | w[h]));
-                atomicAdd((unsigned long long *)&hsw[b], (unsigned long long)s[h]);
+            bin[h] = r[h] >= 0 ? D.Xb[(size_t)r[h] * D.F + f] : -1;
+            if (bin[h] >= 0) {
+                atomicAdd((unsigned long long *)&cw[bin[h]], (unsigned long long)((1ull << 32) | w[h]));
+                atomicAdd((unsigned long long *)&hsw[bin[h]], (unsigned long long)s[h]);
             }
         }
         __syncwarp();
         const BestSplit b = eval_feature(cw, hsw, f, lane);
         if (better(b.proxy, b.feat, b.bin, best)) best = b;
+        __syncwarp();
+#pragma unroll
+        for (int h = 0; h < 2; h++)
+            if (bin[h] >= 0) {
+                cw[bin[h]] = 0;
+                hsw[bin[h]] = 0;
+            }
         __syncwarp();
     }
 #pragma unroll
@@ -513,21 +525,23 @@ __global__ void __launch_bounds__(256) k5_partition(RfTrainData D, const RfTask 
 
 // ---------------------------------------------------------------- leaf stats
 
-// one warp per leaf segment: n, sum w, sum w*y, sum w*y^2 as exact 64-bit
-// fixed-point integer sums (row order inside a segment is not deterministic,
-// integer sums are); y2fp = y^2 in its own fixed-point scale
+// leaf segments: n, sum w, sum w*y, sum w*y^2 as exact 64-bit fixed-point
+// integer sums (row order inside a segment is not deterministic, integer sums
+// are).  grid = (leaf, row chunk): a few warps per large leaf accumulate into
+// out[] with integer atomics (associative: still exact and deterministic).
+// y2fp = y^2 in its own fixed-point scale; out must be zeroed.
 __global__ void k5_leaf_stats(RfTrainData D, const int64_t *__restrict__ y2fp,
                               const RfTask *__restrict__ leaves, int n_leaves,
                               const int32_t *__restrict__ rows0, const int32_t *__restrict__ rows1,
                               int64_t *__restrict__ out /*[n_leaves][4]*/) {
     const int lane = threadIdx.x & 31;
-    const int li = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (li >= n_leaves) return;
+    const int li = blockIdx.x;
     const RfTask T = leaves[li];
     const int32_t *rows = T.parity ? rows1 : rows0;
     const uint32_t *cnt = D.counts + (size_t)T.tree * D.n;
     long long w = 0, sy = 0, sy2 = 0;
-    for (int p = T.begin + lane; p < T.end; p += 32) {
+    const int stride = gridDim.y * blockDim.x;
+    for (int p = T.begin + blockIdx.y * blockDim.x + threadIdx.x; p < T.end; p += stride) {
         const int32_t r = rows[p];
         const long long ww = cnt[r];
         w += ww;
@@ -540,12 +554,12 @@ __global__ void k5_leaf_stats(RfTrainData D, const int64_t *__restrict__ y2fp,
         sy += __shfl_xor_sync(GK_FULL, sy, o);
         sy2 += __shfl_xor_sync(GK_FULL, sy2, o);
     }
-    if (lane == 0) {
-        out[4 * li + 0] = T.end - T.begin;
-        out[4 * li + 1] = w;
-        out[4 * li + 2] = sy;
-        out[4 * li + 3] = sy2;
+    if (lane == 0 && (w | sy | sy2)) {
+        atomicAdd((unsigned long long *)&out[4 * li + 1], (unsigned long long)w);
+        atomicAdd((unsigned long long *)&out[4 * li + 2], (unsigned long long)sy);
+        atomicAdd((unsigned long long *)&out[4 * li + 3], (unsigned long long)sy2);
     }
+    if (blockIdx.y == 0 && threadIdx.x == 0) out[4 * li + 0] = T.end - T.begin;
 }
 
 // ---------------------------------------------------------- gradient boosting
@@ -685,11 +699,19 @@ int gk_rf_partition(const uint8_t *Xb, const int64_t *yfp, const double *y,
 
 int gk_rf_leaf_stats(const uint32_t *counts, int64_t n_rows, const int64_t *yfp,
                      const int64_t *y2fp, const void *leaves, int32_t n_leaves,
-                     const int32_t *rows0, const int32_t *rows1, int64_t *out, void *stream) {
+                     const int32_t *rows0, const int32_t *rows1, int64_t *out,
+                     int32_t max_leaf_rows, void *stream) {
     if (n_leaves <= 0) return 0;
     const cudaStream_t st = (cudaStream_t)stream;
     gk::RfTrainData D{nullptr, yfp, nullptr, counts, n_rows, 0};
-    gk::k5_leaf_stats<<<(n_leaves * 32 + 127) / 128, 128, 0, st>>>(
+    cudaMemsetAsync(out, 0, sizeof(int64_t) * 4 * (size_t)n_leaves, st);
+    // chunks sized by the largest leaf (one 32-lane warp per 2048 rows, <= 64)
+    int max_rows = 0;
+    if (max_leaf_rows > 0) max_rows = max_leaf_rows;
+    int chunks = (max_rows + 2047) / 2048;
+    if (chunks < 1) chunks = 1;
+    if (chunks > 64) chunks = 64;
+    gk::k5_leaf_stats<<<dim3((unsigned)n_leaves, (unsigned)chunks), 32, 0, st>>>(
         D, y2fp, (const gk::RfTask *)leaves, n_leaves, rows0, rows1, out);
     return gk_check_launch("k5_leaf_stats");
 }

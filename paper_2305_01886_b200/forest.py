@@ -53,7 +53,7 @@ def _lib():
         L.gk_rf_hist_bytes.restype = C.c_size_t
         L.gk_rf_partition.argtypes = [vp, vp, vp, vp, i64, i32, vp, i32, vp, vp, i32, i32, vp,
                                       vp, vp, vp]
-        L.gk_rf_leaf_stats.argtypes = [vp, i64, vp, vp, vp, i32, vp, vp, vp, vp]
+        L.gk_rf_leaf_stats.argtypes = [vp, i64, vp, vp, vp, i32, vp, vp, vp, i32, vp]
         L._rf_bound = True
     return L
 
@@ -287,7 +287,8 @@ class _LevelGrower:
         lv_d = torch.from_numpy(lv.view(np.uint8)).to(dev)
         stats_d = torch.empty(4 * len(lt), dtype=torch.int64, device=dev)
         _check(L.gk_rf_leaf_stats(_ptr(counts), n, _ptr(D["yfp"]), _ptr(D["y2fp"]), _ptr(lv_d),
-                                  len(lt), _ptr(rows0), _ptr(rows1), _ptr(stats_d), st))
+                                  len(lt), _ptr(rows0), _ptr(rows1), _ptr(stats_d),
+                                  int((le - lb).max()) if len(lt) else 0, st))
         # exactly-sized node arrays
         node_base = np.concatenate([[0], np.cumsum(next_id)[:-1]]).astype(np.int64)
         n_nodes_tot = int(next_id.sum())
