@@ -650,13 +650,13 @@ int gk_rf_split_level(const uint8_t *Xb, const int64_t *yfp, const double *y,
     const gk::RfTask *T = (const gk::RfTask *)tasks;
     gk::RfSplit *out = (gk::RfSplit *)split_out;
     const size_t smem = sizeof(gk::HistSmem);
-    static bool attr = false;
-    if (!attr) {
+    static const bool attr = [smem] {  // thread-safe one-time init (concurrent tree batches)
         cudaFuncSetAttribute(gk::k5_split_medium, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(gk::k5_hist_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(gk::k5_eval_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-    }
+        return true;
+    }();
+    (void)attr;
     if (n_small > 0)
         gk::k5_split_small<<<(n_small * 32 + 127) / 128, 128, 0, st>>>(D, T, small_ids, n_small,
                                                                        rows0, rows1, out);

@@ -342,13 +342,14 @@ class RandomForestRegressor(_LevelGrower):
 
     def __init__(self, n_estimators: int = 100, *, max_depth: int | None = None,
                  random_state=None, n_bins: int = N_BINS, trees_per_batch: int = 32,
-                 shard: tuple[int, int] | None = None):
+                 shard: tuple[int, int] | None = None, concurrent: bool = True):
         self.n_estimators = n_estimators
         self.max_depth = max_depth
         self.random_state = random_state
         self.n_bins = n_bins
         self.trees_per_batch = trees_per_batch
         self.shard = shard  # (rank, world): build trees t with t % world == rank
+        self.concurrent = concurrent  # overlap two tree batches (host work vs kernels)
         self.estimators_: list = []
 
     # ------------------------------------------------------------------ fit
@@ -385,9 +386,30 @@ class RandomForestRegressor(_LevelGrower):
             rank, world = self.shard
             todo = [t for t in todo if t % world == rank]
         self.estimators_ = [None] * self.n_estimators
-        for b0 in range(0, len(todo), self.trees_per_batch):
-            batch = todo[b0: b0 + self.trees_per_batch]
-            for t, tree in zip(batch, self._grow_batch(seeds[batch])):
+        batches = [todo[b0: b0 + self.trees_per_batch]
+                   for b0 in range(0, len(todo), self.trees_per_batch)]
+        # two batches in flight on their own streams: one batch's host-side level
+        # bookkeeping (numpy, GIL released) overlaps the other's kernels
+        streams = [torch.cuda.Stream(device=dev) for _ in range(min(2, len(batches)))]
+        main = torch.cuda.current_stream(dev)
+
+        def grow(k):
+            s = streams[k % len(streams)]
+            s.wait_stream(main)
+            with torch.cuda.stream(s):
+                trees = self._grow_batch(seeds[batches[k]])
+            s.synchronize()
+            return trees
+
+        if len(batches) > 1 and self.concurrent:
+            from concurrent.futures import ThreadPoolExecutor
+
+            with ThreadPoolExecutor(max_workers=len(streams)) as ex:
+                results = list(ex.map(grow, range(len(batches))))
+        else:
+            results = [grow(k) for k in range(len(batches))]
+        for batch, trees in zip(batches, results):
+            for t, tree in zip(batch, trees):
                 self.estimators_[t] = TreeEstimator(tree_=tree, random_state=int(seeds[t]))
         if self.shard is None:
             self._flat = None
