@@ -588,6 +588,10 @@ def rf_fit_measure(args, rank, world, threads):
     t0 = time.perf_counter()
     m = RandomForestRegressor(args.rf_trees, max_depth=16, random_state=0,
                               shard=(rank, world) if world > 1 else None).fit(X, y)
+    if world > 1:   # every rank ends with the whole forest (NCCL all-gather of the trees)
+        from paper_2305_01886_b200.dist import allgather_forest
+
+        allgather_forest(m)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     t = torch.tensor([dt], dtype=torch.float64, device="cuda")
@@ -599,7 +603,8 @@ def rf_fit_measure(args, rank, world, threads):
                        f"{args.rf_trees} trees measured (tree-sharded over {world} GPU)",
            "fit_s": dt, "s_per_tree": dt / args.rf_trees,
            "fit_s_500_trees_extrapolated": dt * 500 / args.rf_trees,
-           "nodes_per_tree": nodes, "timing": "host wall clock around fit(), device synced"}
+           "nodes_per_tree": nodes,
+           "timing": "host wall clock around fit() (+ the tree all-gather at N > 1), device synced"}
     if rank == 0 and not args.no_cpu:
         from sklearn.ensemble import RandomForestRegressor as SkRF
 

@@ -88,18 +88,70 @@ def broadcast_flat(flat, src: int = 0, group=None, device=None):
                         tree_depth=dep.cpu().numpy())
 
 
-def allgather_forest(model, group=None):
-    """Complete a tree-sharded forest on every rank: each rank contributes the
-    trees it built (estimators_[t] for t % world == rank), in global tree order."""
+_TREE_INT = ("children_left", "children_right", "feature", "n_node_samples")
+_TREE_F64 = ("threshold", "impurity", "weighted_n_node_samples")
+
+
+def _pack_trees(items) -> np.ndarray:
+    """[(tree id, TreeEstimator)] -> one byte buffer (int64 header + arrays)."""
+    parts = []
+    for t, est in items:
+        tr = est.tree_
+        nc = int(tr.node_count)
+        parts.append(np.array([t, nc, int(tr.max_depth), int(est.random_state)], np.int64))
+        parts += [np.asarray(getattr(tr, k), np.int64).reshape(nc) for k in _TREE_INT]
+        parts += [np.asarray(getattr(tr, k), np.float64).reshape(nc) for k in _TREE_F64]
+        parts.append(np.asarray(tr.value, np.float64).reshape(nc))
+    if not parts:
+        return np.zeros(0, np.uint8)
+    return np.concatenate([p.view(np.uint8) for p in parts])
+
+
+def _unpack_trees(buf: np.ndarray) -> dict:
+    from .forest import Tree, TreeEstimator
+
+    out, at = {}, 0
+    w = buf.view(np.int64) if len(buf) else np.zeros(0, np.int64)
+    while at < len(w):
+        t, nc, md, rs = (int(v) for v in w[at:at + 4])
+        at += 4
+        cols = {}
+        for k in _TREE_INT:
+            cols[k] = w[at:at + nc].copy()
+            at += nc
+        f = buf.view(np.float64)
+        for k in _TREE_F64:
+            cols[k] = f[at:at + nc].copy()
+            at += nc
+        value = f[at:at + nc].copy().reshape(nc, 1, 1)
+        at += nc
+        out[t] = TreeEstimator(tree_=Tree(node_count=nc, value=value, max_depth=md, **cols),
+                               random_state=rs)
+    return out
+
+
+def allgather_forest(model, group=None, device=None):
+    """Complete a tree-sharded forest on every rank: each rank's trees
+    (estimators_[t] for t % world == rank) are packed into one byte tensor and
+    all-gathered (NCCL over NVLink on the GPU box, gloo in the CPU tests), then
+    unpacked in global tree order."""
+    import torch
     import torch.distributed as dist
 
-    world = dist.get_world_size(group)
-    mine = {t: e for t, e in enumerate(model.estimators_) if e is not None}
-    parts = [None] * world
-    dist.all_gather_object(parts, mine, group=group)
+    mine = [(t, e) for t, e in enumerate(model.estimators_) if e is not None]
+    dev = device or (torch.device("cuda", torch.cuda.current_device())
+                     if dist.get_backend(group) == "nccl" else torch.device("cpu"))
+    buf = torch.from_numpy(_pack_trees(mine)).to(dev)
+    (gathered,) = allgather_results([buf], group=group)
     merged = {}
-    for p in parts:
-        merged.update(p)
+    # the concatenation is in rank order; each rank's part parses independently
+    sizes = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(dist.get_world_size(group))]
+    dist.all_gather(sizes, torch.tensor([buf.numel()], dtype=torch.int64, device=dev), group=group)
+    host = gathered.cpu().numpy()
+    at = 0
+    for sz in (int(s.item()) for s in sizes):
+        merged.update(_unpack_trees(host[at:at + sz]))
+        at += sz
     if sorted(merged) != list(range(model.n_estimators)):
         raise RuntimeError("tree shards do not cover the forest")
     model.estimators_ = [merged[t] for t in range(model.n_estimators)]

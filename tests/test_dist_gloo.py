@@ -84,22 +84,44 @@ def test_broadcast_flat_ensemble():
         assert dep == list(ref.tree_depth) and man == ("a", "b", "c")
 
 
+def _tiny_tree(t):
+    from paper_2305_01886_b200.forest import Tree
+
+    nc = 3 + 2 * (t % 2)
+    rng = np.random.default_rng(t)
+    return Tree(node_count=nc, children_left=np.r_[1, [-1] * (nc - 1)].astype(np.int64),
+                children_right=np.r_[2, [-1] * (nc - 1)].astype(np.int64),
+                feature=rng.integers(0, 4, nc), threshold=rng.random(nc),
+                value=rng.random((nc, 1, 1)), impurity=rng.random(nc),
+                n_node_samples=rng.integers(1, 99, nc),
+                weighted_n_node_samples=rng.random(nc) * 10, max_depth=1 + t % 3)
+
+
 def _forest_fn(rank, world):
     from paper_2305_01886_b200.dist import allgather_forest
     from paper_2305_01886_b200.forest import RandomForestRegressor, TreeEstimator
 
     # a tree-sharded forest as fit(shard=(rank, world)) leaves it (no GPU needed)
     m = RandomForestRegressor(5, random_state=0, shard=(rank, world))
-    m.estimators_ = [TreeEstimator(tree_=f"tree{t}", random_state=t) if t % world == rank else None
-                     for t in range(5)]
+    m.estimators_ = [TreeEstimator(tree_=_tiny_tree(t), random_state=100 + t)
+                     if t % world == rank else None for t in range(5)]
     allgather_forest(m)
-    return [e.tree_ for e in m.estimators_]
+    return [(e.random_state, e.tree_.node_count, e.tree_.max_depth,
+             e.tree_.threshold.tolist(), e.tree_.value.tolist(), e.tree_.feature.tolist(),
+             e.tree_.children_left.tolist(), e.tree_.weighted_n_node_samples.tolist())
+            for e in m.estimators_]
 
 
 def test_tree_sharded_forest_reassembles_in_order():
     out = _spawn(_forest_fn)
+    want = []
+    for t in range(5):
+        tr = _tiny_tree(t)
+        want.append((100 + t, tr.node_count, tr.max_depth, tr.threshold.tolist(),
+                     tr.value.tolist(), tr.feature.tolist(), tr.children_left.tolist(),
+                     tr.weighted_n_node_samples.tolist()))
     for r in (0, 1):
-        assert out[r] == [f"tree{t}" for t in range(5)]
+        assert out[r] == want
 
 
 def test_kernel_shards_partition_the_corpus():
