@@ -225,9 +225,19 @@ __device__ __forceinline__ double schedule_block(const gk_corpus &C, const gk_bl
     double delay = 0.0;
     bool neg = false;  // a negative-length span exists: ends may be unsorted
     const gk_token *tok = C.tok + B.tok0;
+    gk_token Tn = tok[0];  // carried: token i + 1 is loaded once (its pred0 ends i's list)
     for (uint32_t i = 0; i < B.n; i++) {
-        const gk_token T = tok[i];
-        const uint32_t p1 = tok[i + 1].pred0;
+        const gk_token T = Tn;
+        Tn = tok[i + 1];  // the next block's first token or the corpus sentinel
+        const uint32_t p1 = Tn.pred0;
+        // the resource list's last span, loaded early: the probe's first step
+        // and the insertion's first compare read it (70 % of inserts append)
+        const uint32_t base = T.lst_row, L = T.lst_len;
+        double s_last = 0.0, e_last = 0.0;
+        if (L) {
+            s_last = ROW(m.ss, base + L - 1);
+            e_last = ROW(m.se, base + L - 1);
+        }
         double dterm, gap;
         int64_t nb;
         RT.pick(T.res, dterm, gap, nb);
@@ -240,7 +250,6 @@ __device__ __forceinline__ double schedule_block(const gk_corpus &C, const gk_bl
         // earliest_start (scheduler.py:59-68).  With only non-negative spans
         // the list is disjoint, so its ends are sorted and every span before
         // the first end > ready is skipped by the reference's `continue`.
-        const uint32_t base = T.lst_row, L = T.lst_len;
         // first span with end > ready: probe back from the frontier (ready is
         // usually near it -- measured: 39 % of queries need no span at all),
         // binary search only past GK_PROBE steps
@@ -248,9 +257,13 @@ __device__ __forceinline__ double schedule_block(const gk_corpus &C, const gk_bl
         if (!neg) {
             k = L;
             int steps = 0;
-            while (k > 0 && steps < GK_PROBE && ROW(m.se, base + k - 1) > ready) {
+            if (k > 0 && e_last > ready) {
                 k--;
                 steps++;
+                while (k > 0 && steps < GK_PROBE && ROW(m.se, base + k - 1) > ready) {
+                    k--;
+                    steps++;
+                }
             }
             if (k > 0 && steps == GK_PROBE && ROW(m.se, base + k - 1) > ready) {
                 uint32_t lo = 0, hi = k - 1;
@@ -292,12 +305,17 @@ __device__ __forceinline__ double schedule_block(const gk_corpus &C, const gk_bl
         // insort-right on (start, end) tuples (scheduler.py:70-71): one
         // insertion-sort step from the back (70 % of inserts append)
         uint32_t q = L;
-        while (q > 0) {
-            const double s = ROW(m.ss, base + q - 1), e = ROW(m.se, base + q - 1);
-            if (!(start < s || (start == s && end < e))) break;
-            ROW(m.ss, base + q) = s;
-            ROW(m.se, base + q) = e;
+        if (q > 0 && (start < s_last || (start == s_last && end < e_last))) {
+            ROW(m.ss, base + q) = s_last;
+            ROW(m.se, base + q) = e_last;
             q--;
+            while (q > 0) {
+                const double s = ROW(m.ss, base + q - 1), e = ROW(m.se, base + q - 1);
+                if (!(start < s || (start == s && end < e))) break;
+                ROW(m.ss, base + q) = s;
+                ROW(m.se, base + q) = e;
+                q--;
+            }
         }
         ROW(m.ss, base + q) = start;
         ROW(m.se, base + q) = end;
@@ -505,7 +523,7 @@ struct FusedArgs {
 #define GK_K23_MINB 6
 #endif
 #ifndef GK_FUSED_MINB
-#define GK_FUSED_MINB 6
+#define GK_FUSED_MINB 7  // measured: 6.56 ms vs 6.67 (6) and 6.66 (8) on config #2
 #endif
 #ifndef GK_FUSED_ILP
 #define GK_FUSED_ILP 8  // trees walked in lock-step inside the fused sweep (8 measured best)
