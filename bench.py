@@ -50,6 +50,8 @@ def ncu_traffic(workload: str, kernel: str, units: int):
     src = f"ncu --set full, {rec['capture']}"
     if rec["units"] != units:
         src += f"; scaled from {rec['units']} to {units} {rec['unit']}s"
+    if rec.get("binding"):
+        src += f"; binding unit (ncu): {rec['binding']}"
     return per_unit * units, src
 
 
