@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(kRfThreads) k4_rf_predict(RfArgs R) {
 }
 
 #ifndef GK_RF_B2_ILP
-#define GK_RF_B2_ILP 4
+#define GK_RF_B2_ILP 10  // config #4: 82 M rows/s (8: 72 M, 4: 52 M, 12: 51 M)
 #endif
 // K4 over compact layouts (gk_node8 / gk_block2): the CTA's row tile is loaded
 // coalesced, scaled, rounded toward -inf to f32 and stored transposed

@@ -17,48 +17,46 @@ namespace gk {
 // x: this row's scaled features, feature f at x[f * stride], and x[-stride]
 // must hold +inf: a leaf {value, -1, self - 1} then compares +inf <= value
 // (false) and steps "right" to itself, so walks absorb without a leaf test.
+template <int kIlp, bool kTail>
+__device__ __forceinline__ void walk16_group(const gk_ensemble &E, uint32_t t, int nq,
+                                             const double *x, int stride, double &total) {
+    const gk_node *__restrict__ nodes = E.nodes;
+    const gk_node *base[kIlp];
+    int32_t idx[kIlp];
+    double v[kIlp];
+    int d = 0;
+#pragma unroll
+    for (int q = 0; q < kIlp; q++) {
+        const uint32_t tq = t + (!kTail || q < nq ? q : 0);
+        base[q] = nodes + __ldg(E.tree_off + tq);
+        idx[q] = 0;
+        d = max(d, __ldg(E.tree_depth + tq));
+    }
+    for (int s = 0; s <= d; s++) {
+#pragma unroll
+        for (int q = 0; q < kIlp; q++) {
+            const double2 raw = __ldg(reinterpret_cast<const double2 *>(base[q] + idx[q]));
+            const int f = __double2loint(raw.y), l = __double2hiint(raw.y);
+            v[q] = raw.x;
+            idx[q] = x[f * stride] <= raw.x ? l : l + 1;
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < kIlp; q++)
+        if (!kTail || q < nq) total = __dadd_rn(total, v[q]);  // tree order
+}
+
+// Groups of kIlp trees in lock-step.  A partial last group keeps the lock
+// step: its idle slots re-walk the group's first tree (loads in flight, no
+// latency chain of their own) and are not added -- tail trees walked one by
+// one would serialise max(depth) dependent loads each.
 template <int kIlp = GK_RF_ILP>
 __device__ __forceinline__ double walk_ensemble(const gk_ensemble &E, const double *x,
                                                 int stride) {
-    const gk_node *__restrict__ nodes = E.nodes;
     double total = E.base_score;
     uint32_t t = 0;
-    for (; t + kIlp <= E.n_trees; t += kIlp) {
-        const gk_node *base[kIlp];
-        int32_t idx[kIlp];
-        double v[kIlp];
-        int d = 0;
-#pragma unroll
-        for (int q = 0; q < kIlp; q++) {
-            base[q] = nodes + __ldg(E.tree_off + t + q);
-            idx[q] = 0;
-            d = max(d, __ldg(E.tree_depth + t + q));
-        }
-        for (int s = 0; s <= d; s++) {
-#pragma unroll
-            for (int q = 0; q < kIlp; q++) {
-                const double2 raw = __ldg(reinterpret_cast<const double2 *>(base[q] + idx[q]));
-                const int f = __double2loint(raw.y), l = __double2hiint(raw.y);
-                v[q] = raw.x;
-                idx[q] = x[f * stride] <= raw.x ? l : l + 1;
-            }
-        }
-#pragma unroll
-        for (int q = 0; q < kIlp; q++) total = __dadd_rn(total, v[q]);  // tree order
-    }
-    for (; t < E.n_trees; t++) {
-        const gk_node *b = nodes + E.tree_off[t];
-        int32_t i = 0;
-        while (true) {
-            const double2 raw = __ldg(reinterpret_cast<const double2 *>(b + i));
-            const int f = __double2loint(raw.y), l = __double2hiint(raw.y);
-            if (f < 0) {
-                total = __dadd_rn(total, raw.x);
-                break;
-            }
-            i = x[f * stride] <= raw.x ? l : l + 1;
-        }
-    }
+    for (; t + kIlp <= E.n_trees; t += kIlp) walk16_group<kIlp, false>(E, t, kIlp, x, stride, total);
+    if (t < E.n_trees) walk16_group<kIlp, true>(E, t, (int)(E.n_trees - t), x, stride, total);
     return total;
 }
 
@@ -68,18 +66,20 @@ __device__ __forceinline__ double walk_ensemble(const gk_ensemble &E, const doub
 // one 8-byte node load, one 4-byte shared load, two f32 compares -- 12 bytes
 // through the L1 data pipe instead of 24.  Loads of the kIlp trees are issued
 // together; the rare tie test runs out of line.
-template <int kIlp, class X64>
-__device__ __forceinline__ void walk8_group(const gk_ensemble &E, uint32_t t, const float *xf,
-                                            int stride, const X64 &x64, double &total) {
+template <int kIlp, bool kTail, class X64>
+__device__ __forceinline__ void walk8_group(const gk_ensemble &E, uint32_t t, int nq,
+                                            const float *xf, int stride, const X64 &x64,
+                                            double &total) {
     const uint2 *__restrict__ n8 = reinterpret_cast<const uint2 *>(E.nodes8);
     const uint2 *base[kIlp];
     int32_t idx[kIlp];
     int d = 0;
 #pragma unroll
-    for (int q = 0; q < kIlp; q++) {
-        base[q] = n8 + __ldg(E.tree_off + t + q);
+    for (int q = 0; q < kIlp; q++) {  // idle slots (partial group) re-walk tree t
+        const uint32_t tq = t + (!kTail || q < nq ? q : 0);
+        base[q] = n8 + __ldg(E.tree_off + tq);
         idx[q] = 0;
-        d = max(d, __ldg(E.tree_depth + t + q));
+        d = max(d, __ldg(E.tree_depth + tq));
     }
     for (int s = 0; s < d; s++) {
         uint2 raw[kIlp];
@@ -110,7 +110,8 @@ __device__ __forceinline__ void walk8_group(const gk_ensemble &E, uint32_t t, co
         }
     }
 #pragma unroll
-    for (int q = 0; q < kIlp; q++) total = __dadd_rn(total, __ldg(&E.nodes[(base[q] - n8) + idx[q]].v));
+    for (int q = 0; q < kIlp; q++)
+        if (!kTail || q < nq) total = __dadd_rn(total, __ldg(&E.nodes[(base[q] - n8) + idx[q]].v));
 }
 
 template <int kIlp, class X64>
@@ -118,8 +119,9 @@ __device__ __forceinline__ double walk_ensemble8(const gk_ensemble &E, const flo
                                                  const X64 &x64) {
     double total = E.base_score;
     uint32_t t = 0;
-    for (; t + kIlp <= E.n_trees; t += kIlp) walk8_group<kIlp>(E, t, xf, stride, x64, total);
-    for (; t < E.n_trees; t++) walk8_group<1>(E, t, xf, stride, x64, total);
+    for (; t + kIlp <= E.n_trees; t += kIlp) walk8_group<kIlp, false>(E, t, kIlp, xf, stride, x64, total);
+    if (t < E.n_trees)
+        walk8_group<kIlp, true>(E, t, (int)(E.n_trees - t), xf, stride, x64, total);
     return total;
 }
 
@@ -136,15 +138,17 @@ __device__ __forceinline__ void ld_block2(const gk_block2 *p, uint32_t (&w)[8]) 
                  : "l"(p));
 }
 
-template <int kIlp, class X64>
-__device__ __forceinline__ void walk_b2_group(const gk_ensemble &E, uint32_t t, const float *xf,
-                                              int stride, const X64 &x64, double &total) {
+template <int kIlp, bool kTail, class X64>
+__device__ __forceinline__ void walk_b2_group(const gk_ensemble &E, uint32_t t, int nq,
+                                              const float *xf, int stride, const X64 &x64,
+                                              double &total) {
     uint32_t ref[kIlp];
     int d = 0;
 #pragma unroll
-    for (int q = 0; q < kIlp; q++) {
-        ref[q] = __ldg(E.root + t + q);
-        d = max(d, __ldg(E.tree_depth + t + q));
+    for (int q = 0; q < kIlp; q++) {  // idle slots of a partial group start at a leaf
+        const bool on = !kTail || q < nq;
+        ref[q] = on ? __ldg(E.root + t + q) : GK_LEAF;
+        if (on) d = max(d, __ldg(E.tree_depth + t + q));
     }
     const int steps = (d + 1) >> 1;
     for (int s = 0; s < steps; s++) {
@@ -193,7 +197,8 @@ __device__ __forceinline__ void walk_b2_group(const gk_ensemble &E, uint32_t t, 
             if (!(ref[q] & GK_LEAF)) ref[q] = nref[q];
     }
 #pragma unroll
-    for (int q = 0; q < kIlp; q++) total = __dadd_rn(total, __ldg(E.leaf_val + (ref[q] & ~GK_LEAF)));
+    for (int q = 0; q < kIlp; q++)
+        if (!kTail || q < nq) total = __dadd_rn(total, __ldg(E.leaf_val + (ref[q] & ~GK_LEAF)));
 }
 
 template <int kIlp, class X64>
@@ -201,8 +206,9 @@ __device__ __forceinline__ double walk_ensemble_b2(const gk_ensemble &E, const f
                                                    const X64 &x64) {
     double total = E.base_score;
     uint32_t t = 0;
-    for (; t + kIlp <= E.n_trees; t += kIlp) walk_b2_group<kIlp>(E, t, xf, stride, x64, total);
-    for (; t < E.n_trees; t++) walk_b2_group<1>(E, t, xf, stride, x64, total);
+    for (; t + kIlp <= E.n_trees; t += kIlp) walk_b2_group<kIlp, false>(E, t, kIlp, xf, stride, x64, total);
+    if (t < E.n_trees)
+        walk_b2_group<kIlp, true>(E, t, (int)(E.n_trees - t), xf, stride, x64, total);
     return total;
 }
 
