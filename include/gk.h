@@ -248,7 +248,7 @@ int gk_rf_predict(const gk_ensemble *ens, const double *X, int64_t ld, int64_t n
  * pointers; all ensembles share the manifest sel_idx[n_sel], a device array).
  * Writes status / time_us / power_w / energy_uj per point.  `work` must hold
  * gk_sweep_workspace_bytes() bytes of device memory. */
-size_t gk_sweep_workspace_bytes(const gk_grid *grid, uint32_t n_sel);
+size_t gk_sweep_workspace_bytes(const gk_corpus *corpus, const gk_grid *grid, uint32_t n_sel);
 int gk_predict_energy_sweep(const gk_corpus *corpus, const gk_grid *grid,
                             const gk_ensemble *ens_host, const int32_t *sel_idx,
                             uint32_t n_sel, void *work, uint8_t *out_status,

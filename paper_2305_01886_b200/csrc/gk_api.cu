@@ -171,12 +171,17 @@ int gk_rf_predict(const gk_ensemble *ens, const double *X, int64_t ld, int64_t n
                         (cudaStream_t)stream);
 }
 
-size_t gk_sweep_workspace_bytes(const gk_grid *grid, uint32_t n_sel) {
+size_t gk_sweep_workspace_bytes(const gk_corpus *corpus, const gk_grid *grid, uint32_t n_sel) {
     const size_t n_points = (size_t)grid->n_k * grid->n_arch * grid->n_cfg;
     size_t b = 0;
     b += ((sizeof(gk_kstat) * grid->n_k + 255) / 256) * 256;
     b += ((sizeof(double) * 3 * grid->n_k * grid->n_arch + 255) / 256) * 256;
     b += ((sizeof(double) * n_points * n_sel + 255) / 256) * 256;
+    // the per-warp reservation-table slabs + work-queue counter: owned by the
+    // caller's workspace, so concurrent sweeps on different streams never share
+    const uint32_t max_n = corpus && corpus->max_n ? corpus->max_n : 1;
+    const uint32_t max_blk = corpus && corpus->max_blk ? corpus->max_blk : 1;
+    b += ((gk_sched_scratch_bytes(grid, max_n, max_blk) + 255) / 256) * 256;
     return b;
 }
 
@@ -207,8 +212,8 @@ int gk_predict_energy_sweep(const gk_corpus *corpus, const gk_grid *grid,
     stage_mark(1, st);
     const uint32_t max_n = corpus->max_n ? corpus->max_n : 1;
     const uint32_t max_blk = corpus->max_blk ? corpus->max_blk : 1;
-    void *ws = nullptr;
-    if (int rc = scratch(gk_sched_scratch_bytes(grid, max_n, max_blk), &ws)) return rc;
+    w += ((sizeof(double) * n_points * n_sel + 255) / 256) * 256;
+    void *ws = w;  // scratch slabs inside the caller's workspace (gk_sweep_workspace_bytes)
     if (sweep_fused()) {
         // one kernel: schedule + features + ensemble walk + energy per warp of points
         if (int rc = gk_launch_sweep_fused(corpus, grid, ks, latsum, ens_host, grid->n_arch,

@@ -46,7 +46,7 @@ def load_library(path: Path | None = None):
     L.gk_static_features.argtypes = [vp, vp, vp, vp, vp]
     L.gk_schedule_features.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, u32, vp, vp, vp]
     L.gk_rf_predict.argtypes = [vp, vp, i64, i64, vp, vp, vp, vp, vp]
-    L.gk_sweep_workspace_bytes.argtypes = [vp, u32]
+    L.gk_sweep_workspace_bytes.argtypes = [vp, vp, u32]
     L.gk_sweep_workspace_bytes.restype = C.c_size_t
     L.gk_predict_energy_sweep.argtypes = [vp, vp, vp, vp, u32, vp, vp, vp, vp, vp, vp]
     L.gk_set_stage_timing.argtypes = [C.c_int]
@@ -306,7 +306,7 @@ class Sweep:
         arr = (abi.GkEnsemble * len(ensembles))(*[e.desc for e in ensembles])
         self.ens_arr = arr
         L = load_library()
-        ws = L.gk_sweep_workspace_bytes(C.byref(dg.desc), self.n_sel)
+        ws = L.gk_sweep_workspace_bytes(C.byref(dc.desc), C.byref(dg.desc), self.n_sel)
         dev = device()
         self.work = t.empty(max(ws, 256), dtype=t.uint8, device=dev)
         n = dg.n_points
