@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define GK_ABI_VERSION 2
+#define GK_ABI_VERSION 3
 
 /* resource / class codes (reference ptx/types.py:12-24) */
 enum { GK_SP = 0, GK_SFU = 1, GK_DPU = 2, GK_LSU = 3, GK_WS = 4, GK_NRES = 5 };

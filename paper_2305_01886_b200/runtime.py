@@ -51,7 +51,7 @@ def load_library(path: Path | None = None):
     L.gk_predict_energy_sweep.argtypes = [vp, vp, vp, vp, u32, vp, vp, vp, vp, vp, vp]
     L.gk_set_stage_timing.argtypes = [C.c_int]
     L.gk_get_stage_ms.argtypes = [vp]
-    if L.gk_abi_version() != 2:
+    if L.gk_abi_version() != 3:
         raise DeviceError("libgk ABI version mismatch")
     if path is None:
         _lib = L
