@@ -404,8 +404,80 @@ __global__ void __launch_bounds__(256) k5_eval_big(RfTrainData D, const int32_t 
     reduce_best(H, mine, out + task_ids[bi]);
 }
 
-// small tasks (<= 64 rows): one warp; per feature, each lane's keys are
-// evaluated against all rows (prefix sums by broadcast)
+// Tiny nodes (<= kTiny rows): lane = feature.  Each lane loads its feature's
+// bin for every row (a row's bins are one coalesced 32-byte read per warp) and
+// evaluates every row's bin as a boundary against all rows -- O(m^2) per
+// feature but m <= 16, instead of filling and scanning 256-bin histograms one
+// feature at a time.  Candidates, integer sums and proxies are the same as the
+// histogram path's (boundary b = a bin present in the node; left = bins <= b),
+// so the chosen split is identical.
+constexpr int kTiny = 16;
+
+__device__ __forceinline__ void split_tiny(const RfTrainData &D, const RfTask &T,
+                                           const int32_t *__restrict__ rows, int m, int lane,
+                                           int wib, uint32_t wv, int64_t sv, int32_t rv,
+                                           RfSplit *out) {
+    __shared__ uint32_t tw[4][kTiny];
+    __shared__ int64_t ts[4][kTiny];
+    if (lane < m) {
+        tw[wib][lane] = wv;
+        ts[wib][lane] = sv;
+    }
+    uint32_t W = lane < m ? wv : 0u;
+    int64_t S = lane < m ? sv : 0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        W += __shfl_xor_sync(GK_FULL, W, o);
+        S += __shfl_xor_sync(GK_FULL, S, o);
+    }
+    __syncwarp();
+    const double parent = (double)S * (double)S / (double)W;
+    BestSplit best{-1.0, 0x7fffffff, 0x7fffffff, 0};
+    for (int f0 = 0; f0 < D.F; f0 += 32) {
+        const int f = f0 + lane;
+        const bool fv = f < D.F;
+        uint32_t bin[kTiny];
+#pragma unroll
+        for (int j = 0; j < kTiny; j++) {
+            const int32_t rj = __shfl_sync(GK_FULL, rv, j);
+            bin[j] = (j < m && fv) ? D.Xb[(size_t)rj * D.F + f] : 0xFFFFu;
+        }
+        if (fv) {
+#pragma unroll
+            for (int j = 0; j < kTiny; j++) {
+                if (j >= m) break;
+                const uint32_t b = bin[j];
+                uint32_t CL = 0, WL = 0;
+                int64_t SL = 0;
+#pragma unroll
+                for (int i = 0; i < kTiny; i++) {
+                    if (i < m && bin[i] <= b) {
+                        CL++;
+                        WL += tw[wib][i];
+                        SL += ts[wib][i];
+                    }
+                }
+                if (CL == (uint32_t)m || b >= (uint32_t)(kBins - 1)) continue;
+                const double SLd = (double)SL, SRd = (double)(S - SL);
+                const double p = SLd * SLd / (double)WL + SRd * SRd / (double)(W - WL);
+                if (better(p, f, (int)b, best)) best = BestSplit{p, f, (int)b, CL};
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        BestSplit q;
+        q.proxy = __shfl_xor_sync(GK_FULL, best.proxy, o);
+        q.feat = __shfl_xor_sync(GK_FULL, best.feat, o);
+        q.bin = __shfl_xor_sync(GK_FULL, best.bin, o);
+        q.n_left = __shfl_xor_sync(GK_FULL, best.n_left, o);
+        if (better(q.proxy, q.feat, q.bin, best)) best = q;
+    }
+    if (lane == 0) finish_split(best, parent, out);
+}
+
+// small tasks (<= 64 rows): one warp; tiny ones (<= kTiny rows) lane-per-
+// feature (split_tiny), the rest through per-warp 256-bin histograms
 __global__ void __launch_bounds__(128) k5_split_small(RfTrainData D, const RfTask *__restrict__ tasks,
                                                      const int32_t *__restrict__ task_ids,
                                                      int n_ids, const int32_t *__restrict__ rows0,
@@ -419,6 +491,13 @@ __global__ void __launch_bounds__(128) k5_split_small(RfTrainData D, const RfTas
     const int32_t *rows = T.parity ? rows1 : rows0;
     const int m = T.end - T.begin;
     const uint32_t *cnt = D.counts + (size_t)T.tree * D.n;
+    if (m <= kTiny) {  // warp-uniform branch
+        const int32_t rv = lane < m ? rows[T.begin + lane] : 0;
+        const uint32_t wv = lane < m ? cnt[rv] : 0u;
+        const int64_t sv = lane < m ? (int64_t)wv * D.yfp[rv] : 0;
+        split_tiny(D, T, rows, m, lane, threadIdx.x >> 5, wv, sv, rv, out + ti);
+        return;
+    }
     int32_t r[2];
     uint32_t w[2];
     int64_t s[2];
