@@ -341,7 +341,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2", choices=["c2", "c4", "c5s"])
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c4", "c5s"])
     ap.add_argument("--kernels", type=int, default=0)
     ap.add_argument("--rows", type=int, default=0, help="c4: total rows (default 100M)")
     ap.add_argument("--trees", type=int, default=500)
@@ -396,6 +396,12 @@ def main():
 
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    if args.workload == "c1":
+        if rank == 0:
+            run_c1(args, threads)
+        if world > 1:
+            dist.destroy_process_group()
+        return
     if args.workload == "c4":
         run_c4(args, rank, world, local_rank, threads)
         if world > 1:
@@ -558,6 +564,129 @@ def run_c4(args, rank, world, local_rank, threads):
         cs = time.perf_counter() - t0
         line["cpu_baseline"] = {"value": ns / cs, "unit": "rows/s", "cores": threads,
                                 "kind": "port", "sample": f"{ns} rows, oracle walk"}
+    print(json.dumps(line))
+
+
+def run_c1(args, threads):
+    """BASELINE configs[0], the reference's own CPU-runnable case, end to end
+    through this package's public API: 100 synthetic PTX kernels x the 4
+    config #1 launches on tesla_k20 -> parse + pack (native front-end) ->
+    cycles + features (K1/K3) -> power labels from the trainer tests'
+    generative form (seed 2026) -> train(..., "random_forest", 500 trees,
+    seed 0: 5-fold CV + final fit, GPU forest) -> export (native writer) + load
+    (native loader) -> energy for every point (fused sweep).  Metric: seconds
+    (lower is better).  CPU leg (same run, this host): the same pipeline
+    through the oracle port (C, all threads), scikit-learn's forest and the
+    Python JSON path."""
+    import tempfile
+
+    import torch
+
+    from paper_2305_01886_b200 import corpus as CG
+    from paper_2305_01886_b200 import pack
+    from paper_2305_01886_b200 import runtime as rt
+    from paper_2305_01886_b200.ensemble import flatten, load_ensemble
+    from paper_2305_01886_b200.profiles import resolve_profile
+    from paper_2305_01886_b200.ptx_native import pack_ptx
+    from paper_2305_01886_b200.trainer import ensemble_document_text, train
+
+    items = CG.synth_corpus(100, 0)
+    prof = [resolve_profile("tesla_k20")]
+    sel = pack.manifest_indices(pack.SELECTED_FEATURES)
+    names = pack.SELECTED_FEATURES
+
+    def labels(feat):
+        rng = np.random.default_rng(2026)
+        F = pack.FEATURE_ORDER
+        occ, iic, ld = (feat[:, F.index(n)] for n in ("occupancy", "inst_issue_cycles",
+                                                      "glob_load_sm"))
+        return 30.0 + 40.0 * occ + 0.003 * iic + 12.0 * (ld > 50) + rng.normal(0, 1, len(feat))
+
+    def gpu_once():
+        t = {}
+        t0 = time.perf_counter()
+        c = pack_ptx(items)
+        t["parse"] = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        dc = rt.DeviceCorpus.upload(c)
+        dg = rt.DeviceGrid.build(dc, prof, CG.CONFIG1)
+        out = {k: v.cpu().numpy() for k, v in rt.schedule_features(dc, dg, sel_idx=sel).items()}
+        t["schedule_features"] = time.perf_counter() - t0
+        ok = out["status"] == 0
+        X, y = out["feat"][ok][:, sel], labels(out["feat"][ok])
+        t0 = time.perf_counter()
+        res = train((X, y, names), "random_forest", n_estimators=500, seed=0)
+        torch.cuda.synchronize()
+        t["train_rf"] = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        with tempfile.TemporaryDirectory() as d:
+            path = Path(d) / "ensemble.json"
+            path.write_text(ensemble_document_text(res) + "\n")
+            ens = load_ensemble(path)
+        t["export_load"] = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        sw = rt.Sweep(dc, dg, [rt.DeviceEnsemble.upload(flatten(ens))], sel)
+        st, tu, pw, en = (x.cpu().numpy() for x in sw.run())
+        t["predict_energy"] = time.perf_counter() - t0
+        return t, int(ok.sum()), res.mean_metrics.r2
+
+    gpu_once()  # warm-up (library load, first-touch allocations)
+    torch.cuda.synchronize()
+    runs = [gpu_once() for _ in range(args.steps)]
+    tot = [sum(r[0].values()) for r in runs]
+    best = runs[int(np.argmin(tot))]
+    line = {"metric": "config #1 end-to-end pipeline seconds", "value": float(np.median(tot)),
+            "unit": "s", "n_gpus": 1, "steps": args.steps, "warmup": 1,
+            "ms_per_step": float(np.median(tot)) * 1e3, "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "BASELINE configs[0]: 100 synthetic PTX kernels x 4 launch "
+                                   "configs (tesla_k20): parse, cycles + features, "
+                                   "train RF (500 trees, 5-fold CV + final), export + load, "
+                                   "energy", "feasible_points": best[1],
+                       "cv_r2": best[2]},
+            "stages_s": best[0]}
+    if not args.no_cpu:
+        import oracle as O
+        from sklearn.ensemble import RandomForestRegressor as SkRF
+
+        from paper_2305_01886_b200 import ptx
+        from paper_2305_01886_b200 import trainer as T
+        from paper_2305_01886_b200.ensemble import _load_python
+        from paper_2305_01886_b200.ensemble import random_forest_flat  # noqa: F401
+
+        t = {}
+        t0 = time.perf_counter()
+        c = pack.pack_corpus(ptx.parse_ptx(tx, n, loop_counts=lp) for n, tx, lp in items)
+        t["parse"] = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        o = O.schedule_features(O.HostGrid(c, prof, CG.CONFIG1), sel_idx=sel, threads=threads)
+        t["schedule_features"] = time.perf_counter() - t0
+        ok = o["status"] == 0
+        X, y = o["feat"][ok][:, sel], labels(o["feat"][ok])
+        orig = T._make_model
+        T._make_model = lambda fam, n_est, lr, md, seed: SkRF(n_estimators=n_est, max_depth=md,
+                                                              random_state=seed)
+        try:
+            t0 = time.perf_counter()
+            res = T.train((X, y, names), "random_forest", n_estimators=500, seed=0)
+            t["train_rf"] = time.perf_counter() - t0
+        finally:
+            T._make_model = orig
+        t0 = time.perf_counter()
+        with tempfile.TemporaryDirectory() as d:
+            path = Path(d) / "ensemble.json"
+            path.write_text(json.dumps(T.ensemble_document(res), indent=2) + "\n")
+            flat = flatten(_load_python(path))
+        t["export_load"] = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        O.rf_predict(flat, o["feat"][ok][:, sel], time_us=o["sf"][ok, 7], threads=threads)
+        t["predict_energy"] = time.perf_counter() - t0
+        line["cpu_baseline"] = {"value": sum(t.values()), "unit": "s", "cores": threads,
+                                "kind": "port", "stages_s": t,
+                                "sample": "the whole workload: Python parser + oracle port (C, "
+                                          "all threads) + scikit-learn RandomForestRegressor "
+                                          "(the reference trainer's model, n_jobs=None) + "
+                                          "Python JSON export / load"}
     print(json.dumps(line))
 
 

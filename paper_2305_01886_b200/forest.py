@@ -341,7 +341,7 @@ class RandomForestRegressor(_LevelGrower):
     """GPU-trained random forest with scikit-learn's constructor/fit/predict."""
 
     def __init__(self, n_estimators: int = 100, *, max_depth: int | None = None,
-                 random_state=None, n_bins: int = N_BINS, trees_per_batch: int = 32,
+                 random_state=None, n_bins: int = N_BINS, trees_per_batch: int | None = None,
                  shard: tuple[int, int] | None = None, concurrent: bool = True):
         self.n_estimators = n_estimators
         self.max_depth = max_depth
@@ -386,8 +386,10 @@ class RandomForestRegressor(_LevelGrower):
             rank, world = self.shard
             todo = [t for t in todo if t % world == rank]
         self.estimators_ = [None] * self.n_estimators
-        batches = [todo[b0: b0 + self.trees_per_batch]
-                   for b0 in range(0, len(todo), self.trees_per_batch)]
+        # trees grown level-wise together: 32 at 1M rows, more for small tables
+        # (each level costs a few host round trips whatever the batch holds)
+        tpb = self.trees_per_batch or max(32, min(len(todo), int(32_000_000 // max(n, 1))))
+        batches = [todo[b0: b0 + tpb] for b0 in range(0, len(todo), tpb)]
         # two batches in flight on their own streams: one batch's host-side level
         # bookkeeping (numpy, GIL released) overlaps the other's kernels
         streams = [torch.cuda.Stream(device=dev) for _ in range(min(2, len(batches)))]
