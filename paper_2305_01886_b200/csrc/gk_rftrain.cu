@@ -26,6 +26,11 @@ namespace gk {
 constexpr int kFC = 16;          // features per histogram chunk
 constexpr int kBins = 256;
 constexpr int kMedRows = 32768;  // larger nodes use the multi-CTA histogram path
+#ifndef GK_BIG_ROWS
+#define GK_BIG_ROWS 2048  // rows per CTA of the multi-CTA histograms (GBT 1M x 64: 7.7 -> 5.4 ms/stage vs 32768)
+#endif
+constexpr int kBigRows = GK_BIG_ROWS;
+static_assert(kMedRows % kBigRows == 0, "chunking");
 constexpr int kSmallRows = 64;
 
 struct RfTrainData {
@@ -360,9 +365,9 @@ __global__ void __launch_bounds__(256) k5_hist_big(RfTrainData D, const RfTask *
     const RfTask T = tasks[task_ids[bi]];
     const int32_t *rows = T.parity ? rows1 : rows0;
     const int fc = blockIdx.y;
-    const int p0 = T.begin + blockIdx.x * kMedRows;
+    const int p0 = T.begin + blockIdx.x * kBigRows;
     if (p0 >= T.end) return;
-    const int p1 = min(T.end, p0 + kMedRows);
+    const int p1 = min(T.end, p0 + kBigRows);
     zero_hist(H);
     __syncthreads();
     accumulate(H, D, T, rows, p0, p1, fc);
@@ -745,7 +750,9 @@ int gk_rf_split_level(const uint8_t *Xb, const int64_t *yfp, const double *y,
         uint64_t *gcw = (uint64_t *)hist_ws;
         int64_t *gs = (int64_t *)(gcw + (size_t)n_big * n_feat * gk::kBins);
         cudaMemsetAsync(hist_ws, 0, 2 * sizeof(uint64_t) * (size_t)n_big * n_feat * gk::kBins, st);
-        dim3 grid(big_max_chunks, (n_feat + gk::kFC - 1) / gk::kFC, n_big);
+        // the host sizes big_max_chunks in kMedRows units; CTAs take kBigRows
+        dim3 grid(big_max_chunks * (gk::kMedRows / gk::kBigRows), (n_feat + gk::kFC - 1) / gk::kFC,
+                  n_big);
         gk::k5_hist_big<<<grid, 256, smem, st>>>(D, T, big_ids, rows0, rows1, gcw, gs);
         gk::k5_eval_big<<<n_big, 256, smem, st>>>(D, big_ids, gcw, gs, out);
     }
