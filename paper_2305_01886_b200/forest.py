@@ -342,14 +342,16 @@ class RandomForestRegressor(_LevelGrower):
 
     def __init__(self, n_estimators: int = 100, *, max_depth: int | None = None,
                  random_state=None, n_bins: int = N_BINS, trees_per_batch: int | None = None,
-                 shard: tuple[int, int] | None = None, concurrent: bool = True):
+                 shard: tuple[int, int] | None = None, concurrent: bool = True,
+                 streams: int = 4):
         self.n_estimators = n_estimators
         self.max_depth = max_depth
         self.random_state = random_state
         self.n_bins = n_bins
         self.trees_per_batch = trees_per_batch
         self.shard = shard  # (rank, world): build trees t with t % world == rank
-        self.concurrent = concurrent  # overlap two tree batches (host work vs kernels)
+        self.concurrent = concurrent  # overlap tree batches (host work vs kernels)
+        self.streams = streams        # batches in flight
         self.estimators_: list = []
 
     # ------------------------------------------------------------------ fit
@@ -386,13 +388,17 @@ class RandomForestRegressor(_LevelGrower):
             rank, world = self.shard
             todo = [t for t in todo if t % world == rank]
         self.estimators_ = [None] * self.n_estimators
-        # trees grown level-wise together: 32 at 1M rows, more for small tables
-        # (each level costs a few host round trips whatever the batch holds)
-        tpb = self.trees_per_batch or max(32, min(len(todo), int(32_000_000 // max(n, 1))))
+        # trees grown level-wise together: <= 32 at 1M rows, more for small tables
+        # (each level costs a few host round trips whatever the batch holds), and
+        # at least `streams` batches when there are enough trees (measured on
+        # B200 at 1M x 64: 4 batches in flight 18.7 ms/tree, 2: 24 ms/tree)
+        tpb = self.trees_per_batch or max(16, min(int(32_000_000 // max(n, 1)),
+                                                  -(-len(todo) // max(self.streams, 1))))
         batches = [todo[b0: b0 + tpb] for b0 in range(0, len(todo), tpb)]
         # two batches in flight on their own streams: one batch's host-side level
         # bookkeeping (numpy, GIL released) overlaps the other's kernels
-        streams = [torch.cuda.Stream(device=dev) for _ in range(min(2, len(batches)))]
+        streams = [torch.cuda.Stream(device=dev)
+                   for _ in range(max(1, min(self.streams, len(batches))))]
         main = torch.cuda.current_stream(dev)
 
         def grow(k):

@@ -32,6 +32,7 @@ def main():
     ap.add_argument("--depth", type=int, default=16)
     ap.add_argument("--batch", type=int, default=32)
     ap.add_argument("--profile", action="store_true")
+    ap.add_argument("--streams", type=int, default=2)
     a = ap.parse_args()
     import torch
 
@@ -49,7 +50,7 @@ def main():
         prof.enable()
     t0 = time.perf_counter()
     m = RandomForestRegressor(a.trees, max_depth=a.depth, random_state=0,
-                              trees_per_batch=a.batch).fit(Xs, y)
+                              trees_per_batch=a.batch, streams=a.streams).fit(Xs, y)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     if prof is not None:
