@@ -128,3 +128,27 @@ def test_train_r2_mape_parity_with_reference(key):
     mape = float(np.mean(res.fold_mape_pct))
     assert abs(r2 - ref["mean"]["r2"]) <= 0.005, (r2, ref["mean"]["r2"])
     assert abs(mape - ref["mean_mape_pct"]) <= 0.5, (mape, ref["mean_mape_pct"])
+
+
+@pytest.mark.gpu
+def test_unbounded_depth_forest_matches_sklearn_quality():
+    """max_depth=None (the reference trainer's default, training.py:100): trees
+    grow until no split improves (> depth 16 here); held-out R^2 within 0.01
+    of scikit-learn's forest on the same split."""
+    from sklearn.ensemble import RandomForestRegressor as SkRF
+
+    from paper_2305_01886_b200.forest import RandomForestRegressor
+
+    fr = power_frame(20_000, 17)
+    feats = [c for c in fr.columns if c not in ("kernel", "power_w")]
+    X, y = fr[feats].to_numpy(), fr["power_w"].to_numpy()
+    tr, te = slice(0, 16_000), slice(16_000, None)
+    ours = RandomForestRegressor(24, max_depth=None, random_state=0).fit(X[tr], y[tr])
+    sk = SkRF(24, max_depth=None, random_state=0).fit(X[tr], y[tr])
+    depth = max(e.tree_.max_depth for e in ours.estimators_)
+    assert depth > 16
+
+    def r2(p):
+        return 1 - np.mean((p - y[te]) ** 2) / np.var(y[te])
+
+    assert abs(r2(ours.predict(X[te])) - r2(sk.predict(X[te]))) < 0.01
