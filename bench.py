@@ -349,6 +349,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline (profiling)")
     ap.add_argument("--no-rf", action="store_true", help="skip the config #3 forest fit")
+    ap.add_argument("--no-e2e", action="store_true", help="c4: skip the host-row e2e leg")
     ap.add_argument("--rf-rows", type=int, default=1_000_000)
     ap.add_argument("--rf-trees", type=int, default=64)
     ap.add_argument("--gbt-stages", type=int, default=100)
@@ -554,6 +555,29 @@ def run_c4(args, rank, world, local_rank, threads):
                          "frac": achieved / peak, "algorithmic_bytes": alg, "traffic": traffic,
                          "traffic_source": traffic_src},
             "clocks": clk.summary()}
+    # e2e: the same rows from pinned HOST memory, streamed in chunks through
+    # runtime.HostRowsPredictor (H2D / K4 / D2H on three streams), power back
+    # to pinned host memory -- all inside the timing
+    if not args.no_e2e:
+        Xh = torch.empty((n, F), dtype=torch.float64).pin_memory()
+        Xh.copy_(X)
+        ph = torch.empty(n, dtype=torch.float64).pin_memory()
+        hp = rt.HostRowsPredictor(de, F)
+        hp.run(Xh, ph)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(args.steps):
+            hp.run(Xh, ph)
+        b.record()
+        torch.cuda.synchronize()
+        e2e_ms = a.elapsed_time(b)
+        assert torch.equal(ph[:100000].to(power.device), power[:100000])
+        line["e2e"] = {"value": rows_total * args.steps / (e2e_ms / 1e3), "unit": "rows/s",
+                       "h2d_bytes_per_step": n * F * 8, "d2h_bytes_per_step": n * 8,
+                       "path": "runtime.HostRowsPredictor: pinned host rows -> 8M-row chunks "
+                               "(H2D / K4 / D2H on 3 streams) -> pinned host power"}
+        del Xh, ph, hp
     if not args.no_cpu:
         import oracle as O
 

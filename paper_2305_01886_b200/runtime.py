@@ -470,3 +470,53 @@ class HostSweep:
         out = self.submit(stream)
         self.finish(stream)
         return out
+
+
+class HostRowsPredictor:
+    """Batched power (+ energy) for a HOST row table (the reference-facing
+    `predict_power` over many rows), streamed through the device in chunks:
+    chunk k + 1's H2D copy and chunk k - 1's D2H copy run on their own
+    streams while K4 walks chunk k (two device slots).  X_host / out_host
+    should be pinned (torch `pin_memory()`) for the copies to be asynchronous."""
+
+    def __init__(self, ensemble: "DeviceEnsemble", n_cols: int, chunk_rows: int = 8 << 20):
+        t = _torch()
+        dev = device()
+        self.de, self.n_cols, self.chunk = ensemble, int(n_cols), int(chunk_rows)
+        self.x = [t.empty((self.chunk, self.n_cols), dtype=t.float64, device=dev) for _ in range(2)]
+        self.p = [t.empty(self.chunk, dtype=t.float64, device=dev) for _ in range(2)]
+        self.s_h2d = t.cuda.Stream(device=dev)
+        self.s_d2h = t.cuda.Stream(device=dev)
+        self.ev_free = [t.cuda.Event() for _ in range(2)]   # slot's D2H done
+        self.used = [False, False]
+
+    def run(self, X_host, out_host, stream=None):
+        """Enqueue power for every row of X_host [n, n_cols] into out_host [n];
+        returns after enqueueing (synchronise before reading out_host)."""
+        t = _torch()
+        cs = stream or t.cuda.current_stream()
+        n = X_host.shape[0]
+        L = load_library()
+        self.s_h2d.wait_stream(cs)
+        self.s_d2h.wait_stream(cs)
+        for k, r0 in enumerate(range(0, n, self.chunk)):
+            r1 = min(n, r0 + self.chunk)
+            slot = k % 2
+            with t.cuda.stream(self.s_h2d):
+                if self.used[slot]:
+                    self.s_h2d.wait_event(self.ev_free[slot])
+                self.x[slot][: r1 - r0].copy_(X_host[r0:r1], non_blocking=True)
+                ev_in = t.cuda.Event()
+                ev_in.record(self.s_h2d)
+            cs.wait_event(ev_in)
+            _check(L.gk_rf_predict(C.byref(self.de.desc), _ptr(self.x[slot]), self.n_cols, r1 - r0,
+                                   None, None, _ptr(self.p[slot]), None, cs.cuda_stream))
+            ev_done = t.cuda.Event()
+            ev_done.record(cs)
+            with t.cuda.stream(self.s_d2h):
+                self.s_d2h.wait_event(ev_done)
+                out_host[r0:r1].copy_(self.p[slot][: r1 - r0], non_blocking=True)
+                self.ev_free[slot].record(self.s_d2h)
+            self.used[slot] = True
+        cs.wait_stream(self.s_d2h)
+        return out_host

@@ -54,3 +54,24 @@ def test_host_sweep_matches_device_sweep(chunks, depth):
     out = hs.run()
     torch.cuda.synchronize()
     assert np.array_equal(out["energy_uj"].numpy().view(np.uint64), want[3].view(np.uint64))
+
+
+@pytest.mark.gpu
+def test_host_rows_predictor_matches_device_walk():
+    import torch
+
+    from paper_2305_01886_b200 import runtime as rt
+
+    rng = np.random.default_rng(4)
+    n, F = 10_007, 12
+    X = rng.random((n, F))
+    flat = random_forest_flat(23, 7, [f"f{i}" for i in range(F)], np.zeros(F), np.ones(F), seed=2)
+    de = rt.DeviceEnsemble.upload(flat)
+    want, _ = rt.rf_predict(de, torch.tensor(X, device="cuda"))
+    Xh = torch.from_numpy(X).pin_memory()
+    out = torch.empty(n, dtype=torch.float64).pin_memory()
+    hp = rt.HostRowsPredictor(de, F, chunk_rows=3000)   # 4 chunks over 2 device slots
+    for _ in range(2):
+        hp.run(Xh, out)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.numpy().view(np.uint64), want.cpu().numpy().view(np.uint64))
