@@ -328,6 +328,11 @@ size_t gk_corr_pearson_workspace(int64_t n, int32_t K);
 int gk_corr_pearson(const double *X, int64_t n, int32_t K, int64_t ld, double *mean,
                     double *comoment, void *ws, size_t ws_bytes, void *stream);
 
+/* mem_throughput clamps to tp_floor (profiles.py:173-181: the reference logs a
+ * warning per clamped call) counted on the device since the last reset;
+ * synchronous.  reset != 0 zeroes the counter after reading. */
+int gk_throughput_clamps(uint64_t *out, int reset);
+
 int gk_set_stage_timing(int on);
 int gk_get_stage_ms(float *out3);
 

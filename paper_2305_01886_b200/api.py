@@ -18,6 +18,7 @@ energy is the fp64 product on the device (<= 1 ulp apart).
 
 from __future__ import annotations
 
+import logging
 from collections.abc import Mapping
 from dataclasses import dataclass, fields
 from decimal import Decimal
@@ -30,6 +31,8 @@ from .errors import EnsembleError, ScheduleError
 from .ir import InstClass, Resource
 from .pack import FEATURE_ORDER, SELECTED_FEATURES, CorpusBuilder, pack_corpus
 from .profiles import ArchProfile, us_from_cycles
+
+log = logging.getLogger(__name__.rsplit(".", 1)[0] + ".profiles")  # where the reference warns
 
 # ------------------------------------------------------------------ types
 
@@ -217,9 +220,21 @@ def schedule_batch(profiles, graphs, launches, *, features: bool = True, sel_idx
     dc = _device_corpus(graphs)
     dg = DeviceGrid.build(dc, profiles, [_launch_tuple(L) for L in launches])
     out = schedule_features(dc, dg, feat=features, sel_idx=sel_idx, trace=trace)
+    _log_clamps()
     if not to_host:
         return out
     return {k: (v.cpu().numpy() if hasattr(v, "cpu") else v) for k, v in out.items()}
+
+
+def _log_clamps() -> None:
+    """The reference warns on every clamped mem_throughput call
+    (profiles.py:173-181); the device counts them, logged once per batch."""
+    from .runtime import throughput_clamps
+
+    n = throughput_clamps(reset=True)
+    if n:
+        log.warning("throughput model gave a non-positive value %d times in this batch; "
+                    "clamped to tp_floor", n)
 
 
 def extract_features_batch(profiles, graphs, launches, *, selected=None) -> np.ndarray:

@@ -22,7 +22,8 @@ from .pack import KSTAT_DT, Corpus, arch_records, config_array, latency_table
 LIB_PATH = Path(__file__).resolve().parent / "libgk.so"
 EXPORTS = ("gk_abi_version", "gk_last_error", "gk_device_sm_count", "gk_static_features",
            "gk_schedule_features", "gk_rf_predict", "gk_sweep_workspace_bytes",
-           "gk_predict_energy_sweep", "gk_set_stage_timing", "gk_get_stage_ms")
+           "gk_predict_energy_sweep", "gk_set_stage_timing", "gk_get_stage_ms",
+           "gk_throughput_clamps")
 _lib = None
 
 
@@ -51,6 +52,7 @@ def load_library(path: Path | None = None):
     L.gk_predict_energy_sweep.argtypes = [vp, vp, vp, vp, u32, vp, vp, vp, vp, vp, vp]
     L.gk_set_stage_timing.argtypes = [C.c_int]
     L.gk_get_stage_ms.argtypes = [vp]
+    L.gk_throughput_clamps.argtypes = [vp, C.c_int]
     if L.gk_abi_version() != 3:
         raise DeviceError("libgk ABI version mismatch")
     if path is None:
@@ -276,6 +278,15 @@ def schedule_features(dc: DeviceCorpus, dg: DeviceGrid, *, si=True, sf=True, fea
         C.byref(tr) if tr is not None else None, _stream(stream)))
     out["kstat"], out["latsum"] = ks, ls
     return out
+
+
+def throughput_clamps(reset: bool = True) -> int:
+    """How often the throughput model was clamped to tp_floor on the device
+    since the last reset (the reference logs a warning per clamped call,
+    profiles.py:173-181).  Synchronises."""
+    v = C.c_uint64()
+    _check(load_library().gk_throughput_clamps(C.byref(v), int(reset)))
+    return int(v.value)
 
 
 def rf_predict(de: DeviceEnsemble, X, *, status=None, time_us=None, stream=None):

@@ -212,3 +212,27 @@ def test_fused_sweep_matches_oracle_pipeline():
         pw, en = O.rf_predict(flats[a], d["feat"][m][:, sel], time_us=d["sf"][m, 7])
         assert bits_equal(power[m], pw)
         assert bits_equal(energy[m], en)
+
+
+def test_throughput_clamps_counted_and_logged(caplog):
+    """A throughput model that goes non-positive is clamped to tp_floor
+    (profiles.py:173-181, the reference warns per call): the device counts the
+    clamps, the batched face logs them once, results equal the oracle's."""
+    import logging
+
+    from paper_2305_01886_b200 import api
+    from paper_2305_01886_b200.profiles import profile_from_dict, profile_to_dict
+
+    doc = profile_to_dict(resolve_profile("k20"))
+    doc["throughput_models"]["global"]["b"] = 0.5   # a (b - exp(-c n)) < 0 for small n
+    prof = profile_from_dict(doc)
+    gs = graphs(6, 41)
+    cfgs = [(1, 32, 0, 0), (4, 64, 0, 0), (64, 256, 0, 0)]
+    with caplog.at_level(logging.WARNING):
+        got = api.schedule_batch([prof], gs, cfgs)
+    msgs = [r.getMessage() for r in caplog.records if "clamped to tp_floor" in r.getMessage()]
+    assert len(msgs) == 1 and int(msgs[0].split(" times")[0].rsplit(" ", 1)[1]) > 0
+    want = O.schedule_features(O.HostGrid(pack.pack_corpus(gs), [prof], cfgs))
+    assert np.array_equal(got["status"], want["status"])
+    ok = want["status"] == 0
+    assert bits_equal(got["sf"][ok], want["sf"][ok]) and bits_equal(got["feat"][ok], want["feat"][ok])
