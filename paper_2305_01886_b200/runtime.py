@@ -441,7 +441,10 @@ class HostSweep:
         first = self.n_submitted < self.depth
         self.n_submitted += 1
         # the slot's previous step must have finished its D2H (which follows its compute)
-        self.s_h2d.wait_stream(cs) if first else self.s_h2d.wait_event(self.ev_free[k])
+        if first:
+            self.s_h2d.wait_stream(cs)
+        else:
+            self.s_h2d.wait_event(self.ev_free[k])
         ev_in = []
         with t.cuda.stream(self.s_h2d):
             for c in self.chunks:
