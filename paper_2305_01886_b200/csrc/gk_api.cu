@@ -51,38 +51,12 @@ namespace {
 
 // optional per-stage timing of the fused sweep (profiling aid; synchronises)
 bool g_stage_timing = false;
-float g_stage_ms[3] = {0.f, 0.f, 0.f};
 cudaEvent_t g_ev[4] = {nullptr, nullptr, nullptr, nullptr};
 
 void stage_mark(int i, cudaStream_t st) {
     if (!g_stage_timing) return;
     if (!g_ev[i]) cudaEventCreate(&g_ev[i]);
     cudaEventRecord(g_ev[i], st);
-}
-
-struct Scratch {
-    void *p = nullptr;
-    size_t n = 0;
-    ~Scratch() {
-        if (p) cudaFree(p);
-    }
-};
-thread_local Scratch g_scratch;
-
-int scratch(size_t bytes, void **out) {
-    if (g_scratch.n < bytes) {
-        if (g_scratch.p) cudaFree(g_scratch.p);
-        g_scratch.p = nullptr;
-        g_scratch.n = 0;
-        const cudaError_t e = cudaMalloc(&g_scratch.p, bytes);
-        if (e != cudaSuccess) {
-            gk_set_error("scratch allocation of %zu B: %s", bytes, cudaGetErrorString(e));
-            return -2;
-        }
-        g_scratch.n = bytes;
-    }
-    *out = g_scratch.p;
-    return 0;
 }
 
 int check_grid(const gk_corpus *C, const gk_grid *G) {
@@ -149,11 +123,19 @@ int gk_schedule_features(const gk_corpus *corpus, const gk_grid *grid, const gk_
     const cudaStream_t st = (cudaStream_t)stream;
     const uint32_t max_n = corpus->max_n ? corpus->max_n : 1;
     const uint32_t max_blk = corpus->max_blk ? corpus->max_blk : 1;
+    // stream-ordered scratch (pooled by the driver): reentrant per stream
     void *ws = nullptr;
-    if (int rc = scratch(gk_sched_scratch_bytes(grid, max_n, max_blk), &ws)) return rc;
-    return gk_launch_sched(corpus, grid, kstat, latsum, out_status, out_si, out_sf, out_feat,
-                           sel_idx, n_sel, out_sel, nullptr, trace, max_n, max_blk, (double *)ws,
-                           st);
+    const size_t bytes = gk_sched_scratch_bytes(grid, max_n, max_blk);
+    cudaError_t e = cudaMallocAsync(&ws, bytes, st);
+    if (e != cudaSuccess) {
+        gk_set_error("scratch allocation of %zu B: %s", bytes, cudaGetErrorString(e));
+        return -2;
+    }
+    const int rc = gk_launch_sched(corpus, grid, kstat, latsum, out_status, out_si, out_sf,
+                                   out_feat, sel_idx, n_sel, out_sel, nullptr, trace, max_n,
+                                   max_blk, (double *)ws, st);
+    cudaFreeAsync(ws, st);
+    return rc;
 }
 
 int gk_rf_predict(const gk_ensemble *ens, const double *X, int64_t ld, int64_t n_rows,

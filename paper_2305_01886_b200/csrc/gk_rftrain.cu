@@ -31,7 +31,6 @@ constexpr int kMedRows = 32768;  // larger nodes use the multi-CTA histogram pat
 #endif
 constexpr int kBigRows = GK_BIG_ROWS;
 static_assert(kMedRows % kBigRows == 0, "chunking");
-constexpr int kSmallRows = 64;
 
 struct RfTrainData {
     const uint8_t *Xb;      // [n][F] bins
