@@ -65,7 +65,7 @@ class GradientBoostingRegressor(_LevelGrower):
     def fit(self, X, y, sample_weight=None):
         import torch
 
-        from .runtime import _ptr, device
+        from .runtime import _dev, _ptr, device
 
         if sample_weight is not None:
             raise NotImplementedError("sample_weight is not supported (training.py never passes it)")
@@ -92,7 +92,7 @@ class GradientBoostingRegressor(_LevelGrower):
         shift, shift2 = _shifts(rmax, n)
         yfp = torch.from_numpy(np.rint(np.ldexp(r0, shift)).astype(np.int64)).to(dev)
         y2fp = torch.from_numpy(np.rint(np.ldexp(r0 * r0, shift2)).astype(np.int64)).to(dev)
-        yd = torch.from_numpy(y).to(dev)
+        yd = _dev(y, dev)
         Fd = torch.full((n,), f0, dtype=torch.float64, device=dev)
         self._dev = dict(Xb=Xb, yfp=yfp, y2fp=y2fp, y=yd, n=n, F=F, shift=shift, shift2=shift2)
         counts = torch.ones(n, dtype=torch.int32, device=dev)

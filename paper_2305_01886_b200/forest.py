@@ -136,13 +136,13 @@ class _LevelGrower:
         midpoint threshold table; returns the [n][F] u8 bin matrix."""
         import torch
 
-        from .runtime import _ptr, device
+        from .runtime import _dev, _ptr, device
 
         n, F = X.shape
         L = _lib()
         dev = device()
         edges, n_edges = bin_edges(X, self.n_bins)   # float32 sample inside
-        Xd = torch.from_numpy(X).to(dev)               # k5_bin casts to float32 (sklearn)
+        Xd = _dev(X, dev)               # k5_bin casts to float32 (sklearn)
         Xb = torch.empty(n * F, dtype=torch.uint8, device=dev)
         bmin = torch.empty(F * N_BINS, dtype=torch.int32, device=dev)
         bmax = torch.empty(F * N_BINS, dtype=torch.int32, device=dev)
@@ -358,7 +358,7 @@ class RandomForestRegressor(_LevelGrower):
     def fit(self, X, y, sample_weight=None):
         import torch
 
-        from .runtime import _ptr, device
+        from .runtime import _dev, _ptr, device
 
         if sample_weight is not None:
             raise NotImplementedError("sample_weight is not supported (training.py never passes it)")
@@ -379,7 +379,7 @@ class RandomForestRegressor(_LevelGrower):
         shift2 = int(np.floor(62 - np.log2(max(y2max, 1e-300) * n + 1e-300)))
         shift2 = max(min(shift2, 60), -60)
         y2fp = torch.from_numpy(np.rint(np.ldexp(y2, shift2)).astype(np.int64)).to(dev)
-        yd = torch.from_numpy(y).to(dev)
+        yd = _dev(y, dev)
         self._dev = dict(Xb=Xb, yfp=yfp, y2fp=y2fp, y=yd, n=n, F=F, shift=shift, shift2=shift2)
 
         seeds = tree_seeds(self.random_state, self.n_estimators)

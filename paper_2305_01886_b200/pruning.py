@@ -104,14 +104,14 @@ def kendall_counts(X: np.ndarray):
     per pair a < b (discordant, joint ties).  X: [n, K] finite float64."""
     import torch
 
-    from .runtime import _check, _ptr, device
+    from .runtime import _check, _dev, _ptr, device
 
     X = np.ascontiguousarray(X, dtype=np.float64)
     n, K = X.shape
     L = _lib()
     dev = device()
     st = torch.cuda.current_stream().cuda_stream
-    Xd = torch.from_numpy(X).to(dev)
+    Xd = _dev(X, dev)
     ranks = torch.empty(K * n, dtype=torch.int32, device=dev)
     nu = torch.empty(K, dtype=torch.int32, device=dev)
     ties = torch.empty(K, dtype=torch.int64, device=dev)
@@ -166,13 +166,13 @@ def pearson_matrix(X: np.ndarray) -> np.ndarray:
     from the device's centred co-moments (NaN for a zero-variance column)."""
     import torch
 
-    from .runtime import _check, _ptr, device
+    from .runtime import _check, _dev, _ptr, device
 
     X = np.ascontiguousarray(X, dtype=np.float64)
     n, K = X.shape
     L = _lib()
     dev = device()
-    Xd = torch.from_numpy(X).to(dev)
+    Xd = _dev(X, dev)
     mean = torch.empty(K, dtype=torch.float64, device=dev)
     co = torch.empty(K * (K + 1) // 2, dtype=torch.float64, device=dev)
     wsb = L.gk_corr_pearson_workspace(n, K)

@@ -87,6 +87,8 @@ def _dev(a: np.ndarray, dev=None):
     """numpy -> device tensor of raw bytes (structured dtypes go as uint8)."""
     t = _torch()
     a = np.ascontiguousarray(a)
+    if not a.flags.writeable:      # torch.from_numpy wants a writable buffer
+        a = a.copy()
     host = t.from_numpy(a.view(np.uint8).reshape(-1) if a.dtype.fields else a)
     return host.to(dev or device(), non_blocking=False)
 
