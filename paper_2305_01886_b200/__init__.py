@@ -45,6 +45,7 @@ from .profiles import (
     resolve_profile,
     us_from_cycles,
 )
+from .featio import features_csv, features_from_csv, features_from_csv_arrays, features_to_csv
 from .ptx import parse_ptx
 from .ptx_native import pack_ptx
 
@@ -55,7 +56,8 @@ __all__ = [
     "FeatureVector", "FitError", "GpukalcError", "InstClass", "KernelGraph", "KernelSchedule",
     "LaunchConfig", "ProfileError", "PtxInstruction", "PtxParseError", "Resource",
     "SELECTED_FEATURES", "ScheduleError", "TreeEnsemble", "cycles_from_us", "extract_features",
-    "extract_features_batch", "global_mem_latency", "latency_of", "launch_overhead_us",
+    "extract_features_batch", "features_csv", "features_from_csv", "features_from_csv_arrays",
+    "features_to_csv", "global_mem_latency", "latency_of", "launch_overhead_us",
     "list_shipped_profiles", "load_ensemble", "load_profile", "mem_throughput", "pack_ptx",
     "parse_ptx",
     "predict_energy", "predict_launches", "predict_power", "predict_power_batch",

@@ -21,8 +21,8 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libgk.so"
 PTX_LIB = PKG / "libgkhost.so"   # host-only native code (g++, no CUDA): PTX front-end, ensemble I/O
-PTX_SOURCES = ["gk_ptx.cpp", "gk_ensio.cpp"]
-PTX_HEADERS = ["gk_ptx.h", "gk_ensio.h"]
+PTX_SOURCES = ["gk_ptx.cpp", "gk_ensio.cpp", "gk_featio.cpp"]
+PTX_HEADERS = ["gk_ptx.h", "gk_ensio.h", "gk_featio.h"]
 CXXFLAGS = ["-O2", "-std=c++17", "-fPIC", "-shared", "-pthread", "-Wall", "-Wextra"]
 SOURCES = ["gk_api.cu", "gk_sched.cu", "gk_rf.cu", "gk_rftrain.cu", "gk_corr.cu"]
 HEADERS = ["gk_internal.cuh", "gk_exp.h", "gk_exp_table.h", "gk_walk.cuh"]

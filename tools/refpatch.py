@@ -10,6 +10,8 @@ the unmodified reference tests call the CUDA kernels:
 * ``gpukalc.scheduler.schedule_block`` / ``schedule_cfg`` / ``schedule_kernel``
   (``scheduler.py:137-363``) -> K1 + fused K2/K3 (``schedule_batch``, trace on);
 * ``gpukalc.features.extract_features`` (``features.py:149-247``) -> same launch;
+* ``gpukalc.features.features_to_csv`` / ``features_from_csv``
+  (``features.py:250-272``) -> the native CSV writer / parser (``gk_featio``);
 * ``gpukalc.power.load_ensemble`` (``power.py:73-125``) -> native loader
   (``gk_ensio``), ``predict_power`` (``power.py:148-168``) -> K4;
 * ``gpukalc_trainer.training._make_model`` (``training.py:65-79``) -> the K5
@@ -160,6 +162,14 @@ def extract_features(profile, graph, launch):
     return ref_features.FeatureVector(*fv.as_row())
 
 
+def features_to_csv(rows, *, selected=False):
+    return gk.features_to_csv(rows, selected=selected)
+
+
+def features_from_csv(text):
+    return gk.features_from_csv(text)
+
+
 # ----------------------------------------------------------------- power
 
 _ENS: dict = {}
@@ -255,6 +265,8 @@ def install(trainer: bool = True) -> None:
     _rebind(inf, "schedule_cfg", schedule_cfg)
     _rebind(inf, "schedule_kernel", schedule_kernel)
     _rebind(inf, "extract_features", extract_features)
+    _rebind(inf, "features_to_csv", features_to_csv)
+    _rebind(inf, "features_from_csv", features_from_csv)
     _rebind(inf, "load_ensemble", load_ensemble)
     _rebind(inf, "predict_power", predict_power)
     if trainer:
