@@ -9,6 +9,7 @@ merged into one corpus with a single signature table.
 
 from __future__ import annotations
 
+import multiprocessing as mp
 import os
 from concurrent.futures import ProcessPoolExecutor
 
@@ -82,6 +83,7 @@ def synth_packed(n_kernels: int, seed: int, prefix: str = "k", procs: int | None
     for s, lo in enumerate(range(0, n_kernels, chunk)):
         hi = min(lo + chunk, n_kernels)
         jobs.append((hi - lo, seed * 100003 + s, f"{prefix}{seed}s{s}_"))
-    with ProcessPoolExecutor(max_workers=procs) as ex:
+    # forkserver: callers (bench, tests) already run CUDA / torch threads, where fork is unsafe
+    with ProcessPoolExecutor(max_workers=procs, mp_context=mp.get_context("forkserver")) as ex:
         parts = list(ex.map(_shard, jobs))
     return merge_corpora(parts)

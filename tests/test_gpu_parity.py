@@ -214,6 +214,41 @@ def test_fused_sweep_matches_oracle_pipeline():
         assert bits_equal(energy[m], en)
 
 
+def test_config5_first_1000_kernels_every_point():
+    """SURVEY §8(d) #5 parity bar: all points of the first 1,000 kernels of
+    config #5 (seed 5; 256 configs x {k20, m60, gtx1050} = 768,000 points)
+    bit-exact against the oracle -- cycles, schedule scalars, all 32 features --
+    and the fused sweep's time / power / energy on the same grid."""
+    from paper_2305_01886_b200 import workloads
+
+    rt = _rt()
+    c = workloads.synth_packed(1000, seed=5)
+    profs = [resolve_profile(a) for a in ("tesla_k20", "tesla_m60", "gtx1050")]
+    cfgs = corpus.config5_grid()
+    got = _run(c, profs, cfgs)
+    want = O.schedule_features(O.HostGrid(c, profs, cfgs))
+    assert len(want["status"]) == 768_000
+    _assert_same(got, want, want["status"])
+    assert (want["status"] == 0).sum() > 700_000
+    sel = pack.manifest_indices(pack.SELECTED_FEATURES)
+    ok = want["status"] == 0
+    hi = np.nanmax(np.where(ok[:, None], want["feat"][:, sel], np.nan), axis=0) + 1.0
+    flats = [random_forest_flat(32, 12, pack.SELECTED_FEATURES, np.zeros(15), hi, seed=50 + a)
+             for a in range(3)]
+    dc = rt.DeviceCorpus.upload(c)
+    dg = rt.DeviceGrid.build(dc, profs, cfgs)
+    sw = rt.Sweep(dc, dg, [rt.DeviceEnsemble.upload(f) for f in flats], sel)
+    status, t_us, power, energy = [x.cpu().numpy() for x in sw.run()]
+    assert np.array_equal(status, want["status"])
+    assert bits_equal(t_us[ok], want["sf"][ok, 7])
+    arch_of = (np.arange(len(status)) // len(cfgs)) % 3
+    for a in range(3):
+        m = ok & (arch_of == a)
+        pw, en = O.rf_predict(flats[a], want["feat"][m][:, sel], time_us=want["sf"][m, 7])
+        assert bits_equal(power[m], pw)
+        assert bits_equal(energy[m], en)
+
+
 def test_throughput_clamps_counted_and_logged(caplog):
     """A throughput model that goes non-positive is clamped to tp_floor
     (profiles.py:173-181, the reference warns per call): the device counts the
