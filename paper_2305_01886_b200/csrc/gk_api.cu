@@ -141,7 +141,11 @@ int gk_schedule_features(const gk_corpus *corpus, const gk_grid *grid, const gk_
 int gk_rf_predict(const gk_ensemble *ens, const double *X, int64_t ld, int64_t n_rows,
                   const uint8_t *status, const double *time_us, double *out_power,
                   double *out_energy, void *stream) {
-    if (!ens || !X || !out_power) {
+    if (n_rows < 0) {
+        gk_set_error("gk_rf_predict: n_rows=%lld", (long long)n_rows);
+        return -1;
+    }
+    if (!ens || ((!X || !out_power) && n_rows > 0)) {  // an empty batch may carry null buffers
         gk_set_error("gk_rf_predict: null argument");
         return -1;
     }

@@ -271,3 +271,40 @@ def test_throughput_clamps_counted_and_logged(caplog):
     assert np.array_equal(got["status"], want["status"])
     ok = want["status"] == 0
     assert bits_equal(got["sf"][ok], want["sf"][ok]) and bits_equal(got["feat"][ok], want["feat"][ok])
+
+
+def test_many_archs_and_single_point_grids():
+    """n_arch > 4 takes K1's wide latency-sum path; a 1 x 1 x 1 grid; the
+    per-arch tables of duplicated profiles stay independent."""
+    from paper_2305_01886_b200.profiles import profile_from_dict, profile_to_dict
+
+    gs = [ptx.parse_ptx(t, n, loop_counts=l) for n, t, l in corpus.synth_corpus(40, 77)]
+    c = pack.pack_corpus(gs)
+    base = [resolve_profile(a) for a in ("k20", "m60", "1050", "k4200")]
+    doc = profile_to_dict(base[0])
+    doc["latencies"]["issue_gap"] = {}
+    doc["name"] = "k20_nogap"
+    profs = base + [profile_from_dict(doc), fixture_profile(), base[2]]
+    cfgs = corpus.random_configs(random.Random(7), 9)
+    got = _run(c, profs, cfgs)
+    want = O.schedule_features(O.HostGrid(c, profs, cfgs))
+    _assert_same(got, want, want["status"])
+    one = pack.pack_corpus(gs[:1])
+    got1 = _run(one, base[:1], [(13, 128, 32, 0)])
+    want1 = O.schedule_features(O.HostGrid(one, base[:1], [(13, 128, 32, 0)]))
+    _assert_same(got1, want1, want1["status"])
+
+
+def test_empty_inputs():
+    """Zero kernels and zero rows are valid batches: empty outputs, no launch errors."""
+    rt = _rt()
+    import torch
+
+    got = _run(pack.pack_corpus([]), [resolve_profile("k20")], corpus.config2_grid())
+    assert got["status"].shape == (0,) and got["feat"].shape[0] == 0
+    flat = random_forest_flat(5, 6, ["a", "b"], np.zeros(2), np.ones(2), seed=3)
+    de = rt.DeviceEnsemble.upload(flat)
+    p, e = rt.rf_predict(de, torch.zeros((0, 2), dtype=torch.float64, device="cuda"),
+                         time_us=torch.zeros(0, dtype=torch.float64, device="cuda"))
+    assert p.shape == (0,) and e.shape == (0,)
+    torch.cuda.synchronize()
