@@ -191,7 +191,7 @@ def run_ours(args, rank, world, local_rank):
     dg = rt.DeviceGrid.build(dc, W["profiles"], W["configs"])
     n_pts = dg.n_points
     flats = make_ensembles(W, dc, dg, rt, args.trees, args.depth)
-    ens = [rt.DeviceEnsemble.upload(f) for f in flats]
+    ens = [rt.DeviceEnsemble.upload(f, layout=os.environ.get("GK_WALK_LAYOUT")) for f in flats]
     sweep = rt.Sweep(dc, dg, ens, W["sel"])
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2

@@ -35,6 +35,7 @@ __device__ __forceinline__ double tput_c(double a, double b, double c, double fl
 }
 
 constexpr int kWarps = 4;            // warps per CTA (each warp: 32 points of one kernel)
+constexpr int kXfStride = 64;        // floats between feature rows of the compact-walk key tile
 #ifndef GK_PROBE
 #define GK_PROBE 2  // backward probe steps before the binary search for the first live span
 #endif
@@ -514,7 +515,7 @@ __device__ __forceinline__ double finish_point(const gk_corpus &C, const gk_grid
         for (uint32_t j = 0; j < O.n_sel; j++) {
             const double v = scale_feature(feature(O.sel_idx[j]), E->scale_lo[j], E->scale_hi[j]);
             xw[(size_t)j * 32] = v;
-            if (xf) xf[(size_t)j * 32] = __double2float_rd(v);  // compact-walk key
+            if (xf) xf[(size_t)j * kXfStride] = __double2float_rd(v);  // compact-walk key
         }
     return time_us;
 }
@@ -527,7 +528,7 @@ __device__ __forceinline__ double finish_point(const gk_corpus &C, const gk_grid
 struct FusedArgs {
     gk_ensemble ens[4];
     uint32_t n_ens;
-    int compact;  // walk a compact layout when the ensemble has one (GK_FUSED_COMPACT=1)
+    int compact;  // walk a compact layout when the ensemble has one (default; GK_FUSED_COMPACT=0: 16-byte nodes)
     double *power, *energy;
 };
 
@@ -541,8 +542,11 @@ struct FusedArgs {
 #ifndef GK_FUSED_ILP
 #define GK_FUSED_ILP 8  // trees walked in lock-step inside the fused sweep (8 measured best)
 #endif
+#ifndef GK_FUSED_B2_SINK
+#define GK_FUSED_B2_SINK 1
+#endif
 #ifndef GK_FUSED_B2_ILP
-#define GK_FUSED_B2_ILP 4  // blocked walk: trees in lock-step (each step = 2 levels, 8 regs/tree)
+#define GK_FUSED_B2_ILP 6  // blocked walk: trees in lock-step (each step = 2 levels); c2: 6.36 ms (4: 6.75 w/o sink, 7: 6.71, 8: 7.87)
 #endif
 template <bool kFused>
 __global__ void __launch_bounds__(kWarps * 32, kFused ? GK_FUSED_MINB : GK_K23_MINB) k23_schedule(
@@ -587,16 +591,18 @@ __global__ void __launch_bounds__(kWarps * 32, kFused ? GK_FUSED_MINB : GK_K23_M
     // (row 0 of each warp's tile is the +inf leaf slot; features start at row 1)
     double *xw = slab_base + (size_t)kWarps * 3 * ns * 32 + (size_t)warp * (O.n_sel + 1) * 32 +
                  32 + lane;
-    // fused: per-warp [n_sel + 1][32] f32 keys for the compact walk after the fp64 tiles
-    // (only allocated when the fused walk uses a compact layout, F.compact)
+    // fused: f32 keys for the compact walk after the fp64 tiles (only allocated
+    // when the fused walk uses a compact layout, F.compact), a warp pair's
+    // tiles interleaved as [n_sel + 1][64] so the row stride is 256 B (the
+    // blocked walk's PRMT feature offsets)
     float *xf = (kFused && F.compact)
                     ? reinterpret_cast<float *>(slab_base + (size_t)kWarps * 3 * ns * 32 +
                                                 (size_t)kWarps * (O.n_sel + 1) * 32) +
-                          (size_t)warp * (O.n_sel + 1) * 32 + 32 + lane
+                          (size_t)(warp >> 1) * (O.n_sel + 1) * 64 + 64 + (warp & 1) * 32 + lane
                     : nullptr;
     if (kFused) {
         xw[-32] = __longlong_as_double(0x7ff0000000000000ll);
-        if (xf) xf[-32] = __int_as_float(0x7f800000);
+        if (xf) xf[-kXfStride] = __int_as_float(0x7f800000);
     }
 
     // dynamic work queue (items differ widely in cost; G.order puts the most
@@ -713,11 +719,13 @@ __global__ void __launch_bounds__(kWarps * 32, kFused ? GK_FUSED_MINB : GK_K23_M
                 double pw = NaN, en = NaN;
                 if (!isnan(t_ok)) {
                     auto x64 = [&](int f) { return xw[f * 32]; };
-                    // measured on B200 (c2): inside the fused sweep the 16-byte
-                    // nodes beat both compact layouts (80-register budget,
-                    // L1 data-pipe bound), so they are the default here
-                    pw = F.compact && Ep->blocks   ? walk_ensemble_b2<GK_FUSED_B2_ILP>(*Ep, xf, 32, x64)
-                         : F.compact && Ep->nodes8 ? walk_ensemble8<GK_FUSED_ILP>(*Ep, xf, 32, x64)
+                    // measured on B200 (c2): the blocked walk (half the L1
+                    // wavefronts of the 16-byte nodes, more instructions) wins
+                    // once its loads are unpredicated (sink) and its feature
+                    // offsets are one PRMT: 6.36 vs 6.44 ms; nodes8 loses
+                    pw = F.compact && Ep->blocks
+                             ? walk_ensemble_b2<GK_FUSED_B2_ILP, true, GK_FUSED_B2_SINK>(*Ep, xf, kXfStride, x64)
+                         : F.compact && Ep->nodes8 ? walk_ensemble8<GK_FUSED_ILP>(*Ep, xf, kXfStride, x64)
                                                    : walk_ensemble<GK_FUSED_ILP>(*Ep, xw, 32);
                     en = __dmul_rn(pw, t_ok);
                 }
@@ -903,7 +911,7 @@ int gk_launch_sweep_fused(const gk_corpus *C, const gk_grid *G, const gk_kstat *
     F.n_ens = n_ens;
     {
         const char *e = getenv("GK_FUSED_COMPACT");
-        F.compact = e && atoi(e) != 0;
+        F.compact = e ? atoi(e) != 0 : 1;
     }
     F.power = power;
     F.energy = energy;

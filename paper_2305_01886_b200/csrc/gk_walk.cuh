@@ -138,10 +138,19 @@ __device__ __forceinline__ void ld_block2(const gk_block2 *p, uint32_t (&w)[8]) 
                  : "l"(p));
 }
 
-template <int kIlp, bool kTail, class X64>
+// kS64: the feature tile's stride is 64 floats (256 B), so a feature byte
+// becomes its byte offset with one PRMT (byte k -> byte 1) instead of a
+// shift / mask / multiply-add chain per slot.  kSink: finished trees load a
+// shared dummy block instead of a predicated load + zeroed words -- fewer
+// instructions and registers for more L1 wavefronts.  Measured on B200: the
+// fused sweep (issue-bound with this walk) wants both; K4 on config #4
+// (L1-wavefront-bound) loses 10 % with kSink and gains nothing from kS64.
+template <int kIlp, bool kTail, bool kS64, bool kSink, class X64>
 __device__ __forceinline__ void walk_b2_group(const gk_ensemble &E, uint32_t t, int nq,
                                               const float *xf, int stride, const X64 &x64,
                                               double &total) {
+    // hoisted: E may sit in a dynamically indexed parameter array (fused sweep)
+    const gk_block2 *__restrict__ blocks = E.blocks;
     uint32_t ref[kIlp];
     int d = 0;
 #pragma unroll
@@ -155,8 +164,13 @@ __device__ __forceinline__ void walk_b2_group(const gk_ensemble &E, uint32_t t, 
         uint32_t w[kIlp][8];
 #pragma unroll
         for (int q = 0; q < kIlp; q++) {
-            if (!(ref[q] & GK_LEAF)) ld_block2(E.blocks + ref[q], w[q]);
-            else {
+            if (kSink) {
+                // a finished tree loads block 0 (one shared line; its words are
+                // never used) instead of predicating the load and zeroing
+                ld_block2(blocks + (ref[q] & GK_LEAF ? 0u : ref[q]), w[q]);
+            } else if (!(ref[q] & GK_LEAF)) {
+                ld_block2(blocks + ref[q], w[q]);
+            } else {
 #pragma unroll
                 for (int k = 0; k < 8; k++) w[q][k] = 0;
             }
@@ -165,7 +179,11 @@ __device__ __forceinline__ void walk_b2_group(const gk_ensemble &E, uint32_t t, 
 #pragma unroll
         for (int q = 0; q < kIlp; q++)
 #pragma unroll
-            for (int k = 0; k < 3; k++) a[q][k] = xf[((w[q][3] >> (8 * k)) & 0xFFu) * stride];
+            for (int k = 0; k < 3; k++)
+                a[q][k] = kS64 ? *reinterpret_cast<const float *>(
+                                     reinterpret_cast<const char *>(xf) +
+                                     __byte_perm(w[q][3], 0u, 0x4404u | (k << 4)))
+                               : xf[((w[q][3] >> (8 * k)) & 0xFFu) * stride];
         uint32_t tie = 0;
         uint32_t nref[kIlp];
 #pragma unroll
@@ -201,14 +219,15 @@ __device__ __forceinline__ void walk_b2_group(const gk_ensemble &E, uint32_t t, 
         if (!kTail || q < nq) total = __dadd_rn(total, __ldg(E.leaf_val + (ref[q] & ~GK_LEAF)));
 }
 
-template <int kIlp, class X64>
+template <int kIlp, bool kS64 = false, bool kSink = false, class X64>
 __device__ __forceinline__ double walk_ensemble_b2(const gk_ensemble &E, const float *xf, int stride,
                                                    const X64 &x64) {
     double total = E.base_score;
     uint32_t t = 0;
-    for (; t + kIlp <= E.n_trees; t += kIlp) walk_b2_group<kIlp, false>(E, t, kIlp, xf, stride, x64, total);
+    for (; t + kIlp <= E.n_trees; t += kIlp)
+        walk_b2_group<kIlp, false, kS64, kSink>(E, t, kIlp, xf, stride, x64, total);
     if (t < E.n_trees)
-        walk_b2_group<kIlp, true>(E, t, (int)(E.n_trees - t), xf, stride, x64, total);
+        walk_b2_group<kIlp, true, kS64, kSink>(E, t, (int)(E.n_trees - t), xf, stride, x64, total);
     return total;
 }
 

@@ -474,6 +474,8 @@ def blocked(flat: FlatEnsemble) -> Blocked | None:
         own = ref(s_k)
         out["e"][:, 2 * (k - 1)] = np.where(lf, own, ref(np.where(lf, s_k, c)))
         out["e"][:, 2 * (k - 1) + 1] = np.where(lf, own, ref(np.where(lf, s_k, c + 1)))
+    if len(r) == 0:  # all trees are single leaves: keep block 0 (the walk's sink) addressable
+        out, thr = np.zeros(1, BLOCK2_DT), np.zeros((1, 3))
     return Blocked(blocks=out, thr64=np.ascontiguousarray(thr.reshape(-1)),
                    leaf_val=np.ascontiguousarray(nd["v"][leaf]),
                    root=ref(flat.tree_off.astype(np.int64)))
