@@ -149,7 +149,9 @@ template <int kIlp, bool kTail, bool kS64, bool kSink, class X64>
 __device__ __forceinline__ void walk_b2_group(const gk_ensemble &E, uint32_t t, int nq,
                                               const float *xf, int stride, const X64 &x64,
                                               double &total) {
-    // hoisted: E may sit in a dynamically indexed parameter array (fused sweep)
+    // hoisted for the sink form (the fused sweep, where E sits in a dynamically
+    // indexed parameter array); K4 keeps re-reading E.blocks -- measured: the
+    // hoisted pointer costs K4 5 % on config #4
     const gk_block2 *__restrict__ blocks = E.blocks;
     uint32_t ref[kIlp];
     int d = 0;
@@ -169,7 +171,7 @@ __device__ __forceinline__ void walk_b2_group(const gk_ensemble &E, uint32_t t, 
                 // never used) instead of predicating the load and zeroing
                 ld_block2(blocks + (ref[q] & GK_LEAF ? 0u : ref[q]), w[q]);
             } else if (!(ref[q] & GK_LEAF)) {
-                ld_block2(blocks + ref[q], w[q]);
+                ld_block2(E.blocks + ref[q], w[q]);
             } else {
 #pragma unroll
                 for (int k = 0; k < 8; k++) w[q][k] = 0;
