@@ -537,7 +537,7 @@ struct FusedArgs {
 #define GK_K23_MINB 6
 #endif
 #ifndef GK_FUSED_MINB
-#define GK_FUSED_MINB 7  // measured: 6.56 ms vs 6.67 (6) and 6.66 (8) on config #2
+#define GK_FUSED_MINB 8  // blocked walk, c2: 6.22 ms at 8 (7: 6.35, 9: 6.40, 10: 8.3); 16-byte nodes preferred 7
 #endif
 #ifndef GK_FUSED_ILP
 #define GK_FUSED_ILP 8  // trees walked in lock-step inside the fused sweep (8 measured best)
@@ -546,7 +546,7 @@ struct FusedArgs {
 #define GK_FUSED_B2_SINK 1
 #endif
 #ifndef GK_FUSED_B2_ILP
-#define GK_FUSED_B2_ILP 6  // blocked walk: trees in lock-step (each step = 2 levels); c2: 6.36 ms (4: 6.75 w/o sink, 7: 6.71, 8: 7.87)
+#define GK_FUSED_B2_ILP 5  // blocked walk: trees in lock-step (each step = 2 levels); c2 at MINB 8: 6.22 ms (4: 6.40, 6: 6.49)
 #endif
 template <bool kFused>
 __global__ void __launch_bounds__(kWarps * 32, kFused ? GK_FUSED_MINB : GK_K23_MINB) k23_schedule(
