@@ -164,7 +164,12 @@ def make_ensembles(W, dc, dg, rt, n_trees, depth):
     from paper_2305_01886_b200 import pack
     from paper_2305_01886_b200.ensemble import random_forest_flat
 
-    out = rt.schedule_features(dc, dg, si=False, sf=False, feat=False, sel_idx=W["sel"])
+    if dg.n_points > 100_000_000:   # bounds from a kernel subset (the full selection would be ~92 GB at config #5)
+        sub = rt.DeviceGrid.build(dc, W["profiles"], W["configs"],
+                                  kernel_ids=np.arange(min(dg.n_k, 100_000_000 // (dg.n_points // dg.n_k))))
+        out = rt.schedule_features(dc, sub, si=False, sf=False, feat=False, sel_idx=W["sel"])
+    else:
+        out = rt.schedule_features(dc, dg, si=False, sf=False, feat=False, sel_idx=W["sel"])
     X = out["sel"]
     ok = out["status"] == 0
     Xo = X[ok]

@@ -162,7 +162,9 @@ size_t gk_sweep_workspace_bytes(const gk_corpus *corpus, const gk_grid *grid, ui
     size_t b = 0;
     b += ((sizeof(gk_kstat) * grid->n_k + 255) / 256) * 256;
     b += ((sizeof(double) * 3 * grid->n_k * grid->n_arch + 255) / 256) * 256;
-    b += ((sizeof(double) * n_points * n_sel + 255) / 256) * 256;
+    // the two-kernel form stages the manifest features of every point; the
+    // fused sweep keeps them on chip (config #5 full: 92 GB not allocated)
+    if (!sweep_fused()) b += ((sizeof(double) * n_points * n_sel + 255) / 256) * 256;
     // the per-warp reservation-table slabs + work-queue counter: owned by the
     // caller's workspace, so concurrent sweeps on different streams never share
     const uint32_t max_n = corpus && corpus->max_n ? corpus->max_n : 1;
@@ -198,7 +200,7 @@ int gk_predict_energy_sweep(const gk_corpus *corpus, const gk_grid *grid,
     stage_mark(1, st);
     const uint32_t max_n = corpus->max_n ? corpus->max_n : 1;
     const uint32_t max_blk = corpus->max_blk ? corpus->max_blk : 1;
-    w += ((sizeof(double) * n_points * n_sel + 255) / 256) * 256;
+    if (!sweep_fused()) w += ((sizeof(double) * n_points * n_sel + 255) / 256) * 256;
     void *ws = w;  // scratch slabs inside the caller's workspace (gk_sweep_workspace_bytes)
     if (sweep_fused()) {
         // one kernel: schedule + features + ensemble walk + energy per warp of points
