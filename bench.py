@@ -233,6 +233,10 @@ def run_ours(args, rank, world, local_rank):
     # ---- per-kernel split (same stream, events between launches)
     split = per_kernel_split(rt, dc, dg, sweep, W, flush, args.steps)
 
+    # ---- config #2 as BASELINE words it: the cycle estimator alone (K1 + K3,
+    # every KernelSchedule scalar out, no features / power), same grid
+    cyc = cycle_sweep(rt, dc, dg, flush, args.steps, world)
+
     # ---- e2e: host buffers in, results out, through the C-ABI per step
     e2e = run_e2e(rt, W, ens, args.steps, flush)
     # the host-buffer path returns the same bits as the device-resident sweep
@@ -249,8 +253,36 @@ def run_ours(args, rank, world, local_rank):
     total_ms, e2e_ms = float(t[0]), float(t[1])
     st = sweep.status.cpu().numpy()
     return {"W": W, "n_pts": n_pts, "total_ms": total_ms, "step_ms": step_ms, "split": split,
-            "e2e_ms": e2e_ms, "e2e": e2e, "clk": clk.summary(), "flats": flats,
+            "e2e_ms": e2e_ms, "e2e": e2e, "clk": clk.summary(), "flats": flats, "cycle": cyc,
             "infeasible": int((st != 0).sum()), "dc_bytes": dc.nbytes}
+
+
+def cycle_sweep(rt, dc, dg, flush, steps, world):
+    """K1 + K3 over the grid writing status + the 6 int64 / 9 fp64 schedule
+    outputs per point (schedule_kernel's KernelSchedule scalars), no features,
+    no ensemble: BASELINE configs[1]'s "cycle-estimator-only sweep"."""
+    import torch
+    import torch.distributed as dist
+
+    for _ in range(3):
+        rt.schedule_features(dc, dg, feat=False)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(steps)]
+    for k in range(steps):
+        flush.zero_()
+        evs[k][0].record(stream)
+        rt.schedule_features(dc, dg, feat=False)
+        evs[k][1].record(stream)
+    torch.cuda.synchronize()
+    t = torch.tensor([sum(a.elapsed_time(b) for a, b in evs)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t[0])
+    return {"value": dg.n_points * world * steps / (ms / 1e3), "unit": "points/s",
+            "ms_per_step": ms / steps, "kernels": "k1_static + k23_schedule (status, si[6], sf[9])",
+            "gpu_launches": 2 * steps}
 
 
 def per_kernel_split(rt, dc, dg, sweep, W, flush, steps):
@@ -468,6 +500,7 @@ def main():
                         "on 3 streams (copies overlap the neighbouring steps' sweeps)"},
         "gpu_launches": len(split) * args.steps,
         "kernel_ms": split,
+        "cycle_sweep": R["cycle"],
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                      "algorithmic_bytes": alg[dom], "traffic": traffic,

@@ -4,6 +4,8 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <mutex>
+
 #include "gk_internal.cuh"
 
 static thread_local char g_err[512] = "";
@@ -123,7 +125,22 @@ int gk_schedule_features(const gk_corpus *corpus, const gk_grid *grid, const gk_
     const cudaStream_t st = (cudaStream_t)stream;
     const uint32_t max_n = corpus->max_n ? corpus->max_n : 1;
     const uint32_t max_blk = corpus->max_blk ? corpus->max_blk : 1;
-    // stream-ordered scratch (pooled by the driver): reentrant per stream
+    // stream-ordered scratch from the device's default pool: reentrant per
+    // stream; the pool keeps freed memory (release threshold raised once per
+    // device) so repeated calls do not map / unmap ~1 GB each time
+    {
+        static std::once_flag once[64];
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev >= 0 && dev < 64)
+            std::call_once(once[dev], [dev] {
+                cudaMemPool_t pool;
+                if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+                    uint64_t keep = UINT64_MAX;
+                    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+                }
+            });
+    }
     void *ws = nullptr;
     const size_t bytes = gk_sched_scratch_bytes(grid, max_n, max_blk);
     cudaError_t e = cudaMallocAsync(&ws, bytes, st);
