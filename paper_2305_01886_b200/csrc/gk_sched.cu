@@ -534,7 +534,7 @@ struct FusedArgs {
 
 // Persistent warps over work items (kernel, up to 32 consecutive (arch, config) pairs).
 #ifndef GK_K23_MINB
-#define GK_K23_MINB 6
+#define GK_K23_MINB 4  // cycle-only sweep (c2): 2.60 ms at 4 (3: 2.82, 5: 2.67, 6: 2.77, 7: 2.82)
 #endif
 #ifndef GK_FUSED_MINB
 #define GK_FUSED_MINB 8  // blocked walk, c2: 6.22 ms at 8 (7: 6.35, 9: 6.40, 10: 8.3); 16-byte nodes preferred 7

@@ -8,7 +8,7 @@ for spec in "$@"; do
   for rep in 1 2; do
     echo -n "[$flags | $envs] "
     env $envs timeout 300 python bench.py --no-cpu --no-rf --steps 5 2>/dev/null | tail -1 |
-      python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['value']/1e6,2), 'M pts/s', round(d['kernel_ms']['k23_schedule<fused>'],3), 'ms fused')"
+      python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['value']/1e6,2), 'M pts/s', round(d['kernel_ms']['k23_schedule<fused>'],3), 'ms fused', round(d['cycle_sweep']['ms_per_step'],3), 'ms cycles-only')"
   done
 done
 python -m paper_2305_01886_b200.build --force > /dev/null
