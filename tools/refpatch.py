@@ -255,11 +255,12 @@ def _warm() -> None:
     gk.extract_features(gk.resolve_profile("tesla_k20"), g, gk.LaunchConfig(13, 128, 32, 0))
 
 
-def install(trainer: bool = True) -> None:
+def install(trainer: bool = True, warm: bool = True) -> None:
     import paper_2305_01886_b200.runtime as rt
 
     rt.load_library()           # the CUDA library must be there: no silent host path
-    _warm()
+    if warm:
+        _warm()
     inf = [gpukalc, ref_sched, ref_features, ref_power, ref_cli]
     _rebind(inf, "schedule_block", schedule_block)
     _rebind(inf, "schedule_cfg", schedule_cfg)
