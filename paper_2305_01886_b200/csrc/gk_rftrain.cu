@@ -177,8 +177,20 @@ __device__ __forceinline__ bool better(double p, int f, int b, const BestSplit &
 
 // Evaluate all boundaries of one feature's histogram with one warp:
 // left = bins <= b; proxy = S_L^2 / W_L + S_R^2 / W_R (sklearn's MSE proxy).
+// The candidates are the non-empty bins (an empty bin repeats the previous
+// boundary's split, whose proxy ties and wins by the lower bin: exact).  The
+// proxy's two fp64 divisions were a quarter of the split search's
+// instructions when every one of a lane's 8 bin slots took them; sparse
+// histograms now compact their candidates first.
+struct CandSmem {  // one warp's compacted split candidates (<= 64)
+    uint64_t c[64];
+    int64_t s[64];
+    uint16_t b[64];
+};
+
+template <bool kCompact>
 __device__ __forceinline__ BestSplit eval_feature(const uint64_t *cw, const int64_t *s, int f,
-                                                  int lane) {
+                                                  int lane, CandSmem *cc) {
     uint64_t c8[8];
     int64_t s8[8];
     uint64_t cacc = 0;
@@ -207,20 +219,56 @@ __device__ __forceinline__ BestSplit eval_feature(const uint64_t *cw, const int6
     cpre -= cacc;
     spre -= sacc;
     const uint32_t C = (uint32_t)(ctot >> 32), W = (uint32_t)ctot;
-    BestSplit best{-1.0, 0x7fffffff, 0x7fffffff, 0};
+    uint32_t mask = 0;
 #pragma unroll
     for (int j = 0; j < 8; j++) {
         const int b = lane * 8 + j;
-        if (b >= kBins - 1) continue;
-        // an empty bin repeats the previous boundary's split, whose proxy ties
-        // and wins (lower bin): only non-empty bins are candidates (exact)
-        if (c8[j] == (j ? c8[j - 1] : 0ull)) continue;
-        const uint64_t cl = cpre + c8[j];
-        const uint32_t CL = (uint32_t)(cl >> 32), WL = (uint32_t)cl;
-        if (CL < 1 || C - CL < 1) continue;
-        const double SL = (double)(spre + s8[j]), SR = (double)(stot - spre - s8[j]);
-        const double p = SL * SL / (double)WL + SR * SR / (double)(W - WL);
-        if (better(p, f, b, best)) best = BestSplit{p, f, b, CL};
+        const uint32_t CL = (uint32_t)((cpre + c8[j]) >> 32);
+        const bool nonempty = c8[j] != (j ? c8[j - 1] : 0ull);
+        if (b < kBins - 1 && nonempty && CL >= 1 && C - CL >= 1) mask |= 1u << j;
+    }
+    const int n = __popc(mask);
+    int off = n;  // inclusive scan of the candidate counts
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int a = __shfl_up_sync(GK_FULL, off, o);
+        if (lane >= o) off += a;
+    }
+    const int total = __shfl_sync(GK_FULL, off, 31);
+    BestSplit best{-1.0, 0x7fffffff, 0x7fffffff, 0};
+    if (kCompact && total <= 64) {
+        // sparse (every node of <= 64 rows; small medium nodes): compact the
+        // candidates so each division pair runs once per candidate, <= 2
+        // rounds, instead of in all 8 bin slots of the warp
+        off -= n;
+#pragma unroll
+        for (int j = 0; j < 8; j++)
+            if (mask >> j & 1u) {
+                cc->c[off] = cpre + c8[j];
+                cc->s[off] = spre + s8[j];
+                cc->b[off] = (uint16_t)(lane * 8 + j);
+                off++;
+            }
+        __syncwarp();
+        for (int i = lane; i < total; i += 32) {
+            const uint64_t cl = cc->c[i];
+            const uint32_t CL = (uint32_t)(cl >> 32), WL = (uint32_t)cl;
+            const double SL = (double)cc->s[i], SR = (double)(stot - cc->s[i]);
+            const double p = SL * SL / (double)WL + SR * SR / (double)(W - WL);
+            if (better(p, f, cc->b[i], best)) best = BestSplit{p, f, (int)cc->b[i], CL};
+        }
+        __syncwarp();
+    } else {
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            if (!(mask >> j & 1u)) continue;
+            const int b = lane * 8 + j;
+            const uint64_t cl = cpre + c8[j];
+            const uint32_t CL = (uint32_t)(cl >> 32), WL = (uint32_t)cl;
+            const double SL = (double)(spre + s8[j]), SR = (double)(stot - spre - s8[j]);
+            const double p = SL * SL / (double)WL + SR * SR / (double)(W - WL);
+            if (better(p, f, b, best)) best = BestSplit{p, f, b, CL};
+        }
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
@@ -288,7 +336,8 @@ __device__ __forceinline__ void eval_chunk(HistSmem &H, int F, int fc, BestSplit
     for (int j = warp; j < kFC; j += nwarps) {
         const int f = fc * kFC + j;
         if (f >= F) break;
-        const BestSplit b = eval_feature(H.cw[j], H.s[j], f, lane);
+        // measured: compaction costs the CTA-per-node path more than it saves
+        const BestSplit b = eval_feature<false>(H.cw[j], H.s[j], f, lane, nullptr);
         if (better(b.proxy, b.feat, b.bin, mine)) mine = b;
     }
 }
@@ -525,6 +574,7 @@ __global__ void __launch_bounds__(128) k5_split_small(RfTrainData D, const RfTas
     // boundary scan as the larger nodes
     __shared__ uint64_t hcw[4][kBins];
     __shared__ int64_t hs[4][kBins];
+    __shared__ CandSmem hcand[4];
     uint64_t *cw = hcw[threadIdx.x >> 5];
     int64_t *hsw = hs[threadIdx.x >> 5];
     BestSplit best{-1.0, 0x7fffffff, 0x7fffffff, 0};
@@ -546,7 +596,7 @@ __global__ void __launch_bounds__(128) k5_split_small(RfTrainData D, const RfTas
             }
         }
         __syncwarp();
-        const BestSplit b = eval_feature(cw, hsw, f, lane);
+        const BestSplit b = eval_feature<true>(cw, hsw, f, lane, &hcand[threadIdx.x >> 5]);
         if (better(b.proxy, b.feat, b.bin, best)) best = b;
         __syncwarp();
 #pragma unroll
