@@ -465,6 +465,10 @@ __global__ void __launch_bounds__(256) k5_eval_big(RfTrainData D, const int32_t 
 // histogram path's (boundary b = a bin present in the node; left = bins <= b),
 // so the chosen split is identical.
 constexpr int kTiny = 16;
+#ifndef GK_SMALL_RPL
+#define GK_SMALL_RPL 2  // rows per lane of the warp-per-node path (host SMALL = 32 x this)
+#endif
+constexpr int kSmallRpl = GK_SMALL_RPL;
 
 __device__ __forceinline__ void split_tiny(const RfTrainData &D, const RfTask &T,
                                            const int32_t *__restrict__ rows, int m, int lane,
@@ -551,19 +555,20 @@ __global__ void __launch_bounds__(128) k5_split_small(RfTrainData D, const RfTas
         split_tiny(D, T, rows, m, lane, threadIdx.x >> 5, wv, sv, rv, out + ti);
         return;
     }
-    int32_t r[2];
-    uint32_t w[2];
-    int64_t s[2];
+    int32_t r[kSmallRpl];
+    uint32_t w[kSmallRpl];
+    int64_t s[kSmallRpl];
+    uint32_t W = 0;
+    int64_t S = 0;
 #pragma unroll
-    for (int h = 0; h < 2; h++) {
+    for (int h = 0; h < kSmallRpl; h++) {
         const int i = lane + 32 * h;
         r[h] = i < m ? rows[T.begin + i] : -1;
         w[h] = i < m ? cnt[r[h]] : 0u;
         s[h] = i < m ? (int64_t)w[h] * D.yfp[r[h]] : 0;
+        W += w[h];
+        S += s[h];
     }
-    // totals
-    uint32_t W = w[0] + w[1];
-    int64_t S = s[0] + s[1];
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
         W += __shfl_xor_sync(GK_FULL, W, o);
@@ -586,9 +591,9 @@ __global__ void __launch_bounds__(128) k5_split_small(RfTrainData D, const RfTas
     }
     __syncwarp();
     for (int f = 0; f < D.F; f++) {
-        int bin[2];
+        int bin[kSmallRpl];
 #pragma unroll
-        for (int h = 0; h < 2; h++) {
+        for (int h = 0; h < kSmallRpl; h++) {
             bin[h] = r[h] >= 0 ? D.Xb[(size_t)r[h] * D.F + f] : -1;
             if (bin[h] >= 0) {
                 atomicAdd((unsigned long long *)&cw[bin[h]], (unsigned long long)((1ull << 32) | w[h]));
@@ -600,7 +605,7 @@ __global__ void __launch_bounds__(128) k5_split_small(RfTrainData D, const RfTas
         if (better(b.proxy, b.feat, b.bin, best)) best = b;
         __syncwarp();
 #pragma unroll
-        for (int h = 0; h < 2; h++)
+        for (int h = 0; h < kSmallRpl; h++)
             if (bin[h] >= 0) {
                 cw[bin[h]] = 0;
                 hsw[bin[h]] = 0;

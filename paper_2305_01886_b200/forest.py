@@ -30,7 +30,7 @@ import numpy as np
 from .ensemble import NODE_DT, FlatEnsemble
 
 N_BINS = 256
-SMALL, MEDIUM = 64, 32768
+SMALL, MEDIUM = 64, 32768  # SMALL = 32 x GK_SMALL_RPL of gk_rftrain.cu (128 / 256 measured slower)
 TASK_DT = np.dtype([("tree", "<i4"), ("begin", "<i4"), ("end", "<i4"), ("parity", "<i4")])
 SPLIT_DT = np.dtype({"names": ["feat", "bin", "n_left", "pad", "proxy"],
                      "formats": ["<i4", "<i4", "<i4", "<i4", "<f8"],
