@@ -182,6 +182,41 @@ __device__ __forceinline__ bool better(double p, int f, int b, const BestSplit &
 // proxy's two fp64 divisions were a quarter of the split search's
 // instructions when every one of a lane's 8 bin slots took them; sparse
 // histograms now compact their candidates first.
+// A histogram bin as four 32-bit words: row count, bootstrap weight, and the
+// fixed-point sum of w * y split into low / high words.  B200 has no native
+// 64-bit shared-memory atomic add (ATOMS.CAST.SPIN.64 CAS loops were 60 % of
+// the node-split instructions); 32-bit adds are native, and the carry out of
+// the low word is recovered from the returned old value -- exact.
+struct BinsRef {
+    uint32_t *cnt, *wgt, *slo;
+    int32_t *shi;
+    __device__ __forceinline__ uint64_t cw(int b) const {
+        return ((uint64_t)cnt[b] << 32) | wgt[b];
+    }
+    __device__ __forceinline__ int64_t sum(int b) const {
+        return (int64_t)(((uint64_t)(uint32_t)shi[b] << 32) + slo[b]);
+    }
+    __device__ __forceinline__ void add(int b, uint32_t w, int64_t sv) const {
+        atomicAdd(cnt + b, 1u);
+        atomicAdd(wgt + b, w);
+        const uint32_t lo = (uint32_t)sv;
+        const uint32_t old = atomicAdd(slo + b, lo);
+        atomicAdd(shi + b, (int32_t)(sv >> 32) + (old + lo < old ? 1 : 0));
+    }
+    __device__ __forceinline__ void clear(int b) const {
+        cnt[b] = 0;
+        wgt[b] = 0;
+        slo[b] = 0;
+        shi[b] = 0;
+    }
+    __device__ __forceinline__ void set(int b, uint64_t c, int64_t sv) const {
+        cnt[b] = (uint32_t)(c >> 32);
+        wgt[b] = (uint32_t)c;
+        slo[b] = (uint32_t)sv;
+        shi[b] = (int32_t)(sv >> 32);
+    }
+};
+
 struct CandSmem {  // one warp's compacted split candidates (<= 64)
     uint64_t c[64];
     int64_t s[64];
@@ -189,16 +224,16 @@ struct CandSmem {  // one warp's compacted split candidates (<= 64)
 };
 
 template <bool kCompact>
-__device__ __forceinline__ BestSplit eval_feature(const uint64_t *cw, const int64_t *s, int f,
-                                                  int lane, CandSmem *cc) {
+__device__ __forceinline__ BestSplit eval_feature(const BinsRef &H, int f, int lane,
+                                                  CandSmem *cc) {
     uint64_t c8[8];
     int64_t s8[8];
     uint64_t cacc = 0;
     int64_t sacc = 0;
 #pragma unroll
     for (int j = 0; j < 8; j++) {
-        cacc += cw[lane * 8 + j];
-        sacc += s[lane * 8 + j];
+        cacc += H.cw(lane * 8 + j);
+        sacc += H.sum(lane * 8 + j);
         c8[j] = cacc;
         s8[j] = sacc;
     }
@@ -295,10 +330,15 @@ __device__ __forceinline__ void finish_split(const BestSplit &b, double parent, 
 }
 
 struct HistSmem {
-    uint64_t cw[kFC][kBins];   // (count << 32) | weight
-    int64_t s[kFC][kBins];     // sum of w * y (fixed point)
+    uint32_t cnt[kFC][kBins];  // rows
+    uint32_t wgt[kFC][kBins];  // bootstrap weight
+    uint32_t slo[kFC][kBins];  // sum of w * y (fixed point), low word
+    int32_t shi[kFC][kBins];   //   high word (BinsRef)
     BestSplit best[8];
     double parent;
+    __device__ __forceinline__ BinsRef feat(int j) {
+        return BinsRef{cnt[j], wgt[j], slo[j], shi[j]};
+    }
 };
 
 // add one task's rows [p0, p1) to the shared histograms of feature chunk fc
@@ -310,24 +350,15 @@ __device__ __forceinline__ void accumulate(HistSmem &H, const RfTrainData &D, co
     for (int p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
         const int32_t r = rows[p];
         const uint32_t w = cnt[r];
-        const uint64_t cw = (1ull << 32) | w;
         const int64_t sv = (int64_t)w * D.yfp[r];
         const uint8_t *xb = D.Xb + (size_t)r * D.F + f0;
-        for (int j = 0; j < nf; j++) {
-            const int b = xb[j];
-            atomicAdd((unsigned long long *)&H.cw[j][b], (unsigned long long)cw);
-            atomicAdd((unsigned long long *)&H.s[j][b], (unsigned long long)sv);
-        }
+        for (int j = 0; j < nf; j++) H.feat(j).add(xb[j], w, sv);
     }
 }
 
 __device__ __forceinline__ void zero_hist(HistSmem &H) {
-    uint64_t *a = &H.cw[0][0];
-    int64_t *b = &H.s[0][0];
-    for (int i = threadIdx.x; i < kFC * kBins; i += blockDim.x) {
-        a[i] = 0;
-        b[i] = 0;
-    }
+    uint4 *a = reinterpret_cast<uint4 *>(&H.cnt[0][0]);  // the four word arrays are contiguous
+    for (int i = threadIdx.x; i < kFC * kBins; i += blockDim.x) a[i] = make_uint4(0, 0, 0, 0);
 }
 
 // evaluate the kFC features in shared memory; fold into H.best[warp]
@@ -337,7 +368,7 @@ __device__ __forceinline__ void eval_chunk(HistSmem &H, int F, int fc, BestSplit
         const int f = fc * kFC + j;
         if (f >= F) break;
         // measured: compaction costs the CTA-per-node path more than it saves
-        const BestSplit b = eval_feature<false>(H.cw[j], H.s[j], f, lane, nullptr);
+        const BestSplit b = eval_feature<false>(H.feat(j), f, lane, nullptr);
         if (better(b.proxy, b.feat, b.bin, mine)) mine = b;
     }
 }
@@ -359,9 +390,10 @@ __device__ __forceinline__ void parent_proxy(HistSmem &H) {
     if (threadIdx.x < 32) {
         uint64_t c = 0;
         int64_t s = 0;
+        const BinsRef f0 = H.feat(0);
         for (int b = threadIdx.x; b < kBins; b += 32) {
-            c += H.cw[0][b];
-            s += H.s[0][b];
+            c += f0.cw(b);
+            s += f0.sum(b);
         }
 #pragma unroll
         for (int o = 16; o; o >>= 1) {
@@ -424,10 +456,12 @@ __global__ void __launch_bounds__(256) k5_hist_big(RfTrainData D, const RfTask *
     uint64_t *dcw = gcw + ((size_t)bi * D.F + f0) * kBins;
     int64_t *ds = gs + ((size_t)bi * D.F + f0) * kBins;
     for (int i = threadIdx.x; i < nf * kBins; i += blockDim.x) {
-        const uint64_t c = (&H.cw[0][0])[i];
+        const BinsRef hb = H.feat(i / kBins);
+        const int b = i % kBins;
+        const uint64_t c = hb.cw(b);
         if (c) {
             atomicAdd((unsigned long long *)(dcw + i), (unsigned long long)c);
-            atomicAdd((unsigned long long *)(ds + i), (unsigned long long)(&H.s[0][0])[i]);
+            atomicAdd((unsigned long long *)(ds + i), (unsigned long long)hb.sum(b));
         }
     }
 }
@@ -445,10 +479,9 @@ __global__ void __launch_bounds__(256) k5_eval_big(RfTrainData D, const int32_t 
         const int f0 = fc * kFC, nf = min(kFC, D.F - f0);
         const uint64_t *scw = gcw + ((size_t)bi * D.F + f0) * kBins;
         const int64_t *ss = gs + ((size_t)bi * D.F + f0) * kBins;
-        for (int i = threadIdx.x; i < kFC * kBins; i += blockDim.x) {
-            (&H.cw[0][0])[i] = i < nf * kBins ? scw[i] : 0;
-            (&H.s[0][0])[i] = i < nf * kBins ? ss[i] : 0;
-        }
+        for (int i = threadIdx.x; i < kFC * kBins; i += blockDim.x)
+            H.feat(i / kBins).set(i % kBins, i < nf * kBins ? scw[i] : 0,
+                                  i < nf * kBins ? ss[i] : 0);
         __syncthreads();
         if (fc == 0) parent_proxy(H);
         eval_chunk(H, D.F, fc, mine);
@@ -577,39 +610,30 @@ __global__ void __launch_bounds__(128) k5_split_small(RfTrainData D, const RfTas
     const double parent = (double)S * (double)S / (double)W;
     // per-warp 256-bin histogram, one feature at a time, evaluated by the same
     // boundary scan as the larger nodes
-    __shared__ uint64_t hcw[4][kBins];
-    __shared__ int64_t hs[4][kBins];
+    __shared__ uint32_t hcnt[4][kBins], hwgt[4][kBins], hslo[4][kBins];
+    __shared__ int32_t hshi[4][kBins];
     __shared__ CandSmem hcand[4];
-    uint64_t *cw = hcw[threadIdx.x >> 5];
-    int64_t *hsw = hs[threadIdx.x >> 5];
+    const int wib = threadIdx.x >> 5;
+    const BinsRef hb{hcnt[wib], hwgt[wib], hslo[wib], hshi[wib]};
     BestSplit best{-1.0, 0x7fffffff, 0x7fffffff, 0};
     // zero once; after each feature every lane clears only the bins it filled
 #pragma unroll
-    for (int j = 0; j < kBins / 32; j++) {
-        cw[lane + 32 * j] = 0;
-        hsw[lane + 32 * j] = 0;
-    }
+    for (int j = 0; j < kBins / 32; j++) hb.clear(lane + 32 * j);
     __syncwarp();
     for (int f = 0; f < D.F; f++) {
         int bin[kSmallRpl];
 #pragma unroll
         for (int h = 0; h < kSmallRpl; h++) {
             bin[h] = r[h] >= 0 ? D.Xb[(size_t)r[h] * D.F + f] : -1;
-            if (bin[h] >= 0) {
-                atomicAdd((unsigned long long *)&cw[bin[h]], (unsigned long long)((1ull << 32) | w[h]));
-                atomicAdd((unsigned long long *)&hsw[bin[h]], (unsigned long long)s[h]);
-            }
+            if (bin[h] >= 0) hb.add(bin[h], w[h], s[h]);
         }
         __syncwarp();
-        const BestSplit b = eval_feature<true>(cw, hsw, f, lane, &hcand[threadIdx.x >> 5]);
+        const BestSplit b = eval_feature<true>(hb, f, lane, &hcand[wib]);
         if (better(b.proxy, b.feat, b.bin, best)) best = b;
         __syncwarp();
 #pragma unroll
         for (int h = 0; h < kSmallRpl; h++)
-            if (bin[h] >= 0) {
-                cw[bin[h]] = 0;
-                hsw[bin[h]] = 0;
-            }
+            if (bin[h] >= 0) hb.clear(bin[h]);
         __syncwarp();
     }
 #pragma unroll
