@@ -290,6 +290,30 @@ int gk_rf_partition(const uint8_t *Xb, const int64_t *yfp, const double *y,
                     int32_t n_tasks, const void *split, const int32_t *ids, int32_t n_ids,
                     int32_t max_rows, int32_t *rows0, int32_t *rows1, int32_t *cursor,
                     void *stream);
+/* The level loop's bookkeeping on the device (replaces the per-level host
+ * bookkeeping of the tree builder; sklearn's BestFirst/DepthFirst builders,
+ * SK/tree/_tree.pyx, grow node by node).  From one level's tasks (sorted by
+ * tree), node ids and splits: split task i gets children at 2*excl[i] and
+ * 2*excl[i]+1 of tasks_next / node_next (excl = split tasks before i) with BFS
+ * ids lid = next_id[tree] + 2*(rank among the tree's split tasks), written to
+ * lid_out[i] (-1 when task i is a leaf); next_id advances; children with >= 2
+ * rows below max_depth are appended to lists[0 / 1 / 2 x list_cap] (small /
+ * medium / big search lists, any order).  stats (int32[8], device): next-level
+ * task count, the three list lengths, largest medium / big child.  scratch:
+ * gk_rf_level_scratch_bytes. */
+size_t gk_rf_level_scratch_bytes(int32_t n_tasks, int32_t n_trees);
+int gk_rf_next_level(const void *tasks, const int32_t *node, const void *split, int32_t n_tasks,
+                     int32_t n_trees, int32_t child_depth, int32_t max_depth, int32_t *next_id,
+                     int32_t *lid_out, void *tasks_next, int32_t *node_next, int32_t *lists,
+                     int32_t list_cap, int32_t *stats, void *scratch, void *stream);
+/* gk_rf_partition over a level's three search lists (searched tasks that stayed
+ * leaves are skipped); cursor: 2 * n_tasks int32, zeroed here */
+int gk_rf_partition_lists(const uint8_t *Xb, const uint32_t *counts, int64_t n_rows,
+                          int32_t n_feat, const void *tasks, int32_t n_tasks, const void *split,
+                          const int32_t *small_ids, int32_t n_small, const int32_t *med_ids,
+                          int32_t n_med, int32_t max_med, const int32_t *big_ids, int32_t n_big,
+                          int32_t max_big, int32_t *rows0, int32_t *rows1, int32_t *cursor,
+                          void *stream);
 /* per leaf segment: int64 {n, sum w, sum w*yfp, sum w*y2fp} (exact fixed-point
  * sums); max_leaf_rows (the largest segment) sizes the row-chunk grid */
 int gk_rf_leaf_stats(const uint32_t *counts, int64_t n_rows, const int64_t *yfp,

@@ -664,6 +664,7 @@ __global__ void __launch_bounds__(256) k5_partition(RfTrainData D, const RfTask 
     const RfTask T = tasks[ti];
     if (T.begin + (int)(blockIdx.y * blockDim.x) >= T.end) return;  // whole CTA past the node
     const RfSplit sp = split[ti];
+    if (sp.feat < 0) return;  // searched but kept as a leaf
     const int32_t *in = T.parity ? rows1 : rows0;
     int32_t *outp = T.parity ? rows0_out1 : rows1_out0;
     const int p = T.begin + blockIdx.y * blockDim.x + threadIdx.x;
@@ -683,6 +684,152 @@ __global__ void __launch_bounds__(256) k5_partition(RfTrainData D, const RfTask 
     const unsigned below = (1u << lane) - 1u;
     if (left) outp[T.begin + lb + __popc(bl & below)] = r;
     if (right) outp[T.begin + sp.n_left + rb + __popc(br & below)] = r;
+}
+
+// ---------------------------------------------------------------- next level
+//
+// Level bookkeeping on the device (it was numpy on the host, ~3/4 of a fit's
+// wall time).  Tasks of a level are sorted by tree.  A split task i gets its
+// children at 2 * excl[i], 2 * excl[i] + 1 of the next level (excl = number of
+// split tasks before i: task order, as the host did) and the BFS ids
+// lid = next_id[tree] + 2 * (rank of i among its tree's split tasks), i.e.
+// lid_base[tree] + 2 * excl[i] with lid_base = next_id - 2 * (splits of the
+// earlier trees).  Children are classified for the next level's split search
+// (small / medium / big lists; a child with < 2 rows or at max depth is in no
+// list and stays a leaf).  The lists are appended with warp-aggregated
+// atomics, so their order varies from run to run; every kernel that reads them
+// writes per-task results, so trees do not.
+constexpr int kLvlThreads = 256;
+constexpr int kSmallRows = 32 * kSmallRpl;  // host forest.SMALL
+
+enum : int {  // stats[] slots (int32)
+    kStNext = 0, kStSmall = 1, kStMed = 2, kStBig = 3, kStMaxMed = 4, kStMaxBig = 5
+};
+
+__global__ void __launch_bounds__(kLvlThreads) k5_level_count(const RfTask *__restrict__ tasks,
+                                                              const RfSplit *__restrict__ split,
+                                                              int n_tasks,
+                                                              int32_t *__restrict__ block_cnt,
+                                                              int32_t *__restrict__ tree_cnt) {
+    const int i = blockIdx.x * kLvlThreads + threadIdx.x;
+    const bool s = i < n_tasks && split[i].feat >= 0;
+    const int c = __syncthreads_count(s);
+    if (threadIdx.x == 0) block_cnt[blockIdx.x] = c;
+    const int tree = s ? tasks[i].tree : -1;
+    const unsigned act = __ballot_sync(GK_FULL, s);
+    if (s) {
+        const unsigned peers = __match_any_sync(act, tree);
+        if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(tree_cnt + tree, __popc(peers));
+    }
+}
+
+// one CTA: exclusive scans of the per-block and per-tree split counts
+__global__ void __launch_bounds__(1024) k5_level_scan(int32_t *__restrict__ block_cnt, int n_blocks,
+                                                      const int32_t *__restrict__ tree_cnt,
+                                                      int n_trees, int32_t *__restrict__ next_id,
+                                                      int32_t *__restrict__ lid_base,
+                                                      int32_t *__restrict__ stats) {
+    __shared__ int32_t wsum[32];
+    __shared__ int32_t carry;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    auto scan = [&](const int32_t *a, int n, auto &&emit) {
+        if (threadIdx.x == 0) carry = 0;
+        __syncthreads();
+        for (int b0 = 0; b0 < n; b0 += 1024) {
+            const int i = b0 + threadIdx.x;
+            const int32_t v = i < n ? a[i] : 0;
+            int32_t x = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int32_t y = __shfl_up_sync(GK_FULL, x, o);
+                if (lane >= o) x += y;
+            }
+            if (lane == 31) wsum[warp] = x;
+            __syncthreads();
+            if (warp == 0) {
+                int32_t w = wsum[lane];
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int32_t y = __shfl_up_sync(GK_FULL, w, o);
+                    if (lane >= o) w += y;
+                }
+                wsum[lane] = w;  // inclusive over warps
+            }
+            __syncthreads();
+            const int32_t excl = carry + (warp ? wsum[warp - 1] : 0) + x - v;
+            if (i < n) emit(i, excl, v);
+            __syncthreads();
+            if (threadIdx.x == 0) carry += wsum[31];
+            __syncthreads();
+        }
+    };
+    scan(block_cnt, n_blocks, [&](int i, int32_t excl, int32_t) { block_cnt[i] = excl; });
+    if (threadIdx.x == 0) stats[kStNext] = 2 * carry;
+    __syncthreads();
+    scan(tree_cnt, n_trees, [&](int t, int32_t excl, int32_t v) {
+        lid_base[t] = next_id[t] - 2 * excl;
+        next_id[t] += 2 * v;
+    });
+}
+
+__device__ __forceinline__ void append_class(int cls, int k, int32_t *__restrict__ lists, int cap,
+                                             int32_t *__restrict__ stats, int size) {
+    // warp-aggregated appends: one atomic per (warp, class); every lane calls
+#pragma unroll
+    for (int c = 0; c < 3; c++) {
+        const unsigned m = __ballot_sync(GK_FULL, cls == c);
+        if (!m) continue;
+        const int lane = threadIdx.x & 31;
+        const int leader = __ffs(m) - 1;
+        int base = 0;
+        if (lane == leader) base = atomicAdd(stats + kStSmall + c, __popc(m));
+        base = __shfl_sync(GK_FULL, base, leader);
+        if (cls == c) lists[c * cap + base + __popc(m & ((1u << lane) - 1u))] = k;
+    }
+    if (cls == 1) atomicMax(stats + kStMaxMed, size);
+    if (cls == 2) atomicMax(stats + kStMaxBig, size);
+}
+
+__global__ void __launch_bounds__(kLvlThreads) k5_level_emit(
+    const RfTask *__restrict__ tasks, const int32_t *__restrict__ node,
+    const RfSplit *__restrict__ split, int n_tasks, const int32_t *__restrict__ block_excl,
+    const int32_t *__restrict__ lid_base, int child_depth, int max_depth,
+    int32_t *__restrict__ lid_out, RfTask *__restrict__ tasks_next,
+    int32_t *__restrict__ node_next, int32_t *__restrict__ lists, int cap,
+    int32_t *__restrict__ stats) {
+    __shared__ int32_t wsum[kLvlThreads / 32];
+    const int i = blockIdx.x * kLvlThreads + threadIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const bool valid = i < n_tasks;
+    const RfSplit sp = valid ? split[i] : RfSplit{-1, 0, 0, 0, 0.0};
+    const bool s = sp.feat >= 0;
+    const unsigned bal = __ballot_sync(GK_FULL, s);
+    if (lane == 0) wsum[warp] = __popc(bal);
+    __syncthreads();
+    int before = 0;
+#pragma unroll
+    for (int w = 0; w < kLvlThreads / 32; w++) before += w < warp ? wsum[w] : 0;
+    const int excl = block_excl[blockIdx.x] + before + __popc(bal & ((1u << lane) - 1u));
+    int cls_l = -1, cls_r = -1, sz_l = 0, sz_r = 0;
+    if (s) {
+        const RfTask T = tasks[i];
+        const int32_t lid = lid_base[T.tree] + 2 * excl;
+        lid_out[i] = lid;
+        const int mid = T.begin + sp.n_left;
+        tasks_next[2 * excl] = RfTask{T.tree, T.begin, mid, 1 - T.parity};
+        tasks_next[2 * excl + 1] = RfTask{T.tree, mid, T.end, 1 - T.parity};
+        node_next[2 * excl] = lid;
+        node_next[2 * excl + 1] = lid + 1;
+        sz_l = sp.n_left;
+        sz_r = T.end - mid;
+        const bool deep_ok = child_depth < max_depth;
+        cls_l = (deep_ok && sz_l >= 2) ? (sz_l > kSmallRows) + (sz_l > kMedRows) : -1;
+        cls_r = (deep_ok && sz_r >= 2) ? (sz_r > kSmallRows) + (sz_r > kMedRows) : -1;
+    } else if (valid) {
+        lid_out[i] = -1;
+    }
+    append_class(cls_l, 2 * excl, lists, cap, stats, sz_l);
+    append_class(cls_r, 2 * excl + 1, lists, cap, stats, sz_r);
 }
 
 // ---------------------------------------------------------------- leaf stats
@@ -859,6 +1006,72 @@ int gk_rf_partition(const uint8_t *Xb, const int64_t *yfp, const double *y,
     gk::k5_partition<<<grid, 256, 0, st>>>(D, (const gk::RfTask *)tasks, (const gk::RfSplit *)split,
                                            ids, rows0, rows1, rows1, rows0, cursor);
     return gk_check_launch("k5_partition");
+}
+
+// Next level of a tree batch from this level's tasks and splits (device-side
+// bookkeeping, see k5_level_emit).  stats[8] (int32): [0] next-level task
+// count, [1..3] small / medium / big list lengths, [4] / [5] largest medium /
+// big task; lists = 3 regions of list_cap (>= 2 * n_tasks) entries.
+size_t gk_rf_level_scratch_bytes(int32_t n_tasks, int32_t n_trees) {
+    const size_t nb = ((size_t)n_tasks + gk::kLvlThreads - 1) / gk::kLvlThreads;
+    return sizeof(int32_t) * (nb + 2 * (size_t)n_trees + 8);
+}
+
+int gk_rf_next_level(const void *tasks, const int32_t *node, const void *split, int32_t n_tasks,
+                     int32_t n_trees, int32_t child_depth, int32_t max_depth, int32_t *next_id,
+                     int32_t *lid_out, void *tasks_next, int32_t *node_next, int32_t *lists,
+                     int32_t list_cap, int32_t *stats, void *scratch, void *stream) {
+    if (n_tasks < 0 || n_trees < 1 || list_cap < 2 * (int64_t)n_tasks) {
+        gk_set_error("gk_rf_next_level: bad sizes (n_tasks %d, n_trees %d, list_cap %d)", n_tasks,
+                     n_trees, list_cap);
+        return -1;
+    }
+    const cudaStream_t st = (cudaStream_t)stream;
+    const int nb = (n_tasks + gk::kLvlThreads - 1) / gk::kLvlThreads;
+    int32_t *block_cnt = (int32_t *)scratch;
+    int32_t *tree_cnt = block_cnt + nb;
+    int32_t *lid_base = tree_cnt + n_trees;
+    cudaMemsetAsync(stats, 0, 8 * sizeof(int32_t), st);
+    cudaMemsetAsync(tree_cnt, 0, sizeof(int32_t) * n_trees, st);
+    if (nb == 0) return gk_check_launch("k5_next_level");
+    const gk::RfTask *T = (const gk::RfTask *)tasks;
+    const gk::RfSplit *S = (const gk::RfSplit *)split;
+    gk::k5_level_count<<<nb, gk::kLvlThreads, 0, st>>>(T, S, n_tasks, block_cnt, tree_cnt);
+    gk::k5_level_scan<<<1, 1024, 0, st>>>(block_cnt, nb, tree_cnt, n_trees, next_id, lid_base, stats);
+    gk::k5_level_emit<<<nb, gk::kLvlThreads, 0, st>>>(T, node, S, n_tasks, block_cnt, lid_base,
+                                                       child_depth, max_depth, lid_out,
+                                                       (gk::RfTask *)tasks_next, node_next, lists,
+                                                       list_cap, stats);
+    return gk_check_launch("k5_next_level");
+}
+
+// gk_rf_partition over the three search lists of a level (cursor: 2 * n_tasks,
+// zeroed here once); tasks whose search kept them a leaf are skipped
+int gk_rf_partition_lists(const uint8_t *Xb, const uint32_t *counts, int64_t n_rows,
+                          int32_t n_feat, const void *tasks, int32_t n_tasks, const void *split,
+                          const int32_t *small_ids, int32_t n_small, const int32_t *med_ids,
+                          int32_t n_med, int32_t max_med, const int32_t *big_ids, int32_t n_big,
+                          int32_t max_big, int32_t *rows0, int32_t *rows1, int32_t *cursor,
+                          void *stream) {
+    const cudaStream_t st = (cudaStream_t)stream;
+    gk::RfTrainData D{Xb, nullptr, nullptr, counts, n_rows, n_feat};
+    cudaMemsetAsync(cursor, 0, sizeof(int32_t) * 2 * (size_t)n_tasks, st);
+    const int32_t *ids[3] = {small_ids, med_ids, big_ids};
+    const int32_t nid[3] = {n_small, n_med, n_big};
+    const int32_t mx[3] = {gk::kSmallRows, max_med, max_big};
+    for (int c = 0; c < 3; c++) {
+        if (nid[c] <= 0) continue;
+        const int64_t chunks = ((int64_t)mx[c] + 255) / 256;
+        if (chunks < 1 || chunks > 65535) {
+            gk_set_error("gk_rf_partition_lists: node of %d rows out of the chunk grid", mx[c]);
+            return -1;
+        }
+        dim3 grid((unsigned)nid[c], (unsigned)chunks);
+        gk::k5_partition<<<grid, 256, 0, st>>>(D, (const gk::RfTask *)tasks,
+                                               (const gk::RfSplit *)split, ids[c], rows0, rows1,
+                                               rows1, rows0, cursor);
+    }
+    return gk_check_launch("k5_partition_lists");
 }
 
 int gk_rf_leaf_stats(const uint32_t *counts, int64_t n_rows, const int64_t *yfp,

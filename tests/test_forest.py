@@ -152,3 +152,44 @@ def test_unbounded_depth_forest_matches_sklearn_quality():
         return 1 - np.mean((p - y[te]) ** 2) / np.var(y[te])
 
     assert abs(r2(ours.predict(X[te])) - r2(sk.predict(X[te]))) < 0.01
+
+
+def _tree_arrays(t):
+    return (t.node_count, t.children_left, t.children_right, t.feature, t.threshold, t.value,
+            t.impurity, t.n_node_samples, t.weighted_n_node_samples, t.max_depth)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("rows,depth,trees", [(120_000, None, 6), (3_000, 5, 40)])
+def test_device_level_bookkeeping_equals_host_form(monkeypatch, rows, depth, trees):
+    """gk_rf_next_level (device bookkeeping) grows the same trees, node for node,
+    as the numpy level loop it replaced (GK_RF_HOST_LEVELS=1): big (> 32768
+    rows), medium, small and tiny tasks, unbounded depth and a depth cap."""
+    from paper_2305_01886_b200.forest import RandomForestRegressor
+
+    rng = np.random.default_rng(7)
+    X = rng.random((rows, 12))
+    X[:, 9:] = np.floor(X[:, 9:] * 5)
+    y = 3 * X[:, 0] + np.sin(6 * X[:, 1]) + (X[:, 9] > 2) + rng.normal(0, 0.1, rows)
+    got = RandomForestRegressor(trees, max_depth=depth, random_state=11).fit(X, y)
+    monkeypatch.setenv("GK_RF_HOST_LEVELS", "1")
+    want = RandomForestRegressor(trees, max_depth=depth, random_state=11).fit(X, y)
+    for a, b in zip(got.estimators_, want.estimators_):
+        for u, v in zip(_tree_arrays(a.tree_), _tree_arrays(b.tree_)):
+            assert np.array_equal(u, v)
+
+
+@pytest.mark.gpu
+def test_device_level_bookkeeping_equals_host_form_gbt(monkeypatch):
+    from paper_2305_01886_b200.boosting import GradientBoostingRegressor
+
+    rng = np.random.default_rng(8)
+    X = rng.random((50_000, 10))
+    y = 5 * X[:, 0] - 2 * X[:, 3] ** 2 + rng.normal(0, 0.05, 50_000)
+    got = GradientBoostingRegressor(12, learning_rate=0.1, max_depth=4, random_state=0).fit(X, y)
+    monkeypatch.setenv("GK_RF_HOST_LEVELS", "1")
+    want = GradientBoostingRegressor(12, learning_rate=0.1, max_depth=4, random_state=0).fit(X, y)
+    for (a,), (b,) in zip(got.estimators_, want.estimators_):
+        for u, v in zip(_tree_arrays(a.tree_), _tree_arrays(b.tree_)):
+            assert np.array_equal(u, v)
+    np.testing.assert_array_equal(got.predict(X[:1000]), want.predict(X[:1000]))
