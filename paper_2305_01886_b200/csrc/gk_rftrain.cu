@@ -305,6 +305,12 @@ __device__ __forceinline__ BestSplit eval_feature(const BinsRef &H, int f, int l
             if (better(p, f, b, best)) best = BestSplit{p, f, b, CL};
         }
     }
+    // this lane's best only: callers fold lanes across features and reduce the
+    // warp once per task (better() is a total order, so the result is the same)
+    return best;
+}
+
+__device__ __forceinline__ BestSplit warp_best(BestSplit best) {
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
         BestSplit q;
@@ -375,6 +381,7 @@ __device__ __forceinline__ void eval_chunk(HistSmem &H, int F, int fc, BestSplit
 
 __device__ __forceinline__ void reduce_best(HistSmem &H, BestSplit mine, RfSplit *out) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    mine = warp_best(mine);
     if (lane == 0) H.best[warp] = mine;
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -408,7 +415,10 @@ __device__ __forceinline__ void parent_proxy(HistSmem &H) {
 }
 
 // medium tasks: one CTA per task, feature chunks in sequence
-__global__ void __launch_bounds__(256) k5_split_medium(RfTrainData D, const RfTask *__restrict__ tasks,
+#ifndef GK_MED_MINB
+#define GK_MED_MINB 3  // resident CTAs per SM of the medium path (64 KB histograms each)
+#endif
+__global__ void __launch_bounds__(256, GK_MED_MINB) k5_split_medium(RfTrainData D, const RfTask *__restrict__ tasks,
                                                        const int32_t *__restrict__ task_ids,
                                                        const int32_t *__restrict__ rows0,
                                                        const int32_t *__restrict__ rows1,
@@ -568,7 +578,10 @@ __device__ __forceinline__ void split_tiny(const RfTrainData &D, const RfTask &T
 
 // small tasks (<= 64 rows): one warp; tiny ones (<= kTiny rows) lane-per-
 // feature (split_tiny), the rest through per-warp 256-bin histograms
-__global__ void __launch_bounds__(128) k5_split_small(RfTrainData D, const RfTask *__restrict__ tasks,
+#ifndef GK_SMALL_MINB
+#define GK_SMALL_MINB 6  // resident CTAs per SM of the warp-per-node path
+#endif
+__global__ void __launch_bounds__(128, GK_SMALL_MINB) k5_split_small(RfTrainData D, const RfTask *__restrict__ tasks,
                                                      const int32_t *__restrict__ task_ids,
                                                      int n_ids, const int32_t *__restrict__ rows0,
                                                      const int32_t *__restrict__ rows1,
@@ -636,15 +649,7 @@ __global__ void __launch_bounds__(128) k5_split_small(RfTrainData D, const RfTas
             if (bin[h] >= 0) hb.clear(bin[h]);
         __syncwarp();
     }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        BestSplit q;
-        q.proxy = __shfl_xor_sync(GK_FULL, best.proxy, o);
-        q.feat = __shfl_xor_sync(GK_FULL, best.feat, o);
-        q.bin = __shfl_xor_sync(GK_FULL, best.bin, o);
-        q.n_left = __shfl_xor_sync(GK_FULL, best.n_left, o);
-        if (better(q.proxy, q.feat, q.bin, best)) best = q;
-    }
+    best = warp_best(best);
     if (lane == 0) finish_split(best, parent, out + ti);
 }
 
@@ -961,6 +966,8 @@ int gk_rf_split_level(const uint8_t *Xb, const int64_t *yfp, const double *y,
     const size_t smem = sizeof(gk::HistSmem);
     static const bool attr = [smem] {  // thread-safe one-time init (concurrent tree batches)
         cudaFuncSetAttribute(gk::k5_split_medium, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(gk::k5_split_medium, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared);
         cudaFuncSetAttribute(gk::k5_hist_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(gk::k5_eval_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         return true;

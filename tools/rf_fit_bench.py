@@ -33,6 +33,7 @@ def main():
     ap.add_argument("--batch", type=int, default=32)
     ap.add_argument("--profile", action="store_true")
     ap.add_argument("--streams", type=int, default=2)
+    ap.add_argument("--repeat", type=int, default=1)
     a = ap.parse_args()
     import torch
 
@@ -48,11 +49,14 @@ def main():
 
         prof = cProfile.Profile()
         prof.enable()
-    t0 = time.perf_counter()
-    m = RandomForestRegressor(a.trees, max_depth=a.depth, random_state=0,
-                              trees_per_batch=a.batch, streams=a.streams).fit(Xs, y)
-    torch.cuda.synchronize()
-    dt = time.perf_counter() - t0
+    for _ in range(a.repeat):
+        t0 = time.perf_counter()
+        m = RandomForestRegressor(a.trees, max_depth=a.depth, random_state=0,
+                                  trees_per_batch=a.batch, streams=a.streams).fit(Xs, y)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        if a.repeat > 1:
+            print(f"fit {dt:.3f} s ({a.trees} trees, batch {a.batch}, streams {a.streams})")
     if prof is not None:
         import pstats
 
