@@ -512,6 +512,9 @@ constexpr int kTiny = 16;
 #define GK_SMALL_RPL 2  // rows per lane of the warp-per-node path (host SMALL = 32 x this)
 #endif
 constexpr int kSmallRpl = GK_SMALL_RPL;
+#ifndef GK_SMALL_RANK
+#define GK_SMALL_RANK 1  // warp-per-node path: rank-compacted bins (0: 256-bin scan)
+#endif
 
 __device__ __forceinline__ void split_tiny(const RfTrainData &D, const RfTask &T,
                                            const int32_t *__restrict__ rows, int m, int lane,
@@ -621,14 +624,108 @@ __global__ void __launch_bounds__(128, GK_SMALL_MINB) k5_split_small(RfTrainData
         S += __shfl_xor_sync(GK_FULL, S, o);
     }
     const double parent = (double)S * (double)S / (double)W;
+    const int wib = threadIdx.x >> 5;
+    BestSplit best{-1.0, 0x7fffffff, 0x7fffffff, 0};
+#if GK_SMALL_RANK
+    // Rank-compacted histograms: a node of <= 32 * kE rows has at most that
+    // many distinct bins.  A 256-bit occupancy map gives each present bin its
+    // rank among them, the four-word bins are indexed by rank, and lane l scans
+    // entries [l * kE, (l + 1) * kE) -- kE per lane instead of 8, every entry
+    // non-empty, so entry e is a candidate iff a later entry exists (then its
+    // bin is < 255 and both sides hold rows): the same candidates, proxies and
+    // (proxy, feature, bin) order as the 256-bin scan.
+    constexpr int kE = kSmallRpl;
+    constexpr int kN = 32 * kE;
+    __shared__ uint32_t ccnt[4][kN], cwgt[4][kN], cslo[4][kN];
+    __shared__ int32_t cshi[4][kN];
+    __shared__ uint16_t cbin[4][kN];
+    __shared__ uint32_t bmap[4][8], bpre[4][8];
+    const BinsRef hb{ccnt[wib], cwgt[wib], cslo[wib], cshi[wib]};
+#pragma unroll
+    for (int j = 0; j < kE; j++) hb.clear(lane * kE + j);
+    if (lane < 8) bmap[wib][lane] = 0u;
+    __syncwarp();
+    for (int f = 0; f < D.F; f++) {
+        int bin[kSmallRpl], rk[kSmallRpl];
+#pragma unroll
+        for (int h = 0; h < kSmallRpl; h++) {
+            bin[h] = r[h] >= 0 ? D.Xb[(size_t)r[h] * D.F + f] : -1;
+            if (bin[h] >= 0) atomicOr(&bmap[wib][bin[h] >> 5], 1u << (bin[h] & 31));
+        }
+        __syncwarp();
+        const uint32_t word = lane < 8 ? bmap[wib][lane] : 0u;
+        int pc = __popc(word);
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+            const int a = __shfl_up_sync(GK_FULL, pc, o);
+            if (lane >= o) pc += a;
+        }
+        const int nd = __shfl_sync(GK_FULL, pc, 7);  // distinct bins
+        if (lane < 8) bpre[wib][lane] = (uint32_t)(pc - __popc(word));
+        __syncwarp();
+#pragma unroll
+        for (int h = 0; h < kSmallRpl; h++) {
+            rk[h] = -1;
+            if (bin[h] >= 0) {
+                const int k = bin[h] >> 5;
+                rk[h] = (int)bpre[wib][k] + __popc(bmap[wib][k] & ((1u << (bin[h] & 31)) - 1u));
+                hb.add(rk[h], w[h], s[h]);
+                cbin[wib][rk[h]] = (uint16_t)bin[h];
+            }
+        }
+        __syncwarp();
+        uint64_t c8[kE];
+        int64_t s8[kE];
+        uint64_t cacc = 0;
+        int64_t sacc = 0;
+#pragma unroll
+        for (int j = 0; j < kE; j++) {
+            cacc += hb.cw(lane * kE + j);
+            sacc += hb.sum(lane * kE + j);
+            c8[j] = cacc;
+            s8[j] = sacc;
+        }
+        uint64_t cpre = cacc;
+        int64_t spre = sacc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t a = __shfl_up_sync(GK_FULL, cpre, o);
+            const int64_t b = __shfl_up_sync(GK_FULL, spre, o);
+            if (lane >= o) {
+                cpre += a;
+                spre += b;
+            }
+        }
+        const uint64_t ctot = __shfl_sync(GK_FULL, cpre, 31);
+        const int64_t stot = __shfl_sync(GK_FULL, spre, 31);
+        cpre -= cacc;
+        spre -= sacc;
+        const uint32_t Wt = (uint32_t)ctot;
+#pragma unroll
+        for (int j = 0; j < kE; j++) {
+            const int e = lane * kE + j;
+            if (e >= nd - 1) break;
+            const uint64_t cl = cpre + c8[j];
+            const uint32_t CL = (uint32_t)(cl >> 32), WL = (uint32_t)cl;
+            const double SL = (double)(spre + s8[j]), SR = (double)(stot - spre - s8[j]);
+            const double p = SL * SL / (double)WL + SR * SR / (double)(Wt - WL);
+            const int b = cbin[wib][e];
+            if (better(p, f, b, best)) best = BestSplit{p, f, b, CL};
+        }
+        __syncwarp();
+#pragma unroll
+        for (int h = 0; h < kSmallRpl; h++)
+            if (rk[h] >= 0) hb.clear(rk[h]);
+        if (lane < 8) bmap[wib][lane] = 0u;
+        __syncwarp();
+    }
+#else
     // per-warp 256-bin histogram, one feature at a time, evaluated by the same
     // boundary scan as the larger nodes
     __shared__ uint32_t hcnt[4][kBins], hwgt[4][kBins], hslo[4][kBins];
     __shared__ int32_t hshi[4][kBins];
     __shared__ CandSmem hcand[4];
-    const int wib = threadIdx.x >> 5;
     const BinsRef hb{hcnt[wib], hwgt[wib], hslo[wib], hshi[wib]};
-    BestSplit best{-1.0, 0x7fffffff, 0x7fffffff, 0};
     // zero once; after each feature every lane clears only the bins it filled
 #pragma unroll
     for (int j = 0; j < kBins / 32; j++) hb.clear(lane + 32 * j);
@@ -649,6 +746,7 @@ __global__ void __launch_bounds__(128, GK_SMALL_MINB) k5_split_small(RfTrainData
             if (bin[h] >= 0) hb.clear(bin[h]);
         __syncwarp();
     }
+#endif
     best = warp_best(best);
     if (lane == 0) finish_split(best, parent, out + ti);
 }
