@@ -414,6 +414,176 @@ __device__ __forceinline__ void parent_proxy(HistSmem &H) {
     }
 }
 
+// Medium tasks of <= kMidRows rows: the CTA's rows are staged once in shared
+// memory and each warp owns every 8th feature with its own rank-compacted
+// histogram (as the warp-per-node path, k5_split_small): no block barriers per
+// feature chunk, no 64 KB zeroing, and each entry scanned is a present bin.
+// Same candidates, proxies and (proxy, feature, bin) order as the 256-bin scan.
+#ifndef GK_MID_ROWS
+#define GK_MID_ROWS 256  // 0 disables the path (512 measured no faster than the CTA path)
+#endif
+constexpr int kMidRows = GK_MID_ROWS > 0 ? GK_MID_ROWS : 32;
+constexpr int kMidK = kMidRows / 32;  // rows per lane
+constexpr int kMidXS = 68;  // staged bin row stride (17 words: lanes' rows on distinct banks)
+struct MidSmem {
+    uint8_t xb[kMidRows * kMidXS];  // the node's rows of Xb (F <= 64)
+    int32_t row[kMidRows];
+    uint32_t w[kMidRows];
+    int64_t s[kMidRows];
+    uint32_t cnt[8][kBins], wgt[8][kBins], slo[8][kBins];
+    int32_t shi[8][kBins];
+    uint16_t cbin[8][kBins];
+    uint32_t bmap[8][8], bpre[8][8];
+    BestSplit best[8];
+    unsigned long long W;
+    long long S;
+};
+
+__device__ __noinline__ void split_mid(const RfTrainData &D, const RfTask &T,
+                                       const int32_t *__restrict__ rows, unsigned char *smem,
+                                       RfSplit *out) {
+    MidSmem &M = *reinterpret_cast<MidSmem *>(smem);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int m = T.end - T.begin;
+    const uint32_t *cnt = D.counts + (size_t)T.tree * D.n;
+    if (threadIdx.x == 0) {
+        M.W = 0;
+        M.S = 0;
+    }
+    const BinsRef hb{M.cnt[warp], M.wgt[warp], M.slo[warp], M.shi[warp]};
+#pragma unroll
+    for (int j = 0; j < kBins / 32; j++) hb.clear(lane + 32 * j);
+    if (lane < 8) M.bmap[warp][lane] = 0u;
+    __syncthreads();
+    unsigned long long wsum = 0;
+    long long ssum = 0;
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+        const int32_t r = rows[T.begin + i];
+        const uint32_t w = cnt[r];
+        const int64_t sv = (int64_t)w * D.yfp[r];
+        M.row[i] = r;
+        M.w[i] = w;
+        M.s[i] = sv;
+        wsum += w;
+        ssum += sv;
+    }
+    __syncthreads();
+    // stage the node's bin rows: 4-byte words (rows are 4-byte aligned when
+    // F % 4 == 0), 17-word stride
+    const int fw = (D.F + 3) >> 2;
+    if ((D.F & 3) == 0) {
+        for (int q = threadIdx.x; q < m * fw; q += blockDim.x) {
+            const int i = q / fw, k = q - i * fw;
+            reinterpret_cast<uint32_t *>(M.xb + i * kMidXS)[k] =
+                reinterpret_cast<const uint32_t *>(D.Xb + (size_t)M.row[i] * D.F)[k];
+        }
+    } else {
+        for (int q = threadIdx.x; q < m * D.F; q += blockDim.x) {
+            const int i = q / D.F, k = q - i * D.F;
+            M.xb[i * kMidXS + k] = D.Xb[(size_t)M.row[i] * D.F + k];
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        wsum += __shfl_xor_sync(GK_FULL, wsum, o);
+        ssum += __shfl_xor_sync(GK_FULL, ssum, o);
+    }
+    if (lane == 0) {
+        atomicAdd(&M.W, wsum);
+        atomicAdd(reinterpret_cast<unsigned long long *>(&M.S), (unsigned long long)ssum);
+    }
+    __syncthreads();
+    BestSplit best{-1.0, 0x7fffffff, 0x7fffffff, 0};
+    for (int f = warp; f < D.F; f += 8) {
+        int bin[kMidK];
+#pragma unroll
+        for (int k = 0; k < kMidK; k++) {
+            const int i = lane + 32 * k;
+            bin[k] = i < m ? M.xb[i * kMidXS + f] : -1;
+            if (bin[k] >= 0) atomicOr(&M.bmap[warp][bin[k] >> 5], 1u << (bin[k] & 31));
+        }
+        __syncwarp();
+        const uint32_t word = lane < 8 ? M.bmap[warp][lane] : 0u;
+        int pc = __popc(word);
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+            const int a = __shfl_up_sync(GK_FULL, pc, o);
+            if (lane >= o) pc += a;
+        }
+        const int nd = __shfl_sync(GK_FULL, pc, 7);
+        if (lane < 8) M.bpre[warp][lane] = (uint32_t)(pc - __popc(word));
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < kMidK; k++) {
+            if (bin[k] < 0) continue;
+            const int i = lane + 32 * k;
+            const int q = bin[k] >> 5;
+            const int rk = (int)M.bpre[warp][q] + __popc(M.bmap[warp][q] & ((1u << (bin[k] & 31)) - 1u));
+            hb.add(rk, M.w[i], M.s[i]);
+            M.cbin[warp][rk] = (uint16_t)bin[k];
+        }
+        __syncwarp();
+        const int kE = (nd + 31) >> 5;  // entries per lane (warp-uniform, <= 8)
+        uint64_t c8[8];
+        int64_t s8[8];
+        uint64_t cacc = 0;
+        int64_t sacc = 0;
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            if (j < kE) {
+                cacc += hb.cw(lane * kE + j);
+                sacc += hb.sum(lane * kE + j);
+            }
+            c8[j] = cacc;
+            s8[j] = sacc;
+        }
+        uint64_t cpre = cacc;
+        int64_t spre = sacc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t a = __shfl_up_sync(GK_FULL, cpre, o);
+            const int64_t b = __shfl_up_sync(GK_FULL, spre, o);
+            if (lane >= o) {
+                cpre += a;
+                spre += b;
+            }
+        }
+        const uint64_t ctot = __shfl_sync(GK_FULL, cpre, 31);
+        const int64_t stot = __shfl_sync(GK_FULL, spre, 31);
+        cpre -= cacc;
+        spre -= sacc;
+        const uint32_t Wt = (uint32_t)ctot;
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            const int e = lane * kE + j;
+            if (j >= kE || e >= nd - 1) break;
+            const uint64_t cl = cpre + c8[j];
+            const uint32_t CL = (uint32_t)(cl >> 32), WL = (uint32_t)cl;
+            const double SL = (double)(spre + s8[j]), SR = (double)(stot - spre - s8[j]);
+            const double p = SL * SL / (double)WL + SR * SR / (double)(Wt - WL);
+            const int b = M.cbin[warp][e];
+            if (better(p, f, b, best)) best = BestSplit{p, f, b, CL};
+        }
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 8; j++)
+            if (j < kE && lane * kE + j < nd) hb.clear(lane * kE + j);
+        if (lane < 8) M.bmap[warp][lane] = 0u;
+        __syncwarp();
+    }
+    best = warp_best(best);
+    if (lane == 0) M.best[warp] = best;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        BestSplit b = M.best[0];
+        for (int w = 1; w < (int)(blockDim.x >> 5); w++)
+            if (better(M.best[w].proxy, M.best[w].feat, M.best[w].bin, b)) b = M.best[w];
+        const double S = (double)M.S;
+        finish_split(b, S * S / (double)M.W, out);
+    }
+}
+static_assert(sizeof(MidSmem) <= sizeof(HistSmem), "the mid path reuses the medium smem");
+
 // medium tasks: one CTA per task, feature chunks in sequence
 #ifndef GK_MED_MINB
 #define GK_MED_MINB 3  // resident CTAs per SM of the medium path (64 KB histograms each)
@@ -428,6 +598,10 @@ __global__ void __launch_bounds__(256, GK_MED_MINB) k5_split_medium(RfTrainData 
     const int ti = task_ids[blockIdx.x];
     const RfTask T = tasks[ti];
     const int32_t *rows = T.parity ? rows1 : rows0;
+    if (GK_MID_ROWS > 0 && D.F <= 64 && T.end - T.begin <= kMidRows) {  // CTA-uniform
+        split_mid(D, T, rows, smem_raw, out + ti);
+        return;
+    }
     BestSplit mine{-1.0, 0x7fffffff, 0x7fffffff, 0};
     const int n_fc = (D.F + kFC - 1) / kFC;
     for (int fc = 0; fc < n_fc; fc++) {
