@@ -36,7 +36,9 @@ for layout in ("nodes", "nodes8", "blocks"):
     de = rt.DeviceEnsemble.upload(flat, layout=layout)
     rt.rf_predict(de, torch.tensor(X, device="cuda"))      # K4 (+ compact walks)
 Xf, y = rng.random((3000, 8)), rng.random(3000)
-RandomForestRegressor(5, max_depth=6, random_state=0).fit(Xf, y)   # K5
+RandomForestRegressor(5, max_depth=6, random_state=0).fit(Xf, y)   # K5 (medium / mid / small / tiny)
+Xb, yb = rng.random((60000, 8)), rng.random(60000)
+RandomForestRegressor(2, max_depth=2, random_state=0).fit(Xb, yb)  # K5 big-node path
 GradientBoostingRegressor(5, random_state=0).fit(Xf, y)            # K5 + gb_step
 Xk = np.round(rng.random((2000, 5)) * 10)
 kendall_matrix(Xk)
