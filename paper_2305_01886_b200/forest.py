@@ -248,7 +248,7 @@ class _LevelGrower:
             split_d = torch.full((6 * nt,), -1, dtype=i32, device=dev)  # feat -1: leaf
             lp = _ptr(lists_d)
             if n_s + n_m + n_b == 0:
-                records.append((tasks_d, node_d, split_d, None, nt))
+                records.append((tasks_d, node_d, split_d, None, nt, 0))
                 break
             if n_b > n_big_cap:
                 raise RuntimeError("forest: big-task workspace undersized")
@@ -273,8 +273,8 @@ class _LevelGrower:
                 _ptr(tasks_d), _ptr(node_d), _ptr(split_d), nt, TB, depth + 1, max_depth,
                 _ptr(next_id_d), _ptr(lid_d), _ptr(tasks_n), _ptr(node_n), _ptr(lists_n),
                 2 * nt, _ptr(stats_d), _ptr(scratch), st))
-            records.append((tasks_d, node_d, split_d, lid_d, nt))
             stats = stats_d.cpu().numpy().astype(np.int64)  # the level's one sync
+            records.append((tasks_d, node_d, split_d, lid_d, nt, int(stats[0]) // 2))
             depth += 1
             if stats[0] == 0:
                 break
@@ -303,38 +303,46 @@ class _LevelGrower:
         feat = torch.full((N,), TREE_UNDEFINED, dtype=i64, device=dev)
         nbin = torch.zeros(N, dtype=i64, device=dev)
         left = torch.full((N,), TREE_LEAF, dtype=i64, device=dev)
-        depth_d = torch.zeros(TB, dtype=i64, device=dev)
-        leaf_tasks, leaf_g, lvl_split = [], [], []
-        for lvl, (tk_d, nd_d, sp_d, lid_d, nt) in enumerate(records):
-            tk = tk_d[: 4 * nt].view(nt, 4)
-            sp = sp_d[: 6 * nt].view(nt, 6)
-            tree = tk[:, 0].long()
-            g = nb_d[tree] + nd_d[:nt].long()
-            s = sp[:, 0] >= 0
-            leaf_tasks.append(tk[~s])
-            leaf_g.append(g[~s])
-            if lid_d is None:
-                continue
-            gs = g[s]
-            if gs.numel():
-                lid = lid_d[:nt][s].long()
-                feat[gs] = sp[s, 0].long()
-                nbin[gs] = sp[s, 1].long()
-                left[gs] = lid
-                lvl_split.append((gs, nb_d[tree[s]] + lid))
-                depth_d.index_fill_(0, tree[s], lvl + 1)
-        lv_d = torch.cat(leaf_tasks).contiguous()
-        gl = torch.cat(leaf_g)
+        # all levels at once (level order kept), two compactions: split tasks and
+        # leaves -- a few syncs per batch instead of several per level
+        tk = torch.cat([r[0][: 4 * r[4]].view(r[4], 4) for r in records])
+        sp = torch.cat([r[2][: 6 * r[4]].view(r[4], 6) for r in records])
+        nd = torch.cat([r[1][: r[4]] for r in records]).long()
+        lid_all = torch.cat([r[3][: r[4]] if r[3] is not None else
+                             torch.full((r[4],), -1, dtype=torch.int32, device=dev)
+                             for r in records]).long()
+        lvl_all = torch.cat([torch.full((r[4],), k + 1, dtype=i64, device=dev)
+                             for k, r in enumerate(records)])
+        tree = tk[:, 0].long()
+        g = nb_d[tree] + nd
+        s = sp[:, 0] >= 0
+        si = torch.nonzero(s).squeeze(1)
+        li = torch.nonzero(~s).squeeze(1)
+        gs = g[si]
+        lid = lid_all[si]
+        feat[gs] = sp[si, 0].long()
+        nbin[gs] = sp[si, 1].long()
+        left[gs] = lid
+        glid = nb_d[tree[si]] + lid
+        depth_d = torch.zeros(TB, dtype=i64, device=dev).scatter_reduce_(
+            0, tree[si], lvl_all[si], reduce="amax")
+        lv_d = tk[li].contiguous()
+        gl = g[li]
         nl = int(lv_d.shape[0])
         max_leaf = int((lv_d[:, 2] - lv_d[:, 1]).max()) if nl else 0
         stats_d = torch.empty(4 * max(nl, 1), dtype=i64, device=dev)
         _check(L.gk_rf_leaf_stats(_ptr(counts), n, _ptr(D["yfp"]), _ptr(D["y2fp"]), _ptr(lv_d),
                                   nl, _ptr(rows0), _ptr(rows1), _ptr(stats_d), max_leaf, st))
+        # split tasks per level (host counts from the level loop) bound the
+        # bottom-up segments of gs / glid
+        seg = np.concatenate([[0], np.cumsum([r[5] for r in records])]).astype(np.int64)
+        lvl_split = [(gs[seg[k]: seg[k + 1]], glid[seg[k]: seg[k + 1]])
+                     for k in range(len(records)) if seg[k + 1] > seg[k]]
         # exact integer sums bottom-up, converted to float64 once per node
         ist = torch.zeros((N, 4), dtype=i64, device=dev)
         ist[gl] = stats_d[: 4 * nl].view(nl, 4)
-        for gs, glid in reversed(lvl_split):
-            ist[gs] = ist[glid] + ist[glid + 1]
+        for pa, ch in reversed(lvl_split):
+            ist[pa] = ist[ch] + ist[ch + 1]
         is_split = left >= 0
         thr_t = torch.from_numpy(self._thr).to(dev)
         w = ist[:, 1].double()
