@@ -122,7 +122,7 @@ class GradientBoostingRegressor(_LevelGrower):
             self._dev["shift"], self._dev["shift2"] = shift, shift2
         self.n_estimators_ = len(self.estimators_)
         self._flat = None
-        del self._dev
+        del self._dev, self._dev_thr
         return self
 
     # -------------------------------------------------------------- predict

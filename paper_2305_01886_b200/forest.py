@@ -160,6 +160,9 @@ class _LevelGrower:
         del Xd
         self._thr_tables(bmin.cpu().numpy().view(np.uint32).reshape(F, N_BINS),
                          bmax.cpu().numpy().view(np.uint32).reshape(F, N_BINS))
+        # device copy for the tree assembly, complete before any batch stream reads it
+        self._dev_thr = torch.from_numpy(self._thr).to(dev)
+        torch.cuda.current_stream().synchronize()
         return Xb
 
     def _thr_tables(self, bmin_ord, bmax_ord):
@@ -344,7 +347,7 @@ class _LevelGrower:
         for pa, ch in reversed(lvl_split):
             ist[pa] = ist[ch] + ist[ch + 1]
         is_split = left >= 0
-        thr_t = torch.from_numpy(self._thr).to(dev)
+        thr_t = self._dev_thr
         w = ist[:, 1].double()
         s2 = ist[:, 2].double() * (2.0 ** -D["shift"])  # == np.ldexp (power-of-two scale)
         s3 = ist[:, 3].double() * (2.0 ** -D["shift2"])
@@ -619,7 +622,7 @@ class RandomForestRegressor(_LevelGrower):
                 self.estimators_[t] = TreeEstimator(tree_=tree, random_state=int(seeds[t]))
         if self.shard is None:
             self._flat = None
-        del self._dev
+        del self._dev, self._dev_thr
         return self
 
     def _grow_batch(self, seeds):
