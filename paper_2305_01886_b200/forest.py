@@ -645,7 +645,12 @@ class RandomForestRegressor(_LevelGrower):
         # one up-front segment for this batch's row lists and level records, freed
         # into this stream's cache so the level loop's allocations split it
         # instead of each mapping fresh memory (cudaMalloc ~1 ms per level buffer)
-        torch.empty(total * 56 + (64 << 20), dtype=torch.uint8, device=dev)
+        # (capped: a reservation only saves allocation calls, it must never be
+        # what runs a large fit out of memory)
+        try:
+            torch.empty(min(total * 56 + (64 << 20), 4 << 30), dtype=torch.uint8, device=dev)
+        except torch.OutOfMemoryError:
+            pass
         base_d = torch.from_numpy(base).to(dev)
         rows0 = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
         rows1 = torch.empty_like(rows0)
