@@ -160,20 +160,24 @@ def _tree_arrays(t):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("rows,depth,trees", [(120_000, None, 6), (3_000, 5, 40)])
-def test_device_level_bookkeeping_equals_host_form(monkeypatch, rows, depth, trees):
+@pytest.mark.parametrize("rows,depth,trees,tpb", [(120_000, None, 12, None), (3_000, 5, 40, None),
+                                                 (300, None, 1500, 1500)])
+def test_device_level_bookkeeping_equals_host_form(monkeypatch, rows, depth, trees, tpb):
     """gk_rf_next_level (device bookkeeping) grows the same trees, node for node,
     as the numpy level loop it replaced (GK_RF_HOST_LEVELS=1): big (> 32768
-    rows), medium, small and tiny tasks, unbounded depth and a depth cap."""
+    rows), medium, small and tiny tasks, unbounded depth and a depth cap; levels
+    of > 1024 scan blocks and batches of > 1024 trees (the one-CTA scans'
+    multi-chunk loops)."""
     from paper_2305_01886_b200.forest import RandomForestRegressor
 
     rng = np.random.default_rng(7)
     X = rng.random((rows, 12))
     X[:, 9:] = np.floor(X[:, 9:] * 5)
     y = 3 * X[:, 0] + np.sin(6 * X[:, 1]) + (X[:, 9] > 2) + rng.normal(0, 0.1, rows)
-    got = RandomForestRegressor(trees, max_depth=depth, random_state=11).fit(X, y)
+    kw = dict(max_depth=depth, random_state=11, trees_per_batch=tpb)
+    got = RandomForestRegressor(trees, **kw).fit(X, y)
     monkeypatch.setenv("GK_RF_HOST_LEVELS", "1")
-    want = RandomForestRegressor(trees, max_depth=depth, random_state=11).fit(X, y)
+    want = RandomForestRegressor(trees, **kw).fit(X, y)
     for a, b in zip(got.estimators_, want.estimators_):
         for u, v in zip(_tree_arrays(a.tree_), _tree_arrays(b.tree_)):
             assert np.array_equal(u, v)
