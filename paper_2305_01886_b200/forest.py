@@ -243,7 +243,7 @@ class _LevelGrower:
         hist = torch.empty(max(int(L.gk_rf_hist_bytes(n_big_cap, F)), 8), dtype=torch.uint8,
                            device=dev)
         cursor = torch.empty(0, dtype=i32, device=dev)
-        records = []  # per level: (tasks, node, split, lid, n_tasks) on the device
+        records = []  # per level: (tasks, node, split, lid, n_tasks, n_split), device tensors
         depth = 0
         while True:
             nt = int(stats[0])
