@@ -79,17 +79,25 @@ def tree_seeds(random_state, n_estimators: int) -> np.ndarray:
                     dtype=np.int64)
 
 
-def bin_edges(Xf: np.ndarray, n_bins: int = N_BINS, sample: int = 65_536):
+def bin_edges(Xf: np.ndarray, n_bins: int = N_BINS, sample: int = 65_536, device=None):
     """Per-feature bin edges on float32 data: one bin per distinct value when a
     feature has <= n_bins of them, else quantile edges of a deterministic
-    row sample (>= 256 sample rows per bin).  One column-wise sort."""
+    row sample (>= 256 sample rows per bin).  One column-wise sort -- on
+    `device` when given (sorting is exact: the same sorted columns; it was
+    ~1/3 of a 50-stage boosting fit on the host)."""
     n, F = Xf.shape
     if n > sample:
         idx = np.random.default_rng(0).choice(n, sample, replace=False)
         S = Xf[np.sort(idx)]
     else:
         S = Xf
-    S = np.sort(S.astype(np.float32), axis=0)
+    if device is not None:
+        import torch
+
+        S = torch.sort(torch.from_numpy(np.ascontiguousarray(S, dtype=np.float32)).to(device),
+                       dim=0).values.cpu().numpy()
+    else:
+        S = np.sort(S.astype(np.float32), axis=0)
     m = S.shape[0]
     edges = np.zeros((F, n_bins - 1), np.float32)
     n_edges = np.zeros(F, np.int32)
@@ -148,7 +156,7 @@ class _LevelGrower:
         n, F = X.shape
         L = _lib()
         dev = device()
-        edges, n_edges = bin_edges(X, self.n_bins)   # float32 sample inside
+        edges, n_edges = bin_edges(X, self.n_bins, device=dev)   # float32 sample inside
         Xd = _dev(X, dev)               # k5_bin casts to float32 (sklearn)
         Xb = torch.empty(n * F, dtype=torch.uint8, device=dev)
         bmin = torch.empty(F * N_BINS, dtype=torch.int32, device=dev)

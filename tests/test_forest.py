@@ -197,3 +197,16 @@ def test_device_level_bookkeeping_equals_host_form_gbt(monkeypatch):
         for u, v in zip(_tree_arrays(a.tree_), _tree_arrays(b.tree_)):
             assert np.array_equal(u, v)
     np.testing.assert_array_equal(got.predict(X[:1000]), want.predict(X[:1000]))
+
+
+@pytest.mark.gpu
+def test_bin_edges_device_sort_equals_host():
+    rng = np.random.default_rng(4)
+    X = rng.random((200_000, 9))
+    X[:, 3] = np.floor(X[:, 3] * 7)          # few distinct values: one bin each
+    X[:5000, 5] = np.nan                      # NaNs sort last on both
+    X[::7, 6] = -0.0
+    e0, n0 = bin_edges(X)
+    e1, n1 = bin_edges(X, device="cuda")
+    assert np.array_equal(n0, n1)
+    assert np.array_equal(e0, e1, equal_nan=True)  # -0.0 == 0.0 compares equal, as binning does
