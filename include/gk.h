@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define GK_ABI_VERSION 3
+#define GK_ABI_VERSION 4
 
 /* resource / class codes (reference ptx/types.py:12-24) */
 enum { GK_SP = 0, GK_SFU = 1, GK_DPU = 2, GK_LSU = 3, GK_WS = 4, GK_NRES = 5 };
@@ -153,6 +153,11 @@ typedef struct {
      * point; the order only balances the device's dynamic work queue
      * (largest kernels first). */
     const uint32_t  *order;
+    /* optional device counter (NULL = none): mem_throughput clamps to tp_floor
+     * (profiles.py:173-181, where the reference logs a warning per clamped
+     * call) are atomically added here.  Per grid, so concurrent sweeps on
+     * different streams keep separate counts (no library-global state). */
+    unsigned long long *tp_clamps;
     uint32_t n_k, n_cfg, n_arch, pad_;
 } gk_grid;
 
@@ -352,11 +357,6 @@ size_t gk_corr_pearson_workspace(int64_t n, int32_t K);
 /* column means and centred co-moments (upper triangle, row-major), fixed-order sums */
 int gk_corr_pearson(const double *X, int64_t n, int32_t K, int64_t ld, double *mean,
                     double *comoment, void *ws, size_t ws_bytes, void *stream);
-
-/* mem_throughput clamps to tp_floor (profiles.py:173-181: the reference logs a
- * warning per clamped call) counted on the device since the last reset;
- * synchronous.  reset != 0 zeroes the counter after reading. */
-int gk_throughput_clamps(uint64_t *out, int reset);
 
 int gk_set_stage_timing(int on);
 int gk_get_stage_ms(float *out3);

@@ -74,7 +74,7 @@ class HostGrid:
                               corpus.n_ker, max(len(corpus.sigs), 1), corpus.max_n,
                               corpus.max_blk)
         self.g = abi.GkGrid(_p(self.kernel_ids), _p(self.cfg), _p(self.arch), _p(self.lat),
-                            _p(self.n_tw), _p(self.gm), None, len(self.kernel_ids),
+                            _p(self.n_tw), _p(self.gm), None, None, len(self.kernel_ids),
                             len(self.cfg), len(self.arch), 0)
 
     @property

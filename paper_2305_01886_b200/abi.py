@@ -19,7 +19,7 @@ class GkCorpus(C.Structure):
 
 class GkGrid(C.Structure):
     _fields_ = [("kernel_ids", P), ("cfg", P), ("arch", P), ("lat", P),
-                ("n_tw_override", P), ("gm_override", P), ("order", P),
+                ("n_tw_override", P), ("gm_override", P), ("order", P), ("tp_clamps", P),
                 ("n_k", C.c_uint32), ("n_cfg", C.c_uint32), ("n_arch", C.c_uint32),
                 ("pad_", C.c_uint32)]
 
@@ -43,4 +43,4 @@ SF_NAMES = ("gm_latency", "d_kernel", "overhead_cycles", "gm_penalty", "sm_penal
             "cm_penalty", "d_total", "time_us", "cfg_delay")
 STATUS_OK, STATUS_INFEASIBLE_LAUNCH, STATUS_INFEASIBLE_OCCUPANCY = 0, 1, 2
 
-assert C.sizeof(GkCorpus) == 72 and C.sizeof(GkGrid) == 72 and C.sizeof(GkEnsemble) == 104
+assert C.sizeof(GkCorpus) == 72 and C.sizeof(GkGrid) == 80 and C.sizeof(GkEnsemble) == 104

@@ -9,7 +9,8 @@ Scalar face (reference ``gpukalc/__init__.py:16-71``):
 Batched face (new; what the per-launch loops of cli.py:184-197/251-254 become):
     schedule_batch / extract_features_batch / predict_power_batch / predict_launches
 
-Scalar calls pack + upload the graph once (cached per graph object) and run
+Scalar calls pack the graph on every call (as the reference recomputes; device
+uploads are cached by content digest, so edited graphs are never stale) and run
 the same kernels as the batched sweep with a one-point grid.  The scalar
 ``predict_energy`` keeps the reference's decimal product (its exactness is
 part of the contract pinned by pkg/tests/test_power.py:215-217); batched
@@ -184,16 +185,40 @@ def _launch_tuple(launch) -> tuple:
     return tuple(launch)
 
 
+_CORPUS_CAP_BYTES = 256 << 20
+
+
+def _corpus_digest(c) -> bytes:
+    """Content digest of a packed corpus: every record the device reads plus the
+    signature table, so a graph edited in place (trip counts, blocks,
+    instructions) can never hit a stale upload."""
+    import hashlib
+
+    h = hashlib.blake2b(digest_size=20)
+    for arr in (c.tok, c.preds, c.blk, c.fpreds, c.topo, c.ker):
+        h.update(np.ascontiguousarray(arr).view(np.uint8).tobytes())
+        h.update(len(arr).to_bytes(8, "little"))
+    h.update(repr(c.sigs).encode())
+    return h.digest()
+
+
 def _device_corpus(graphs):
+    """The graphs packed (every call: the reference recomputes per call, so
+    in-place edits of a KernelGraph take effect) and uploaded; uploads are
+    cached by content digest, bounded by bytes (LRU)."""
     from .runtime import DeviceCorpus
 
-    key = tuple(id(g) for g in graphs)
-    hit = _CORPUS.get(key)
+    c = pack_corpus(graphs)
+    key = _corpus_digest(c)
+    hit = _CORPUS.pop(key, None)
     if hit is None:
-        if len(_CORPUS) > 64:
-            _CORPUS.clear()
-        hit = _CORPUS[key] = (list(graphs), DeviceCorpus.upload(pack_corpus(graphs)))
-    return hit[1]
+        hit = DeviceCorpus.upload(c)
+    _CORPUS[key] = hit  # most recent last
+    total = sum(d.nbytes for d in _CORPUS.values())
+    while total > _CORPUS_CAP_BYTES and len(_CORPUS) > 1:
+        old = next(iter(_CORPUS))
+        total -= _CORPUS.pop(old).nbytes
+    return hit
 
 
 def _infeasible_message(launch) -> str:
@@ -220,18 +245,19 @@ def schedule_batch(profiles, graphs, launches, *, features: bool = True, sel_idx
     dc = _device_corpus(graphs)
     dg = DeviceGrid.build(dc, profiles, [_launch_tuple(L) for L in launches])
     out = schedule_features(dc, dg, feat=features, sel_idx=sel_idx, trace=trace)
-    _log_clamps()
+    _log_clamps(dg)
     if not to_host:
         return out
     return {k: (v.cpu().numpy() if hasattr(v, "cpu") else v) for k, v in out.items()}
 
 
-def _log_clamps() -> None:
+def _log_clamps(dg) -> None:
     """The reference warns on every clamped mem_throughput call
-    (profiles.py:173-181); the device counts them, logged once per batch."""
+    (profiles.py:173-181); the device counts them per grid, logged once per
+    batch."""
     from .runtime import throughput_clamps
 
-    n = throughput_clamps(reset=True)
+    n = throughput_clamps(dg, reset=True)
     if n:
         log.warning("throughput model gave a non-positive value %d times in this batch; "
                     "clamped to tp_floor", n)

@@ -27,7 +27,7 @@ import ctypes as C
 import numpy as np
 
 from .ensemble import NODE_DT, FlatEnsemble
-from .forest import _LevelGrower, _check, _lib, TreeEstimator
+from .forest import TreeEstimator, _check, _LevelGrower, _lib, check_finite, check_n_bins
 
 
 def _shifts(bound: float, n: int) -> tuple[int, int]:
@@ -59,7 +59,7 @@ class GradientBoostingRegressor(_LevelGrower):
         self.learning_rate = learning_rate
         self.max_depth = max_depth
         self.random_state = random_state
-        self.n_bins = n_bins
+        self.n_bins = check_n_bins(n_bins)
         self.estimators_: list = []
 
     def fit(self, X, y, sample_weight=None):
@@ -76,6 +76,10 @@ class GradientBoostingRegressor(_LevelGrower):
         n, F = X.shape
         if n < 1 or F > 64 * 1024 or n >= 2 ** 31:
             raise ValueError("bad training table shape")
+        if len(y) != n:
+            raise ValueError("X and y have different lengths")
+        check_finite(X, y)
+        check_n_bins(self.n_bins)
         self.n_features_in_ = F
         L = _lib()
         if not getattr(L, "_gb_bound", False):

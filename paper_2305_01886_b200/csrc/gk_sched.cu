@@ -22,13 +22,14 @@
 namespace gk {
 
 // mem_throughput clamps to tp_floor (profiles.py:173-181, where the reference
-// logs a warning per call) counted on the device; read by gk_throughput_clamps
-__device__ unsigned long long g_tp_clamps = 0;
-
-__device__ __forceinline__ double tput_c(double a, double b, double c, double floor_, double n) {
+// logs a warning per call) counted on the device into the caller's per-grid
+// counter (gk_grid.tp_clamps; NULL = not counted): no library-global state, so
+// concurrent sweeps on different streams keep separate counts
+__device__ __forceinline__ double tput_c(double a, double b, double c, double floor_, double n,
+                                         unsigned long long *clamps) {
     const double v = __dmul_rn(a, __dsub_rn(b, gk_exp(__dmul_rn(-c, n))));
     if (v <= 0.0) {
-        atomicAdd(&g_tp_clamps, 1ull);
+        if (clamps) atomicAdd(clamps, 1ull);
         return floor_;
     }
     return v;
@@ -369,14 +370,14 @@ __device__ __forceinline__ double finish_point(const gk_corpus &C, const gk_grid
     const double lsu = (double)A.units[GK_LSU];
     double gm_pen = 0.0, sm_pen = 0.0, cm_pen = 0.0;
     if (n_gm != 0) {
-        const double tp = tput_c(A.tpg_a, A.tpg_b, A.tpg_c, A.tp_floor, (double)n_gm);
+        const double tp = tput_c(A.tpg_a, A.tpg_b, A.tpg_c, A.tp_floor, (double)n_gm, G.tp_clamps);
         gm_pen = __dmul_rn(__dmul_rn(__ddiv_rn(x, lsu), __ddiv_rn((double)A.access_gm_sz, tp)),
                            (double)n_gm);
         const double lines = __ddiv_rn((double)(waves * A.L2_sz), (double)A.access_sz);
         cm_pen = __dmul_rn(__ddiv_rn((double)(tt * n_gm), lines), gm);
     }
     if (n_shm != 0) {
-        const double tp = tput_c(A.tps_a, A.tps_b, A.tps_c, A.tp_floor, (double)n_shm);
+        const double tp = tput_c(A.tps_a, A.tps_b, A.tps_c, A.tp_floor, (double)n_shm, G.tp_clamps);
         sm_pen = __dmul_rn(__dmul_rn(__ddiv_rn(x, (double)(A.units[GK_LSU] * A.nSM)),
                                      __ddiv_rn((double)A.access_shm_sz, tp)),
                            (double)n_shm);
@@ -454,14 +455,14 @@ __device__ __forceinline__ double finish_point(const gk_corpus &C, const gk_grid
         glb_pen = __dmul_rn(
             __dmul_rn(__ddiv_rn(x, lsu),
                       __ddiv_rn((double)A.access_sz,
-                                tput_c(A.tpg_a, A.tpg_b, A.tpg_c, A.tp_floor, glob_sm))),
+                                tput_c(A.tpg_a, A.tpg_b, A.tpg_c, A.tp_floor, glob_sm, G.tp_clamps))),
             glob_sm);
     }
     if (shar_sm > 0) {
         sh_pen = __dmul_rn(
             __dmul_rn(__ddiv_rn(x, (double)(A.units[GK_LSU] * A.nSM)),
                       __ddiv_rn((double)A.access_sz,
-                                tput_c(A.tps_a, A.tps_b, A.tps_c, A.tp_floor, shar_sm))),
+                                tput_c(A.tps_a, A.tps_b, A.tps_c, A.tp_floor, shar_sm, G.tp_clamps))),
             shar_sm);
     }
     // features on demand (no 32-double array: keeps register pressure down)
@@ -768,21 +769,6 @@ uint32_t smem_rows_cap() {
 }
 constexpr int kMaxCtaPerSm = 16;
 }  // namespace
-
-extern "C" int gk_throughput_clamps(uint64_t *out, int reset) {
-    unsigned long long v = 0;
-    cudaError_t e = cudaMemcpyFromSymbol(&v, gk::g_tp_clamps, sizeof v);
-    if (e == cudaSuccess && reset) {
-        const unsigned long long z = 0;
-        e = cudaMemcpyToSymbol(gk::g_tp_clamps, &z, sizeof z);
-    }
-    if (e != cudaSuccess) {
-        gk_set_error("gk_throughput_clamps: %s", cudaGetErrorString(e));
-        return -1;
-    }
-    *out = (uint64_t)v;
-    return 0;
-}
 
 int gk_launch_static(const gk_corpus *C, const gk_grid *G, gk_kstat *ks, double *latsum,
                      cudaStream_t st) {

@@ -10,9 +10,12 @@ path is sharded so that no collective is needed while computing:
   on the world size: ``RandomForestRegressor(shard=(rank, world))`` then
   :func:`allgather_forest`;
 * the only exchanges are the ones the reference's outputs need: the results
-  (:func:`allgather_results`) and the ensemble (:func:`broadcast_flat`).
+  (:class:`ResultGather`, :func:`allgather_results`) and the ensemble
+  (:func:`broadcast_tensors` / :func:`broadcast_device_ensemble`, device
+  buffers broadcast in place -- no host round trip).
 Collectives run on whatever backend the process group uses (``nccl`` on the
-GPU box, ``gloo`` in the CPU tests).
+GPU box, ``gloo`` in the CPU tests); tensors live on the device the group
+needs (``collective_device``).
 """
 
 from __future__ import annotations
@@ -25,6 +28,52 @@ def kernel_shard(n_kernels: int, rank: int, world: int) -> np.ndarray:
     lo = n_kernels * rank // world
     hi = n_kernels * (rank + 1) // world
     return np.arange(lo, hi, dtype=np.uint32)
+
+
+def chunk_shard(n_chunks: int, rank: int, world: int) -> range:
+    """Contiguous ranges of generator chunks (workloads.synth_chunks) per rank:
+    a rank builds only its own kernels, and the union over ranks is the global
+    corpus in kernel order."""
+    return range(n_chunks * rank // world, n_chunks * (rank + 1) // world)
+
+
+def collective_device(group=None):
+    """Where a collective's tensors must live: the current CUDA device for
+    NCCL, host memory for gloo."""
+    import torch
+    import torch.distributed as dist
+
+    if dist.get_backend(group) == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
+class ResultGather:
+    """Preallocated all-gather of equal-length per-rank result vectors (the
+    sweep's status / time / power / energy of each rank's kernel shard) into
+    rank-order concatenations on every rank: one ``all_gather_into_tensor``
+    per vector (ncclAllGather over NVLink on the GPU box).  ``run`` is what
+    the timed multi-GPU step calls after the sweep."""
+
+    def __init__(self, like: list, group=None):
+        import torch
+        import torch.distributed as dist
+
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.out = [torch.empty((self.world * t.shape[0],) + tuple(t.shape[1:]), dtype=t.dtype,
+                                device=t.device) for t in like]
+
+    @property
+    def nbytes(self) -> int:
+        return sum(o.numel() * o.element_size() for o in self.out)
+
+    def run(self, tensors: list) -> list:
+        import torch.distributed as dist
+
+        for o, t in zip(self.out, tensors):
+            dist.all_gather_into_tensor(o, t.contiguous(), group=self.group)
+        return self.out
 
 
 def allgather_results(tensors: list, group=None) -> list:
@@ -50,16 +99,60 @@ def allgather_results(tensors: list, group=None) -> list:
     return out
 
 
+def broadcast_tensors(bufs: dict | None, src: int = 0, group=None, device=None) -> dict:
+    """Broadcast a dict of tensors from rank `src`: shapes / dtypes go as one
+    object broadcast, then every tensor in place (NCCL: device to device over
+    NVLink, no host staging).  Other ranks pass None and get the dict back on
+    `device` (default: the group's collective device)."""
+    import torch
+    import torch.distributed as dist
+
+    rank = dist.get_rank(group)
+    dev = device or collective_device(group)
+    meta = [None]
+    if rank == src:
+        meta = [{k: (tuple(v.shape), str(v.dtype).replace("torch.", "")) for k, v in bufs.items()}]
+    dist.broadcast_object_list(meta, src=src, group=group)
+    if rank != src:
+        bufs = {k: torch.empty(shape, dtype=getattr(torch, dt), device=dev)
+                for k, (shape, dt) in meta[0].items()}
+    for k in sorted(bufs):
+        dist.broadcast(bufs[k], src=src, group=group)
+    return bufs
+
+
+def broadcast_device_ensemble(de, src: int = 0, group=None):
+    """the ensemble replicated once, ncclBroadcast from rank 0.
+    Rank `src` passes its DeviceEnsemble (every walk layout's buffers: the
+    16-byte nodes, blocks, exact thresholds, leaves, scaling); the others pass
+    None and get a DeviceEnsemble over the received device buffers."""
+    import torch.distributed as dist
+
+    from .runtime import DeviceEnsemble
+
+    rank = dist.get_rank(group)
+    meta = [None]
+    if rank == src:
+        meta = [dict(base=float(de.desc.base_score), n_trees=int(de.desc.n_trees),
+                     n_feat=int(de.desc.n_feat), max_depth=int(de.desc.max_depth))]
+    dist.broadcast_object_list(meta, src=src, group=group)
+    bufs = broadcast_tensors(de.bufs if rank == src else None, src=src, group=group)
+    if rank == src:
+        return de
+    return DeviceEnsemble.from_buffers(bufs, **meta[0])
+
+
 def broadcast_flat(flat, src: int = 0, group=None, device=None):
     """Broadcast a FlatEnsemble (node arrays + scaling) from `src` to all ranks;
-    returns the FlatEnsemble on every rank."""
+    returns the FlatEnsemble on every rank (host arrays; the tensors travel
+    on the group's collective device)."""
     import torch
     import torch.distributed as dist
 
     from .ensemble import NODE_DT, FlatEnsemble
 
     rank = dist.get_rank(group)
-    dev = device or torch.device("cpu")
+    dev = device or collective_device(group)
     meta = [None]
     if rank == src:
         meta = [dict(n_nodes=len(flat.nodes), n_trees=flat.n_trees, n_feat=flat.n_feat,

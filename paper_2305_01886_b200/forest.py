@@ -99,7 +99,9 @@ def bin_edges(Xf: np.ndarray, n_bins: int = N_BINS, sample: int = 65_536, device
     else:
         S = np.sort(S.astype(np.float32), axis=0)
     m = S.shape[0]
-    edges = np.zeros((F, n_bins - 1), np.float32)
+    # k5_bin reads a fixed (N_BINS - 1)-wide edge row per feature; fewer bins
+    # use a prefix of it (n_edges[f] <= n_bins - 1)
+    edges = np.zeros((F, N_BINS - 1), np.float32)
     n_edges = np.zeros(F, np.int32)
     qpos = (np.linspace(0.0, 1.0, n_bins + 1)[1:-1] * (m - 1)).astype(np.int64)  # "lower"
     for f in range(F):
@@ -116,6 +118,24 @@ def bin_edges(Xf: np.ndarray, n_bins: int = N_BINS, sample: int = 65_536, device
         edges[f, : len(e)] = e
         n_edges[f] = len(e)
     return edges, n_edges
+
+
+def check_n_bins(n_bins) -> int:
+    """K5 bins are u8 ids with a fixed 256-entry table per feature: any
+    2 <= n_bins <= 256 is exact (fewer bins use a prefix of the edge row)."""
+    if isinstance(n_bins, bool) or not isinstance(n_bins, (int, np.integer)) \
+            or not 2 <= int(n_bins) <= N_BINS:
+        raise ValueError(f"n_bins must be an integer in [2, {N_BINS}], got {n_bins!r}")
+    return int(n_bins)
+
+
+def check_finite(X: np.ndarray, y: np.ndarray) -> None:
+    """scikit-learn rejects NaN / inf in X and y (check_X_y, force_all_finite):
+    same error class here, before anything reaches the device."""
+    if not np.isfinite(X).all():
+        raise ValueError("Input X contains NaN or infinity.")
+    if not np.isfinite(y).all():
+        raise ValueError("Input y contains NaN or infinity.")
 
 
 @dataclass
@@ -556,7 +576,7 @@ class RandomForestRegressor(_LevelGrower):
         self.n_estimators = n_estimators
         self.max_depth = max_depth
         self.random_state = random_state
-        self.n_bins = n_bins
+        self.n_bins = check_n_bins(n_bins)
         self.trees_per_batch = trees_per_batch
         self.shard = shard  # (rank, world): build trees t with t % world == rank
         self.concurrent = concurrent  # overlap tree batches (host work vs kernels)
@@ -574,8 +594,12 @@ class RandomForestRegressor(_LevelGrower):
         X = np.ascontiguousarray(X, dtype=np.float64)
         y = np.ascontiguousarray(y, dtype=np.float64).reshape(-1)
         n, F = X.shape
-        if F > 64 * 1024 or n >= 2 ** 31:
-            raise ValueError("too many rows / features")
+        if n < 1 or F > 64 * 1024 or n >= 2 ** 31:
+            raise ValueError("bad training table shape")
+        if len(y) != n:
+            raise ValueError("X and y have different lengths")
+        check_finite(X, y)
+        check_n_bins(self.n_bins)
         self.n_features_in_ = F
         Xb = self._prepare_bins(X)
         dev = device()
@@ -603,6 +627,9 @@ class RandomForestRegressor(_LevelGrower):
         # B200 at 1M x 64: 4 batches in flight 18.7 ms/tree, 2: 24 ms/tree)
         tpb = self.trees_per_batch or max(16, min(int(32_000_000 // max(n, 1)),
                                                   -(-len(todo) // max(self.streams, 1))))
+        # row-list positions are int32: a batch's bootstrap rows (~0.632 n per
+        # tree) must stay below 2^31 (checked exactly after the bootstrap)
+        tpb = max(1, min(tpb, int(0.9 * 2 ** 31 / (0.64 * n + 1))))
         batches = [todo[b0: b0 + tpb] for b0 in range(0, len(todo), tpb)]
         # two batches in flight on their own streams: one batch's host-side level
         # bookkeeping (numpy, GIL released) overlaps the other's kernels
@@ -650,6 +677,9 @@ class RandomForestRegressor(_LevelGrower):
         m = (counts.view(TB, n) > 0).sum(dim=1).cpu().numpy().astype(np.int64)
         base = np.concatenate([[0], np.cumsum(m)[:-1]]).astype(np.int64)
         total = int(m.sum())
+        if total >= 2 ** 31:
+            raise ValueError(f"forest: {TB} trees x {n} rows exceed the int32 row lists; "
+                             "use a smaller trees_per_batch")
         # one up-front segment for this batch's row lists and level records, freed
         # into this stream's cache so the level loop's allocations split it
         # instead of each mapping fresh memory (cudaMalloc ~1 ms per level buffer)

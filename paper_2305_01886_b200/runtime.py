@@ -22,8 +22,7 @@ from .pack import KSTAT_DT, Corpus, arch_records, config_array, latency_table
 LIB_PATH = Path(__file__).resolve().parent / "libgk.so"
 EXPORTS = ("gk_abi_version", "gk_last_error", "gk_device_sm_count", "gk_static_features",
            "gk_schedule_features", "gk_rf_predict", "gk_sweep_workspace_bytes",
-           "gk_predict_energy_sweep", "gk_set_stage_timing", "gk_get_stage_ms",
-           "gk_throughput_clamps")
+           "gk_predict_energy_sweep", "gk_set_stage_timing", "gk_get_stage_ms")
 _lib = None
 
 
@@ -52,8 +51,7 @@ def load_library(path: Path | None = None):
     L.gk_predict_energy_sweep.argtypes = [vp, vp, vp, vp, u32, vp, vp, vp, vp, vp, vp]
     L.gk_set_stage_timing.argtypes = [C.c_int]
     L.gk_get_stage_ms.argtypes = [vp]
-    L.gk_throughput_clamps.argtypes = [vp, C.c_int]
-    if L.gk_abi_version() != 3:
+    if L.gk_abi_version() != 4:
         raise DeviceError("libgk ABI version mismatch")
     if path is None:
         _lib = L
@@ -149,7 +147,9 @@ class DeviceGrid:
         lat = np.ascontiguousarray(latency_table(profiles, corpus.sigs))
         g = cls(len(kid), len(arch), len(cfg))
         g.bufs = {"kid": _dev(kid if len(kid) else np.zeros(1, np.uint32)), "cfg": _dev(cfg),
-                  "arch": _dev(arch), "lat": _dev(lat)}
+                  "arch": _dev(arch), "lat": _dev(lat),
+                  # this grid's mem_throughput clamp counter (gk_grid.tp_clamps)
+                  "clamps": _dev(np.zeros(1, np.int64))}
         if n_tw is not None:
             g.bufs["n_tw"] = _dev(np.asarray(n_tw, dtype=np.int64))
         if gm is not None:
@@ -167,7 +167,8 @@ class DeviceGrid:
             g.bufs["order"] = _dev(order)
         g.desc = abi.GkGrid(_ptr(g.bufs["kid"]), _ptr(g.bufs["cfg"]), _ptr(g.bufs["arch"]),
                             _ptr(g.bufs["lat"]), _ptr(g.bufs.get("n_tw")),
-                            _ptr(g.bufs.get("gm")), _ptr(g.bufs.get("order")), len(kid),
+                            _ptr(g.bufs.get("gm")), _ptr(g.bufs.get("order")),
+                            _ptr(g.bufs["clamps"]), len(kid),
                             len(cfg), len(arch), 0)
         return g
 
@@ -216,12 +217,26 @@ class DeviceEnsemble:
             if bl is not None:
                 de.bufs.update(blocks=_dev(bl.blocks), thr64=_dev(bl.thr64),
                                leaf_val=_dev(bl.leaf_val), root=_dev(bl.root))
-        b = de.bufs
-        de.desc = abi.GkEnsemble(_ptr(b["nodes"]), _ptr(b["off"]), _ptr(b["depth"]),
-                                 _ptr(b["lo"]), _ptr(b["hi"]),
-                                 float(flat.base_score), flat.n_trees, flat.n_feat,
-                                 flat.max_depth, _ptr(b.get("nodes8")), _ptr(b.get("blocks")),
-                                 _ptr(b.get("thr64")), _ptr(b.get("leaf_val")), _ptr(b.get("root")))
+        de.desc = cls._desc(de.bufs, float(flat.base_score), flat.n_trees, flat.n_feat,
+                            flat.max_depth)
+        return de
+
+    @staticmethod
+    def _desc(b: dict, base: float, n_trees: int, n_feat: int, max_depth: int):
+        return abi.GkEnsemble(_ptr(b["nodes"]), _ptr(b["off"]), _ptr(b["depth"]),
+                              _ptr(b["lo"]), _ptr(b["hi"]), float(base), int(n_trees),
+                              int(n_feat), int(max_depth), _ptr(b.get("nodes8")),
+                              _ptr(b.get("blocks")), _ptr(b.get("thr64")),
+                              _ptr(b.get("leaf_val")), _ptr(b.get("root")))
+
+    @classmethod
+    def from_buffers(cls, bufs: dict, *, base: float, n_trees: int, n_feat: int,
+                     max_depth: int) -> "DeviceEnsemble":
+        """An ensemble over device buffers that are already in walk layout
+        (e.g. received by dist.broadcast_device_ensemble)."""
+        de = cls(None)
+        de.bufs = dict(bufs)
+        de.desc = cls._desc(de.bufs, base, n_trees, n_feat, max_depth)
         return de
 
     @property
@@ -282,13 +297,20 @@ def schedule_features(dc: DeviceCorpus, dg: DeviceGrid, *, si=True, sf=True, fea
     return out
 
 
-def throughput_clamps(reset: bool = True) -> int:
+def throughput_clamps(dg: "DeviceGrid", reset: bool = True, stream=None) -> int:
     """How often the throughput model was clamped to tp_floor on the device
-    since the last reset (the reference logs a warning per clamped call,
-    profiles.py:173-181).  Synchronises."""
-    v = C.c_uint64()
-    _check(load_library().gk_throughput_clamps(C.byref(v), int(reset)))
-    return int(v.value)
+    for grid `dg` since its last reset (the reference logs a warning per
+    clamped call, profiles.py:173-181).  The counter belongs to the grid
+    (gk_grid.tp_clamps), so concurrent sweeps keep separate counts.
+    Synchronises `stream`."""
+    t = _torch()
+    c = dg.bufs["clamps"]
+    s = t.cuda.current_stream() if stream is None else stream
+    with t.cuda.stream(s):
+        v = int(c.item())
+        if reset:
+            c.zero_()
+    return v
 
 
 def rf_predict(de: DeviceEnsemble, X, *, status=None, time_us=None, stream=None):

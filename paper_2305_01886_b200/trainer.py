@@ -226,14 +226,50 @@ def ensemble_document_text(result: TrainResult) -> str:
                          gains=gains, trees=trees, indent=2)
 
 
-def export_ensemble(result: TrainResult, out_dir, *, n_vectors: int = 20):
-    """ensemble.json (+ metrics.json) like ``export.py:150-175``; the JSON text
-    comes from the native writer (identical bytes to json.dumps)."""
+VECTOR_SCHEMA_VERSION = 1  # export.py:23
+
+
+def _sample_rows(result: TrainResult, n_vectors: int) -> np.ndarray:
+    """Rows of the test vectors as ``export.py:128-134`` picks them: the last
+    CV fold's held-out rows (all rows when that pool is too small), sampled
+    without replacement by ``default_rng(seed)``, in row order."""
+    pool = np.asarray(result.holdout_indices)
+    if pool.size < n_vectors:
+        pool = np.arange(result.X.shape[0])
+    rng = np.random.default_rng(result.seed)
+    return np.sort(rng.choice(pool, size=min(n_vectors, pool.size), replace=False))
+
+
+def export_ensemble(result: TrainResult, out_dir, *, n_vectors: int = 20) -> tuple[Path, Path]:
+    """Write ensemble.json and test_vectors.json; return both paths
+    (``export.py:150-175``).  The ensemble text comes from the native writer
+    (the bytes of ``json.dumps(doc, indent=2)``); each vector's prediction is
+    the exported document walked on the device (K4: min-max scaling, then
+    base + leaves in tree order -- the reference walker's arithmetic,
+    ``export.py:101-125``) after loading the file back, so the vectors check
+    the file, not the in-memory model."""
+    import torch
+
+    from .ensemble import flatten, load_ensemble
+    from .runtime import DeviceEnsemble, device, rf_predict
+
     if n_vectors < 1:
         raise TrainerError("need at least one test vector")
     out = Path(out_dir)
     out.mkdir(parents=True, exist_ok=True)
-    p = out / "ensemble.json"
-    p.write_text(ensemble_document_text(result) + "\n")
-    (out / "metrics.json").write_text(json.dumps(result.metrics_doc(), indent=2) + "\n")
-    return p
+    ensemble_path = out / "ensemble.json"
+    ensemble_path.write_text(ensemble_document_text(result) + "\n")
+    picked = _sample_rows(result, n_vectors)
+    rows = np.ascontiguousarray(np.asarray(result.X, np.float64)[picked])
+    de = DeviceEnsemble.upload(flatten(load_ensemble(ensemble_path)))
+    power, _ = rf_predict(de, torch.from_numpy(rows).to(device()))
+    pred = power.cpu().numpy()
+    vectors = [{"inputs": {name: float(v) for name, v in zip(result.manifest, row)},
+                "prediction": float(p)} for row, p in zip(rows, pred)]
+    vectors_path = out / "test_vectors.json"
+    vectors_path.write_text(json.dumps({
+        "schema_version": VECTOR_SCHEMA_VERSION,
+        "ensemble_file": ensemble_path.name,
+        "vectors": vectors,
+    }, indent=2) + "\n")
+    return ensemble_path, vectors_path

@@ -1,0 +1,46 @@
+"""The torchrun path of bench.py executed end to end: 2 ranks
+on the gloo backend against CUDA tensors on ONE GPU (this pool has 1 GPU per
+box; NCCL refuses two ranks on one device).  Every N > 1 code path runs:
+chunk-sharded corpus generation, rank-0 ensemble build + device-buffer
+broadcast, the all-gather inside each timed step, max-over-ranks timing, the
+rank-0 oracle self-check and the e2e host-buffer leg."""
+
+import json
+import os
+import socket
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def _port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.gpu
+def test_bench_torchrun_two_ranks_gloo_on_one_gpu():
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={_port()}", str(ROOT / "bench.py"),
+           "--gpus", "2", "--backend", "gloo", "--kernels", "1000", "--cycle-kernels", "1000",
+           "--steps", "2", "--warmup", "3", "--trees", "24", "--depth", "8", "--no-rf",
+           "--no-c4", "--cpu-seconds", "1", "--e2e-steps", "1"]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900,
+                       env=dict(os.environ, OMP_NUM_THREADS="2"))
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]          # rank 0 prints one line
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong"
+    assert d["config"]["points"] == 1000 * 256 * 3
+    assert d["value"] > 0 and d["e2e"]["value"] > 0
+    assert d["allgather"]["bytes_per_rank"] == 1000 * 256 * 3 * 25
+    assert d["self_check"]["bit_exact"] == ["status", "time_us", "power_w", "energy_uj"]
+    assert d["cycle_sweep"]["value"] > 0

@@ -143,4 +143,59 @@ def test_tree_seeds_independent_of_world_size():
         assert [got[t] for t in range(12)] == list(s)
 
 
+def _result_gather_fn(rank, world):
+    import torch
+
+    from paper_2305_01886_b200.dist import ResultGather
+
+    n = 6   # equal shards (chunk-granular kernel shards)
+    st = torch.full((n,), rank + 1, dtype=torch.uint8)
+    tu = torch.arange(n, dtype=torch.float64) + 100 * rank
+    g = ResultGather([st, tu])
+    for _ in range(2):                       # reused buffers, every timed step
+        a, b = g.run([st, tu])
+    return a.tolist(), b.tolist(), g.nbytes
+
+
+def test_result_gather_rank_order():
+    out = _spawn(_result_gather_fn)
+    for r in (0, 1):
+        st, tu, nb = out[r]
+        assert st == [1] * 6 + [2] * 6
+        assert tu == [float(i) for i in range(6)] + [100.0 + i for i in range(6)]
+        assert nb == 12 * 1 + 12 * 8
+
+
+def _bcast_tensors_fn(rank, world):
+    import torch
+
+    from paper_2305_01886_b200.dist import broadcast_tensors
+
+    bufs = None
+    if rank == 0:
+        bufs = {"nodes": torch.arange(40, dtype=torch.uint8), "lo": torch.tensor([1.5, -2.0]),
+                "off": torch.tensor([0, 7, 19], dtype=torch.int64),
+                "blocks": torch.arange(24, dtype=torch.int32).view(3, 8)}
+    got = broadcast_tensors(bufs)
+    return {k: (str(v.dtype), tuple(v.shape), v.flatten().tolist()) for k, v in got.items()}
+
+
+def test_broadcast_tensors_every_layout_buffer():
+    """The device-ensemble broadcast (dist.broadcast_device_ensemble) ships
+    every walk-layout buffer with its dtype and shape."""
+    out = _spawn(_bcast_tensors_fn)
+    assert out[0] == out[1]
+    assert out[1]["blocks"] == ("torch.int32", (3, 8), list(range(24)))
+    assert out[1]["lo"] == ("torch.float32", (2,), [1.5, -2.0])
+
+
+def test_chunk_shards_cover_the_corpus_in_order():
+    from paper_2305_01886_b200.dist import chunk_shard
+
+    for n, w in ((2000, 1), (2000, 8), (5, 2), (13, 4)):
+        parts = [list(chunk_shard(n, r, w)) for r in range(w)]
+        assert sum(parts, []) == list(range(n))
+        assert parts[0][0] == 0
+
+
 pytestmark = pytest.mark.timeout(300) if hasattr(pytest.mark, "timeout") else []

@@ -149,3 +149,48 @@ def test_document_text_compact_and_escapes():
     assert E.document_text(**kw, indent=0) == json.dumps(doc, indent=0)
     empty = dict(kw, trees=[])
     assert E.document_text(**empty) == json.dumps(dict(doc, trees=[]), indent=2)
+
+
+def _walk_document(doc, inputs):
+    """export.py:101-125 restated (the reference's test-vector walker)."""
+    raw = [float(inputs[n]) for n in doc["feature_manifest"]]
+    lo, hi = doc["scaling"]["min"], doc["scaling"]["max"]
+    x = [(v - a) / (b - a) if b > a else 0.0 for v, a, b in zip(raw, lo, hi)]
+    total = float(doc.get("base_score", 0.0))
+    for tree in doc["trees"]:
+        nodes = tree["nodes"]
+        node = nodes[0]
+        while "value" not in node:
+            node = nodes[node["left"] if x[node["feature"]] <= node["threshold"] else node["right"]]
+        total += node["value"]
+    return total
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("family", ["random_forest", "gradient_boosted"])
+@pytest.mark.parametrize("n_vectors", [1, 7, 20, 500])
+def test_export_ensemble_writes_reference_test_vectors(tmp_path, family, n_vectors):
+    """export_ensemble mirrors export.py:150-175: returns (ensemble_path,
+    vectors_path); vectors are holdout rows (all rows when the holdout is too
+    small) drawn by default_rng(seed), predictions bit-equal to the reference
+    walker over the written file."""
+    from paper_2305_01886_b200.errors import TrainerError
+    from paper_2305_01886_b200.trainer import export_ensemble
+
+    res = _sk_result(family)
+    ep, vp = export_ensemble(res, tmp_path / "out", n_vectors=n_vectors)
+    assert ep.name == "ensemble.json" and vp.name == "test_vectors.json"
+    doc = json.loads(ep.read_text())
+    vec = json.loads(vp.read_text())
+    assert vec["schema_version"] == 1 and vec["ensemble_file"] == "ensemble.json"
+    pool = res.holdout_indices if res.holdout_indices.size >= n_vectors else np.arange(len(res.X))
+    want_rows = np.sort(np.random.default_rng(res.seed).choice(
+        pool, size=min(n_vectors, pool.size), replace=False))
+    assert len(vec["vectors"]) == len(want_rows)
+    for v, i in zip(vec["vectors"], want_rows):
+        assert list(v["inputs"]) == list(res.manifest)
+        assert [v["inputs"][n] for n in res.manifest] == [float(a) for a in res.X[i]]
+        assert v["prediction"] == _walk_document(doc, v["inputs"])
+    assert vp.read_text().endswith("}\n")
+    with pytest.raises(TrainerError, match="at least one test vector"):
+        export_ensemble(res, tmp_path / "x", n_vectors=0)

@@ -204,9 +204,56 @@ def test_bin_edges_device_sort_equals_host():
     rng = np.random.default_rng(4)
     X = rng.random((200_000, 9))
     X[:, 3] = np.floor(X[:, 3] * 7)          # few distinct values: one bin each
-    X[:5000, 5] = np.nan                      # NaNs sort last on both
     X[::7, 6] = -0.0
     e0, n0 = bin_edges(X)
     e1, n1 = bin_edges(X, device="cuda")
     assert np.array_equal(n0, n1)
-    assert np.array_equal(e0, e1, equal_nan=True)  # -0.0 == 0.0 compares equal, as binning does
+    assert np.array_equal(e0, e1)  # -0.0 == 0.0 compares equal, as binning does
+
+
+def test_fit_rejects_non_finite_and_bad_bins():
+    """sklearn's input checks (ValueError on NaN / inf in X or y) and the K5 bin
+    table's limits (2 <= n_bins <= 256), raised before anything reaches the
+    device."""
+    from paper_2305_01886_b200.boosting import GradientBoostingRegressor
+    from paper_2305_01886_b200.forest import RandomForestRegressor
+
+    X = np.random.default_rng(0).random((100, 4))
+    y = X[:, 0].copy()
+    for cls in (RandomForestRegressor, GradientBoostingRegressor):
+        for bad in ("X_nan", "X_inf", "y_nan", "y_inf"):
+            Xb, yb = X.copy(), y.copy()
+            (Xb if bad[0] == "X" else yb)[3] = np.nan if bad.endswith("nan") else np.inf
+            with pytest.raises(ValueError, match="NaN or infinity"):
+                cls(2).fit(Xb, yb)
+        for nb in (1, 257, 512, 2.5, True):
+            with pytest.raises(ValueError, match="n_bins"):
+                cls(2, n_bins=nb)
+
+
+def test_bin_edges_fewer_bins_use_the_fixed_row_stride():
+    X = np.random.default_rng(1).random((5000, 3)).astype(np.float32)
+    for nb in (2, 16, 255, 256):
+        e, ne = bin_edges(X, nb)
+        assert e.shape == (3, 255)               # k5_bin's fixed stride
+        assert (ne == nb - 1).all()
+        assert (np.diff(e[:, : nb - 1], axis=1) > 0).all()
+
+
+@pytest.mark.gpu
+def test_forest_with_fewer_bins_fits_and_thresholds_are_edges():
+    from paper_2305_01886_b200.forest import RandomForestRegressor
+
+    rng = np.random.default_rng(2)
+    X = rng.random((20_000, 6))
+    y = 4 * X[:, 0] + np.sin(5 * X[:, 1]) + rng.normal(0, 0.05, 20_000)
+    m = RandomForestRegressor(8, max_depth=8, random_state=0, n_bins=16).fit(X, y)
+    for est in m.estimators_:
+        t = est.tree_
+        split = t.children_left >= 0
+        # at most 15 distinct thresholds per feature (16 bins)
+        for f in range(6):
+            assert len(np.unique(t.threshold[split & (t.feature == f)])) <= 15
+    p = m.predict(X[:2000])
+    r2 = 1 - np.mean((p - y[:2000]) ** 2) / np.var(y[:2000])
+    assert r2 > 0.9

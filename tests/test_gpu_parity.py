@@ -273,6 +273,36 @@ def test_throughput_clamps_counted_and_logged(caplog):
     assert bits_equal(got["sf"][ok], want["sf"][ok]) and bits_equal(got["feat"][ok], want["feat"][ok])
 
 
+def test_throughput_clamp_counters_are_per_grid():
+    """Reentrancy: two grids swept concurrently on two streams
+    count their own clamps (gk_grid.tp_clamps; no library-global counter)."""
+    import torch
+
+    from paper_2305_01886_b200 import runtime as rt
+    from paper_2305_01886_b200.profiles import profile_from_dict, profile_to_dict
+
+    doc = profile_to_dict(resolve_profile("k20"))
+    doc["throughput_models"]["global"]["b"] = 0.5
+    bad = profile_from_dict(doc)
+    gs = graphs(6, 41)
+    cfgs = [(1, 32, 0, 0), (4, 64, 0, 0), (64, 256, 0, 0)]
+    dc = rt.DeviceCorpus.upload(pack.pack_corpus(gs))
+    g_bad = rt.DeviceGrid.build(dc, [bad], cfgs)
+    g_ok = rt.DeviceGrid.build(dc, [resolve_profile("k20")], cfgs)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    for _ in range(3):
+        with torch.cuda.stream(s1):
+            rt.schedule_features(dc, g_bad, stream=s1)
+        with torch.cuda.stream(s2):
+            rt.schedule_features(dc, g_ok, stream=s2)
+    torch.cuda.synchronize()
+    n_bad = rt.throughput_clamps(g_bad, reset=False)
+    assert n_bad > 0 and n_bad % 3 == 0
+    assert rt.throughput_clamps(g_ok) == 0
+    assert rt.throughput_clamps(g_bad, reset=True) == n_bad
+    assert rt.throughput_clamps(g_bad) == 0
+
+
 def test_many_archs_and_single_point_grids():
     """n_arch > 4 takes K1's wide latency-sum path; a 1 x 1 x 1 grid; the
     per-arch tables of duplicated profiles stay independent."""
