@@ -52,68 +52,88 @@ struct RfSplit {
 
 // ---------------------------------------------------------------- bootstrap
 
-// One warp per tree: MT19937 (init_genrand(seed)), tempering, numpy's masked
+// One CTA per tree: MT19937 (init_genrand(seed)), tempering, numpy's masked
 // rejection for randint(0, n) (mask = 2^bitlen(n-1) - 1, accept v <= n-1),
-// counts[v] += 1 for the first n accepted draws.
-__global__ void __launch_bounds__(128) k5_bootstrap(const uint32_t *__restrict__ seeds,
-                                                    int n_trees, int64_t n,
-                                                    uint32_t *__restrict__ counts) {
-    __shared__ uint32_t mt_s[4][624];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int t = blockIdx.x * 4 + w;
+// counts[v] += 1 for the first n accepted draws.  The whole forest's trees go
+// in one launch (a CTA per tree fills the GPU; one warp per tree in batches of
+// 16-32 trees left most SMs idle: 0.33 ms per tree).  Per 624-word round: the
+// twist in its three dependency phases ([0,227) reads old words, [227,454)
+// needs phase-1 results, [454,623) phase-2's, 623 needs the new mt[0]), one
+// thread per word and phase; then every thread tempers its word and a
+// CTA-wide ballot scan gives each accepted draw its position in the stream.
+constexpr int kBootThreads = 640;  // >= 624 words, 20 warps
+__global__ void __launch_bounds__(kBootThreads) k5_bootstrap(const uint32_t *__restrict__ seeds,
+                                                             int n_trees, int64_t n,
+                                                             uint32_t *__restrict__ counts) {
+    __shared__ uint32_t mt[624];
+    __shared__ int32_t wtot[kBootThreads / 32];
+    const int k = threadIdx.x, lane = k & 31, warp = k >> 5;
+    const int t = blockIdx.x;
     if (t >= n_trees) return;
-    uint32_t *mt = mt_s[w];
     uint32_t *cnt = counts + (size_t)t * n;
     const uint32_t rng = (uint32_t)(n - 1);
     if (rng == 0) {
-        if (lane == 0) cnt[0] = (uint32_t)n;
+        if (k == 0) cnt[0] = (uint32_t)n;
         return;
     }
     uint32_t mask = rng;
     mask |= mask >> 1; mask |= mask >> 2; mask |= mask >> 4; mask |= mask >> 8; mask |= mask >> 16;
-    if (lane == 0) {
-        mt[0] = seeds[t];
-        for (int i = 1; i < 624; i++) mt[i] = 1812433253u * (mt[i - 1] ^ (mt[i - 1] >> 30)) + (uint32_t)i;
+    if (k == 0) {  // init_genrand: a sequential recurrence, 624 steps
+        uint32_t v = seeds[t];
+        mt[0] = v;
+        for (int i = 1; i < 624; i++) {
+            v = 1812433253u * (v ^ (v >> 30)) + (uint32_t)i;
+            mt[i] = v;
+        }
     }
-    __syncwarp();
-    int64_t accepted = 0;
-    auto twist = [&](int k) {
-        const uint32_t y = (mt[k] & 0x80000000u) | (mt[(k + 1) % 624] & 0x7fffffffu);
-        return mt[(k + 397) % 624] ^ (y >> 1) ^ ((y & 1u) ? 0x9908b0dfu : 0u);
+    __syncthreads();
+    auto twist = [&](int i) {
+        const uint32_t y = (mt[i] & 0x80000000u) | (mt[(i + 1) % 624] & 0x7fffffffu);
+        return mt[(i + 397) % 624] ^ (y >> 1) ^ ((y & 1u) ? 0x9908b0dfu : 0u);
     };
+    int64_t accepted = 0;
     while (accepted < n) {
-        // twist in three dependency phases: [0,227) old operands, [227,454)
-        // needs phase-1 results, [454,623) needs phase-2, 623 needs mt[0] new
-        // (warp-uniform trip counts + full-mask syncs: every lane reads its
-        // operands before any lane of the chunk overwrites them)
-        const int phase_lo[3] = {0, 227, 454}, phase_hi[3] = {227, 454, 623};
-        for (int ph = 0; ph < 3; ph++) {
-            for (int k0 = phase_lo[ph]; k0 < phase_hi[ph]; k0 += 32) {
-                const int k = k0 + lane;
-                const bool in = k < phase_hi[ph];
-                const uint32_t v = in ? twist(k) : 0u;
-                __syncwarp();
-                if (in) mt[k] = v;
-                __syncwarp();
-            }
+        // phase p: words [lo_p, hi_p); each thread reads before any writes
+        {
+            const uint32_t v = k < 227 ? twist(k) : 0u;
+            __syncthreads();
+            if (k < 227) mt[k] = v;
+            __syncthreads();
         }
-        if (lane == 0) mt[623] = twist(623);
-        __syncwarp();
-        for (int k0 = 0; k0 < 624 && accepted < n; k0 += 32) {
-            const int k = k0 + lane;
-            uint32_t y = k < 624 ? mt[k] : 0u;
-            y ^= y >> 11;
-            y ^= (y << 7) & 0x9d2c5680u;
-            y ^= (y << 15) & 0xefc60000u;
-            y ^= y >> 18;
-            const uint32_t v = y & mask;
-            const bool ok = k < 624 && v <= rng;
-            const unsigned bal = __ballot_sync(GK_FULL, ok);
-            const int before = __popc(bal & ((1u << lane) - 1u));
-            if (ok && accepted + before < n) atomicAdd(cnt + v, 1u);
-            accepted += __popc(bal);
+        {
+            const uint32_t v = k < 227 ? twist(227 + k) : 0u;
+            __syncthreads();
+            if (k < 227) mt[227 + k] = v;
+            __syncthreads();
         }
-        __syncwarp();
+        {
+            const uint32_t v = k < 169 ? twist(454 + k) : 0u;
+            __syncthreads();
+            if (k < 169) mt[454 + k] = v;
+            __syncthreads();
+        }
+        if (k == 0) mt[623] = twist(623);
+        __syncthreads();
+        uint32_t y = k < 624 ? mt[k] : 0u;
+        y ^= y >> 11;
+        y ^= (y << 7) & 0x9d2c5680u;
+        y ^= (y << 15) & 0xefc60000u;
+        y ^= y >> 18;
+        const uint32_t v = y & mask;
+        const bool ok = k < 624 && v <= rng;
+        const unsigned bal = __ballot_sync(GK_FULL, ok);
+        if (lane == 0) wtot[warp] = __popc(bal);
+        __syncthreads();
+        int before = __popc(bal & ((1u << lane) - 1u)), total = 0;
+#pragma unroll
+        for (int w = 0; w < kBootThreads / 32; w++) {
+            const int c = wtot[w];
+            before += w < warp ? c : 0;
+            total += c;
+        }
+        if (ok && accepted + before < n) atomicAdd(cnt + v, 1u);
+        accepted += total;
+        __syncthreads();  // wtot / mt reuse
     }
 }
 
@@ -1197,7 +1217,8 @@ int gk_rf_bootstrap(const uint32_t *tree_seeds, uint32_t n_trees, int64_t n_rows
     }
     const cudaStream_t st = (cudaStream_t)stream;
     cudaMemsetAsync(counts, 0, sizeof(uint32_t) * (size_t)n_trees * n_rows, st);
-    gk::k5_bootstrap<<<(n_trees + 3) / 4, 128, 0, st>>>(tree_seeds, (int)n_trees, n_rows, counts);
+    if (n_trees == 0) return 0;
+    gk::k5_bootstrap<<<n_trees, gk::kBootThreads, 0, st>>>(tree_seeds, (int)n_trees, n_rows, counts);
     return gk_check_launch("k5_bootstrap");
 }
 

@@ -117,7 +117,10 @@ def broadcast_tensors(bufs: dict | None, src: int = 0, group=None, device=None) 
         bufs = {k: torch.empty(shape, dtype=getattr(torch, dt), device=dev)
                 for k, (shape, dt) in meta[0].items()}
     for k in sorted(bufs):
-        dist.broadcast(bufs[k], src=src, group=group)
+        # as raw bytes: collectives lack some dtypes (uint32 roots, uint16)
+        raw = bufs[k].view(-1).view(torch.uint8) if bufs[k].numel() else None
+        if raw is not None:
+            dist.broadcast(raw, src=src, group=group)
     return bufs
 
 
@@ -223,28 +226,93 @@ def _unpack_trees(buf: np.ndarray) -> dict:
     return out
 
 
+def _pack_trees_dev(items):
+    """[(tree id, device-resident TreeEstimator)] -> one int64 device tensor:
+    [n, n x (id, node_count, max_depth, random_state), per tree it (4 x nc)
+    then fl (4 x nc, f64 bits)] -- built with device copies only."""
+    import torch
+
+    from .runtime import device
+
+    dev = device()
+    hdr = torch.tensor([len(items)] + [v for t, e in items for v in
+                                       (t, e.tree_.node_count, e.tree_.max_depth,
+                                        int(e.random_state))], dtype=torch.int64, device=dev)
+    parts = [hdr]
+    for _, e in items:
+        fl, it = e.tree_.device_slices()
+        parts += [it.reshape(-1), fl.contiguous().view(torch.int64).reshape(-1)]
+    return torch.cat(parts)
+
+
+def _unpack_trees_dev(buf) -> dict:
+    import torch
+
+    from .forest import Tree, TreeBatch, TreeEstimator
+
+    n = int(buf[0].item())
+    if n == 0:
+        return {}
+    hdr = buf[1: 1 + 4 * n].view(n, 4).cpu().numpy()
+    at = 1 + 4 * n
+    fls, its = [], []
+    for t, nc, md, rs in hdr:
+        nc = int(nc)
+        its.append(buf[at: at + 4 * nc].view(4, nc))
+        fls.append(buf[at + 4 * nc: at + 8 * nc].view(4, nc).view(torch.float64))
+        at += 8 * nc
+    counts = hdr[:, 1].astype(np.int64)
+    base = np.concatenate([[0], np.cumsum(counts)[:-1]])
+    batch = TreeBatch(torch.cat(fls, dim=1), torch.cat(its, dim=1), base, counts, hdr[:, 2])
+    return {int(t): TreeEstimator(tree_=Tree(node_count=int(nc), max_depth=int(md), batch=batch,
+                                             start=int(b)), random_state=int(rs))
+            for (t, nc, md, rs), b in zip(hdr, base)}
+
+
 def allgather_forest(model, group=None, device=None):
     """Complete a tree-sharded forest on every rank: each rank's trees
-    (estimators_[t] for t % world == rank) are packed into one byte tensor and
-    all-gathered (NCCL over NVLink on the GPU box, gloo in the CPU tests), then
-    unpacked in global tree order."""
+    (estimators_[t] for t % world == rank) are packed into one buffer and
+    all-gathered, then unpacked in global tree order.  Device-resident trees
+    (the K5 fit's TreeBatch) on an NCCL group go device to device -- packed
+    by device copies, ncclAllGather over NVLink, unpacked into one TreeBatch
+    per source rank, no host round trip; host trees (or gloo groups) travel
+    as one host-packed byte buffer."""
     import torch
     import torch.distributed as dist
 
     mine = [(t, e) for t, e in enumerate(model.estimators_) if e is not None]
-    dev = device or (torch.device("cuda", torch.cuda.current_device())
-                     if dist.get_backend(group) == "nccl" else torch.device("cpu"))
-    buf = torch.from_numpy(_pack_trees(mine)).to(dev)
-    (gathered,) = allgather_results([buf], group=group)
+    nccl = dist.get_backend(group) == "nccl"
+    on_dev = nccl and all(e.tree_.on_device for _, e in mine)
+    flag = torch.tensor([int(on_dev)], dtype=torch.int64, device=collective_device(group))
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+    on_dev = bool(flag.item())
+    world = dist.get_world_size(group)
     merged = {}
-    # the concatenation is in rank order; each rank's part parses independently
-    sizes = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(dist.get_world_size(group))]
-    dist.all_gather(sizes, torch.tensor([buf.numel()], dtype=torch.int64, device=dev), group=group)
-    host = gathered.cpu().numpy()
-    at = 0
-    for sz in (int(s.item()) for s in sizes):
-        merged.update(_unpack_trees(host[at:at + sz]))
-        at += sz
+    if on_dev:
+        buf = _pack_trees_dev(mine)
+        sizes = [torch.zeros(1, dtype=torch.int64, device=buf.device) for _ in range(world)]
+        dist.all_gather(sizes, torch.tensor([buf.numel()], dtype=torch.int64, device=buf.device),
+                        group=group)
+        sizes = [int(v.item()) for v in sizes]
+        pad = torch.zeros(max(sizes), dtype=torch.int64, device=buf.device)
+        pad[: buf.numel()] = buf
+        out = torch.empty(world * max(sizes), dtype=torch.int64, device=buf.device)
+        dist.all_gather_into_tensor(out, pad, group=group)
+        for r, sz in enumerate(sizes):
+            merged.update(_unpack_trees_dev(out[r * max(sizes): r * max(sizes) + sz]))
+    else:
+        dev = device or collective_device(group)
+        buf = torch.from_numpy(_pack_trees(mine)).to(dev)
+        (gathered,) = allgather_results([buf], group=group)
+        # the concatenation is in rank order; each rank's part parses independently
+        sizes = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
+        dist.all_gather(sizes, torch.tensor([buf.numel()], dtype=torch.int64, device=dev),
+                        group=group)
+        host = gathered.cpu().numpy()
+        at = 0
+        for sz in (int(s.item()) for s in sizes):
+            merged.update(_unpack_trees(host[at:at + sz]))
+            at += sz
     if sorted(merged) != list(range(model.n_estimators)):
         raise RuntimeError("tree shards do not cover the forest")
     model.estimators_ = [merged[t] for t in range(model.n_estimators)]

@@ -37,6 +37,7 @@ SPLIT_DT = np.dtype({"names": ["feat", "bin", "n_left", "pad", "proxy"],
                      "formats": ["<i4", "<i4", "<i4", "<i4", "<f8"],
                      "offsets": [0, 4, 8, 12, 16], "itemsize": 24})
 TREE_LEAF, TREE_UNDEFINED = -1, -2
+_LEVEL_LOG = None   # set to a list to record per-level kernel times (tools/k5_levels.py)
 
 
 def _lib():
@@ -138,20 +139,148 @@ def check_finite(X: np.ndarray, y: np.ndarray) -> None:
         raise ValueError("Input y contains NaN or infinity.")
 
 
-@dataclass
-class Tree:
-    """The subset of sklearn's ``Tree`` the reference exporter reads."""
+_TREE_ARRAYS = ("children_left", "children_right", "feature", "threshold", "value", "impurity",
+                "n_node_samples", "weighted_n_node_samples")
 
-    node_count: int
-    children_left: np.ndarray
-    children_right: np.ndarray
-    feature: np.ndarray
-    threshold: np.ndarray
-    value: np.ndarray              # [node_count, 1, 1]
-    impurity: np.ndarray
-    n_node_samples: np.ndarray
-    weighted_n_node_samples: np.ndarray
-    max_depth: int
+
+class TreeBatch:
+    """The K5 output of one batch of trees, resident in HBM: fl [4, N] f64
+    (threshold, value, impurity, weighted_n_node_samples) and it [4, N] int64
+    (children_left, children_right, feature, n_node_samples), trees contiguous
+    from node_base[k].  A fitted forest keeps its trees here -- predict() walks
+    them on the device -- and copies them to host numpy arrays only when
+    something reads a ``tree_`` array (export, sklearn-style inspection):
+    one DMA per batch through a pinned staging buffer."""
+
+    _STAGE = 32 << 20   # bytes per staging buffer (two, alternating)
+
+    def __init__(self, fl_d, it_d, node_base, next_id, tree_depth):
+        import threading
+
+        self.fl_d, self.it_d = fl_d, it_d
+        self.node_base = np.asarray(node_base, np.int64)
+        self.next_id = np.asarray(next_id, np.int64)
+        self.tree_depth = np.asarray(tree_depth, np.int64)
+        self._host = None
+        self._nodes = None
+        self._lock = threading.Lock()
+
+    @property
+    def n_nodes(self) -> int:
+        return int(self.fl_d.shape[1])
+
+    def host(self):
+        """(fl, it) as host numpy arrays (copied once)."""
+        with self._lock:
+            if self._host is None:
+                self._host = (_to_host(self.fl_d), _to_host(self.it_d))
+        return self._host
+
+    def device_nodes(self, leaf_scale: float = 1.0):
+        """[N] gk_node records (16 B: {v, feature, left}) of the batch built on
+        the device: splits {threshold, feature, left}, leaves {value *
+        leaf_scale, -1, self - 1} (include/gk.h gk_node)."""
+        import torch
+
+        key = float(leaf_scale)
+        if self._nodes is not None and self._nodes[0] == key:
+            return self._nodes[1]
+        fl, it = self.fl_d, self.it_d
+        N = self.n_nodes
+        dev = fl.device
+        split = it[0] >= 0
+        tree = torch.repeat_interleave(torch.arange(len(self.next_id), device=dev),
+                                       torch.from_numpy(self.next_id).to(dev), output_size=N)
+        local = torch.arange(N, device=dev) - torch.from_numpy(self.node_base).to(dev)[tree]
+        rec = torch.empty((N, 4), dtype=torch.int32, device=dev)
+        v = torch.where(split, fl[0], fl[1] * key).contiguous()
+        rec[:, 0:2] = v.view(torch.int32).view(N, 2)
+        rec[:, 2] = torch.where(split, it[2], torch.full_like(it[2], -1)).to(torch.int32)
+        rec[:, 3] = torch.where(split, it[0], local - 1).to(torch.int32)
+        self._nodes = (key, rec)
+        return rec
+
+
+def _to_host(t) -> np.ndarray:
+    """Device tensor -> host numpy through two alternating pinned staging
+    buffers (DMA of chunk k + 1 overlaps the host copy of chunk k; a pageable
+    .cpu() ran at ~2 GB/s)."""
+    import torch
+
+    out = np.empty(tuple(t.shape), dtype=np.dtype(str(t.dtype).replace("torch.", "")))
+    src = t.contiguous().view(-1).view(torch.uint8)
+    dst = out.reshape(-1).view(np.uint8)
+    n = src.numel()
+    if n == 0:
+        return out
+    st = torch.cuda.current_stream()
+    cap = TreeBatch._STAGE
+    bufs = [torch.empty(min(cap, n), dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+    evs = [torch.cuda.Event(), torch.cuda.Event()]
+    chunks = [(a, min(n, a + cap)) for a in range(0, n, cap)]
+
+    def issue(k):
+        a, b = chunks[k]
+        bufs[k % 2][: b - a].copy_(src[a:b], non_blocking=True)
+        evs[k % 2].record(st)
+
+    issue(0)
+    for k, (a, b) in enumerate(chunks):
+        if k + 1 < len(chunks):   # its buffer was drained by chunk k - 1's host copy
+            issue(k + 1)
+        evs[k % 2].synchronize()
+        np.copyto(dst[a:b], bufs[k % 2][: b - a].numpy())
+    return out
+
+
+class Tree:
+    """The subset of sklearn's ``Tree`` the reference exporter reads
+    (``export.py:26-50``): node_count, max_depth and the per-node arrays
+    children_left / children_right / feature / threshold / value [n, 1, 1] /
+    impurity / n_node_samples / weighted_n_node_samples.  Built either from
+    host arrays or as a view of a device-resident :class:`TreeBatch`, whose
+    arrays are copied to the host on first access."""
+
+    def __init__(self, node_count: int, children_left=None, children_right=None, feature=None,
+                 threshold=None, value=None, impurity=None, n_node_samples=None,
+                 weighted_n_node_samples=None, max_depth: int = 0, *, batch=None, start: int = 0):
+        self.node_count = int(node_count)
+        self.max_depth = int(max_depth)
+        self._batch, self._start = batch, int(start)
+        self._arrays = None
+        if batch is None:
+            self._arrays = dict(children_left=children_left, children_right=children_right,
+                                feature=feature, threshold=threshold, value=value,
+                                impurity=impurity, n_node_samples=n_node_samples,
+                                weighted_n_node_samples=weighted_n_node_samples)
+
+    @property
+    def on_device(self) -> bool:
+        return self._batch is not None
+
+    def _load(self) -> dict:
+        if self._arrays is None:
+            fl, it = self._batch.host()
+            g = slice(self._start, self._start + self.node_count)
+            self._arrays = dict(children_left=it[0, g], children_right=it[1, g], feature=it[2, g],
+                                threshold=fl[0, g], value=fl[1, g].reshape(-1, 1, 1),
+                                impurity=fl[2, g], n_node_samples=it[3, g],
+                                weighted_n_node_samples=fl[3, g])
+        return self._arrays
+
+    def device_slices(self):
+        """(fl [4, n], it [4, n]) device views of a device-resident tree."""
+        g = slice(self._start, self._start + self.node_count)
+        return self._batch.fl_d[:, g], self._batch.it_d[:, g]
+
+
+def _tree_array(name):
+    return property(lambda self: self._load()[name], doc=f"sklearn Tree.{name}")
+
+
+for _n in _TREE_ARRAYS:
+    setattr(Tree, _n, _tree_array(_n))
+del _n
 
 
 @dataclass
@@ -284,10 +413,23 @@ class _LevelGrower:
             if n_b > n_big_cap:
                 raise RuntimeError("forest: big-task workspace undersized")
             big_chunks = -(-int(stats[5]) // MEDIUM) if n_b else 0
-            _check(L.gk_rf_split_level(
-                _ptr(D["Xb"]), _ptr(D["yfp"]), _ptr(D["y"]), _ptr(counts), n, F, _ptr(tasks_d),
-                lp, n_s, lp + 4 * cap, n_m, lp + 8 * cap, n_b, big_chunks,
-                _ptr(rows0), _ptr(rows1), _ptr(hist), _ptr(split_d), st))
+            if _LEVEL_LOG is not None:   # tuning aid: per-level, per-class device times
+                ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+                ev[0].record()
+                for c, (a, b_, cnt) in enumerate(((lp, 0, n_s), (lp + 4 * cap, 1, n_m),
+                                                  (lp + 8 * cap, 2, n_b))):
+                    args_ = [lp, 0, lp + 4 * cap, 0, lp + 8 * cap, 0]
+                    args_[2 * c + 1] = cnt
+                    _check(L.gk_rf_split_level(
+                        _ptr(D["Xb"]), _ptr(D["yfp"]), _ptr(D["y"]), _ptr(counts), n, F,
+                        _ptr(tasks_d), *args_, big_chunks, _ptr(rows0), _ptr(rows1), _ptr(hist),
+                        _ptr(split_d), st))
+                    ev[c + 1].record()
+            else:
+                _check(L.gk_rf_split_level(
+                    _ptr(D["Xb"]), _ptr(D["yfp"]), _ptr(D["y"]), _ptr(counts), n, F,
+                    _ptr(tasks_d), lp, n_s, lp + 4 * cap, n_m, lp + 8 * cap, n_b, big_chunks,
+                    _ptr(rows0), _ptr(rows1), _ptr(hist), _ptr(split_d), st))
             if len(cursor) < 2 * nt:
                 cursor = torch.empty(2 * nt, dtype=i32, device=dev)
             _check(L.gk_rf_partition_lists(
@@ -304,7 +446,17 @@ class _LevelGrower:
                 _ptr(tasks_d), _ptr(node_d), _ptr(split_d), nt, TB, depth + 1, max_depth,
                 _ptr(next_id_d), _ptr(lid_d), _ptr(tasks_n), _ptr(node_n), _ptr(lists_n),
                 2 * nt, _ptr(stats_d), _ptr(scratch), st))
+            if _LEVEL_LOG is not None:
+                ev[4].record()
+            prev = stats
             stats = stats_d.cpu().numpy().astype(np.int64)  # the level's one sync
+            if _LEVEL_LOG is not None:
+                _LEVEL_LOG.append(dict(depth=depth, n_small=n_s, n_med=n_m, n_big=n_b,
+                                       max_med=int(prev[4]), max_big=int(prev[5]),
+                                       small_ms=ev[0].elapsed_time(ev[1]),
+                                       med_ms=ev[1].elapsed_time(ev[2]),
+                                       big_ms=ev[2].elapsed_time(ev[3]),
+                                       part_next_ms=ev[3].elapsed_time(ev[4])))
             records.append((tasks_d, node_d, split_d, lid_d, nt, int(stats[0]) // 2))
             depth += 1
             if stats[0] == 0:
@@ -382,20 +534,16 @@ class _LevelGrower:
         val = s2 / w
         fl = torch.stack([torch.where(is_split, thr_t[feat.clamp(min=0), nbin],
                                       torch.full_like(w, float(TREE_UNDEFINED))),
-                          val, s3 / w - val * val, w]).cpu().numpy()
+                          val, s3 / w - val * val, w])
         it = torch.stack([left, torch.where(is_split, left + 1, torch.full_like(left, TREE_LEAF)),
-                          feat, ist[:, 0]]).cpu().numpy()
+                          feat, ist[:, 0]])
         leaf_value = (s2[gl] / w[gl]).cpu().numpy()
         tree_depth = depth_d.cpu().numpy()
         lv = lv_d.cpu().numpy().view(TASK_DT).reshape(-1)
-        trees = []
-        for k in range(TB):
-            g = slice(int(node_base[k]), int(node_base[k] + next_id[k]))
-            trees.append(Tree(node_count=int(next_id[k]), children_left=it[0, g],
-                              children_right=it[1, g], feature=it[2, g], threshold=fl[0, g],
-                              value=fl[1, g].reshape(-1, 1, 1), impurity=fl[2, g],
-                              n_node_samples=it[3, g], weighted_n_node_samples=fl[3, g],
-                              max_depth=int(tree_depth[k])))
+        # the trees stay in HBM (predict walks them there); host arrays on demand
+        batch = TreeBatch(fl, it, node_base, next_id, tree_depth)
+        trees = [Tree(node_count=int(next_id[k]), max_depth=int(tree_depth[k]), batch=batch,
+                      start=int(node_base[k])) for k in range(TB)]
         return trees, (lv, lv_d, leaf_value)
 
     def _grow_host(self, counts, base, m, rows0, rows1, TB):
@@ -698,7 +846,8 @@ class RandomForestRegressor(_LevelGrower):
 
     # -------------------------------------------------------------- predict
     def flat(self, leaf_scale: float = 1.0) -> FlatEnsemble:
-        """The forest in the device node layout (leaves scaled by leaf_scale)."""
+        """The forest in the device node layout (leaves scaled by leaf_scale),
+        as host arrays."""
         parts, offs, depths, off = [], [], [], 0
         for est in self.estimators_:
             t = est.tree_
@@ -718,14 +867,40 @@ class RandomForestRegressor(_LevelGrower):
                             manifest=tuple(f"f{i}" for i in range(F)),
                             tree_depth=np.asarray(depths, np.int32))
 
-    def predict(self, X) -> np.ndarray:
-        """Mean of the trees' predictions on float32-cast X (sklearn semantics)."""
+    def device_ensemble(self, leaf_scale: float = 1.0):
+        """The forest as a DeviceEnsemble (16-byte nodes) without a host round
+        trip when its trees are device-resident (TreeBatch.device_nodes);
+        trees read back to the host go through flat()."""
         import torch
 
-        from .runtime import DeviceEnsemble, device, rf_predict
+        from .runtime import DeviceEnsemble, _dev
+
+        ests = [e.tree_ for e in self.estimators_]
+        if not all(t.on_device for t in ests):
+            return DeviceEnsemble.upload(self.flat(leaf_scale), layout="nodes")
+        parts, offs, off = [], [], 0
+        for t in ests:
+            rec = t._batch.device_nodes(leaf_scale)
+            parts.append(rec[t._start: t._start + t.node_count])
+            offs.append(off)
+            off += t.node_count
+        nodes = torch.cat(parts).view(torch.uint8).view(-1)
+        F = self.n_features_in_
+        depths = np.asarray([t.max_depth for t in ests], np.int32)
+        bufs = {"nodes": nodes, "off": _dev(np.asarray(offs, np.int64)), "depth": _dev(depths),
+                "lo": _dev(np.zeros(F)), "hi": _dev(np.ones(F))}
+        return DeviceEnsemble.from_buffers(bufs, base=0.0, n_trees=len(ests), n_feat=F,
+                                           max_depth=int(depths.max()))
+
+    def predict(self, X) -> np.ndarray:
+        """Mean of the trees' predictions on float32-cast X (sklearn semantics),
+        walked on the device."""
+        import torch
+
+        from .runtime import device, rf_predict
 
         if getattr(self, "_flat", None) is None:
-            self._flat = DeviceEnsemble.upload(self.flat())
+            self._flat = self.device_ensemble()
         Xf = np.ascontiguousarray(np.asarray(X, dtype=np.float64).astype(np.float32), np.float64)
         total, _ = rf_predict(self._flat, torch.from_numpy(Xf).to(device()))
         return total.cpu().numpy() / len(self.estimators_)

@@ -175,7 +175,8 @@ def _bcast_tensors_fn(rank, world):
     if rank == 0:
         bufs = {"nodes": torch.arange(40, dtype=torch.uint8), "lo": torch.tensor([1.5, -2.0]),
                 "off": torch.tensor([0, 7, 19], dtype=torch.int64),
-                "blocks": torch.arange(24, dtype=torch.int32).view(3, 8)}
+                "blocks": torch.arange(24, dtype=torch.int32).view(3, 8),
+                "root": torch.tensor([1, 2 ** 31 + 5], dtype=torch.uint32)}
     got = broadcast_tensors(bufs)
     return {k: (str(v.dtype), tuple(v.shape), v.flatten().tolist()) for k, v in got.items()}
 
@@ -187,6 +188,7 @@ def test_broadcast_tensors_every_layout_buffer():
     assert out[0] == out[1]
     assert out[1]["blocks"] == ("torch.int32", (3, 8), list(range(24)))
     assert out[1]["lo"] == ("torch.float32", (2,), [1.5, -2.0])
+    assert out[1]["root"] == ("torch.uint32", (2,), [1, 2 ** 31 + 5])
 
 
 def test_chunk_shards_cover_the_corpus_in_order():

@@ -76,6 +76,31 @@ def test_device_bootstrap_matches_sklearn():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("n", [1_000_000, 1_048_577, 2])
+def test_device_bootstrap_matches_numpy_at_config3_scale(n):
+    """Config #3 draws n = 1M with a 20-bit rejection mask: counts are
+    bincount(RandomState(tree_seed).randint(0, n, n)) exactly (the draw
+    sklearn's _generate_sample_indices makes, SK/ensemble/_forest.py:95-112),
+    for the first trees of seed 0 (n = 2^20 + 1: a 21-bit mask rejecting ~half)."""
+    import torch
+
+    from paper_2305_01886_b200 import forest
+    from paper_2305_01886_b200.runtime import _ptr
+
+    L = forest._lib()
+    seeds = tree_seeds(0, 3)
+    sd = torch.tensor(seeds.astype(np.uint32).view(np.int32), device="cuda")
+    out = torch.empty(len(seeds) * n, dtype=torch.int32, device="cuda")
+    assert L.gk_rf_bootstrap(_ptr(sd), len(seeds), n, _ptr(out),
+                             torch.cuda.current_stream().cuda_stream) == 0
+    got = out.view(len(seeds), n).cpu().numpy()
+    for t, s in enumerate(seeds):
+        want = np.bincount(np.random.RandomState(int(s)).randint(0, n, n),
+                           minlength=n)
+        assert np.array_equal(got[t], want), t
+
+
+@pytest.mark.gpu
 def test_forest_fit_predict_and_export_roundtrip():
     from paper_2305_01886_b200.ensemble import flatten, load_ensemble
     from paper_2305_01886_b200.forest import RandomForestRegressor
@@ -257,3 +282,50 @@ def test_forest_with_fewer_bins_fits_and_thresholds_are_edges():
     p = m.predict(X[:2000])
     r2 = 1 - np.mean((p - y[:2000]) ** 2) / np.var(y[:2000])
     assert r2 > 0.9
+
+
+@pytest.mark.gpu
+def test_sharded_fits_merge_to_the_unsharded_forest():
+    """SURVEY §8(e) K5 by tree: fit(shard=(r, 2)) builds trees t % 2 == r from
+    the global seed sequence, so the two shards together are the unsharded
+    forest tree for tree (what dist.allgather_forest reassembles)."""
+    from paper_2305_01886_b200.forest import RandomForestRegressor
+
+    rng = np.random.default_rng(5)
+    X = rng.random((60_000, 10))
+    X[:, 8:] = np.floor(X[:, 8:] * 6)
+    y = 4 * X[:, 0] + np.sin(7 * X[:, 1]) + X[:, 8] + rng.normal(0, 0.1, 60_000)
+    full = RandomForestRegressor(9, max_depth=12, random_state=4).fit(X, y)
+    parts = [RandomForestRegressor(9, max_depth=12, random_state=4, shard=(r, 2)).fit(X, y)
+             for r in range(2)]
+    for t, est in enumerate(full.estimators_):
+        other = parts[t % 2].estimators_[t]
+        assert parts[1 - t % 2].estimators_[t] is None
+        assert other.random_state == est.random_state
+        for u, v in zip(_tree_arrays(est.tree_), _tree_arrays(other.tree_)):
+            assert np.array_equal(u, v)
+
+
+@pytest.mark.gpu
+def test_device_resident_trees_predict_and_read_back(monkeypatch):
+    """Fitted trees stay in HBM (TreeBatch): predict() builds the walk nodes
+    on the device; reading a tree_ array copies the batch to the host through
+    the pinned staging buffers (forced to many small chunks here); both agree
+    with a forest rebuilt from the host arrays."""
+    from paper_2305_01886_b200 import forest
+    from paper_2305_01886_b200.runtime import DeviceEnsemble
+
+    monkeypatch.setattr(forest.TreeBatch, "_STAGE", 4096 + 8)
+    rng = np.random.default_rng(6)
+    X = rng.random((30_000, 7))
+    y = 3 * X[:, 0] - X[:, 2] ** 2 + rng.normal(0, 0.05, 30_000)
+    m = forest.RandomForestRegressor(6, max_depth=10, random_state=1).fit(X, y)
+    assert all(e.tree_.on_device for e in m.estimators_)
+    p_dev = m.predict(X[:5000])
+    t = m.estimators_[0].tree_
+    fl_d, it_d = t.device_slices()
+    assert np.array_equal(t.threshold, fl_d[0].cpu().numpy())
+    assert np.array_equal(t.children_left, it_d[0].cpu().numpy())
+    assert t.value.shape == (t.node_count, 1, 1)
+    m._flat = DeviceEnsemble.upload(m.flat(), layout="blocks")   # host arrays -> blocked walk
+    assert np.array_equal(m.predict(X[:5000]), p_dev)
