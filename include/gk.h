@@ -281,7 +281,8 @@ int gk_rf_compact(const uint32_t *counts, uint32_t n_trees, int64_t n_rows,
 int gk_rf_bin(const double *X, int64_t n_rows, int32_t n_feat, int64_t ld, const float *edges,
               const int32_t *n_edges, uint8_t *Xb, uint32_t *bin_min, uint32_t *bin_max,
               void *stream);
-/* best split of every task (small / medium / big index lists) */
+/* best split of every task (small / medium / big index lists); split.n_left is
+ * NOT filled (the partition's cursor gives the left row count) */
 int gk_rf_split_level(const uint8_t *Xb, const int64_t *yfp, const double *y,
                       const uint32_t *counts, int64_t n_rows, int32_t n_feat,
                       const void *tasks, const int32_t *small_ids, int32_t n_small,
@@ -289,7 +290,8 @@ int gk_rf_split_level(const uint8_t *Xb, const int64_t *yfp, const double *y,
                       int32_t n_big, int32_t big_max_chunks, const int32_t *rows0,
                       const int32_t *rows1, void *hist_ws, void *split_out, void *stream);
 size_t gk_rf_hist_bytes(int32_t n_big, int32_t n_feat);
-/* move each split task's rows to [begin, begin+n_left) / [.., end) of the other buffer */
+/* move each split task's rows to the other buffer: left rows up from begin, right
+ * rows down from end; cursor[2*i] ends as task i's left row count (n_left) */
 int gk_rf_partition(const uint8_t *Xb, const int64_t *yfp, const double *y,
                     const uint32_t *counts, int64_t n_rows, int32_t n_feat, const void *tasks,
                     int32_t n_tasks, const void *split, const int32_t *ids, int32_t n_ids,
@@ -298,7 +300,9 @@ int gk_rf_partition(const uint8_t *Xb, const int64_t *yfp, const double *y,
 /* The level loop's bookkeeping on the device (replaces the per-level host
  * bookkeeping of the tree builder; sklearn's BestFirst/DepthFirst builders,
  * SK/tree/_tree.pyx, grow node by node).  From one level's tasks (sorted by
- * tree), node ids and splits: split task i gets children at 2*excl[i] and
+ * tree), node ids, splits and the partition's cursors (cursor[2*i] = split
+ * task i's left row count, after gk_rf_partition_lists): split task i gets
+ * children at 2*excl[i] and
  * 2*excl[i]+1 of tasks_next / node_next (excl = split tasks before i) with BFS
  * ids lid = next_id[tree] + 2*(rank among the tree's split tasks), written to
  * lid_out[i] (-1 when task i is a leaf); next_id advances; children with >= 2
@@ -307,10 +311,11 @@ int gk_rf_partition(const uint8_t *Xb, const int64_t *yfp, const double *y,
  * task count, the three list lengths, largest medium / big child.  scratch:
  * gk_rf_level_scratch_bytes. */
 size_t gk_rf_level_scratch_bytes(int32_t n_tasks, int32_t n_trees);
-int gk_rf_next_level(const void *tasks, const int32_t *node, const void *split, int32_t n_tasks,
-                     int32_t n_trees, int32_t child_depth, int32_t max_depth, int32_t *next_id,
-                     int32_t *lid_out, void *tasks_next, int32_t *node_next, int32_t *lists,
-                     int32_t list_cap, int32_t *stats, void *scratch, void *stream);
+int gk_rf_next_level(const void *tasks, const int32_t *node, const void *split,
+                     const int32_t *cursor, int32_t n_tasks, int32_t n_trees, int32_t child_depth,
+                     int32_t max_depth, int32_t *next_id, int32_t *lid_out, void *tasks_next,
+                     int32_t *node_next, int32_t *lists, int32_t list_cap, int32_t *stats,
+                     void *scratch, void *stream);
 /* gk_rf_partition over a level's three search lists (searched tasks that stayed
  * leaves are skipped); cursor: 2 * n_tasks int32, zeroed here */
 int gk_rf_partition_lists(const uint8_t *Xb, const uint32_t *counts, int64_t n_rows,

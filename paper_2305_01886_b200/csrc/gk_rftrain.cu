@@ -207,35 +207,42 @@ __device__ __forceinline__ bool better(double p, int f, int b, const BestSplit &
 // 64-bit shared-memory atomic add (ATOMS.CAST.SPIN.64 CAS loops were 60 % of
 // the node-split instructions); 32-bit adds are native, and the carry out of
 // the low word is recovered from the returned old value -- exact.
-struct BinsRef {
+template <bool kCnt>
+struct BinsT {
     uint32_t *cnt, *wgt, *slo;
     int32_t *shi;
+    // (row count << 32 | weight); without a count word (the CTA-per-node and
+    // multi-CTA paths) the weight stands in for the count: every row of a
+    // node has weight >= 1, so "both sides non-empty" is the same test, and
+    // the split's row count comes from the partition's cursor instead
     __device__ __forceinline__ uint64_t cw(int b) const {
-        return ((uint64_t)cnt[b] << 32) | wgt[b];
+        return kCnt ? (((uint64_t)cnt[b] << 32) | wgt[b]) : (((uint64_t)wgt[b] << 32) | wgt[b]);
     }
     __device__ __forceinline__ int64_t sum(int b) const {
         return (int64_t)(((uint64_t)(uint32_t)shi[b] << 32) + slo[b]);
     }
     __device__ __forceinline__ void add(int b, uint32_t w, int64_t sv) const {
-        atomicAdd(cnt + b, 1u);
+        if (kCnt) atomicAdd(cnt + b, 1u);
         atomicAdd(wgt + b, w);
         const uint32_t lo = (uint32_t)sv;
         const uint32_t old = atomicAdd(slo + b, lo);
         atomicAdd(shi + b, (int32_t)(sv >> 32) + (old + lo < old ? 1 : 0));
     }
     __device__ __forceinline__ void clear(int b) const {
-        cnt[b] = 0;
+        if (kCnt) cnt[b] = 0;
         wgt[b] = 0;
         slo[b] = 0;
         shi[b] = 0;
     }
     __device__ __forceinline__ void set(int b, uint64_t c, int64_t sv) const {
-        cnt[b] = (uint32_t)(c >> 32);
+        if (kCnt) cnt[b] = (uint32_t)(c >> 32);
         wgt[b] = (uint32_t)c;
         slo[b] = (uint32_t)sv;
         shi[b] = (int32_t)(sv >> 32);
     }
 };
+using BinsRef = BinsT<true>;
+using Bins3 = BinsT<false>;
 
 struct CandSmem {  // one warp's compacted split candidates (<= 64)
     uint64_t c[64];
@@ -243,8 +250,8 @@ struct CandSmem {  // one warp's compacted split candidates (<= 64)
     uint16_t b[64];
 };
 
-template <bool kCompact>
-__device__ __forceinline__ BestSplit eval_feature(const BinsRef &H, int f, int lane,
+template <bool kCompact, class Bins>
+__device__ __forceinline__ BestSplit eval_feature(const Bins &H, int f, int lane,
                                                   CandSmem *cc) {
     uint64_t c8[8];
     int64_t s8[8];
@@ -355,36 +362,62 @@ __device__ __forceinline__ void finish_split(const BestSplit &b, double parent, 
     *out = r;
 }
 
+// CTA-per-node / multi-CTA histograms: three 32-bit words per bin (weight,
+// low / high word of the fixed-point sum of w * y; no row count, see BinsT)
 struct HistSmem {
-    uint32_t cnt[kFC][kBins];  // rows
     uint32_t wgt[kFC][kBins];  // bootstrap weight
     uint32_t slo[kFC][kBins];  // sum of w * y (fixed point), low word
-    int32_t shi[kFC][kBins];   //   high word (BinsRef)
+    int32_t shi[kFC][kBins];   //   high word
     BestSplit best[8];
     double parent;
-    __device__ __forceinline__ BinsRef feat(int j) {
-        return BinsRef{cnt[j], wgt[j], slo[j], shi[j]};
+    __device__ __forceinline__ Bins3 feat(int j) {
+        return Bins3{nullptr, wgt[j], slo[j], shi[j]};
     }
 };
 
-// add one task's rows [p0, p1) to the shared histograms of feature chunk fc
+// add one task's rows [p0, p1) to the shared histograms of feature chunk fc.
+// Per row: the 16 bins in one 16-byte load, then every feature's returning
+// low-word atomic is issued before any dependent high-word add -- 16
+// independent round trips in flight instead of a return-then-add chain per
+// feature (the SASS had one ATOMS latency per feature: issue active 7 %).
 __device__ __forceinline__ void accumulate(HistSmem &H, const RfTrainData &D, const RfTask &T,
                                            const int32_t *__restrict__ rows, int p0, int p1,
                                            int fc) {
     const int f0 = fc * kFC, nf = min(kFC, D.F - f0);
     const uint32_t *cnt = D.counts + (size_t)T.tree * D.n;
+    const bool vec = nf == kFC && (D.F & 15) == 0;  // CTA-uniform
     for (int p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
         const int32_t r = rows[p];
         const uint32_t w = cnt[r];
         const int64_t sv = (int64_t)w * D.yfp[r];
         const uint8_t *xb = D.Xb + (size_t)r * D.F + f0;
-        for (int j = 0; j < nf; j++) H.feat(j).add(xb[j], w, sv);
+        const uint32_t lo = (uint32_t)sv;
+        const int32_t hi = (int32_t)(sv >> 32);
+        if (vec) {
+            const uint4 q = *reinterpret_cast<const uint4 *>(xb);
+            const uint32_t qw[4] = {q.x, q.y, q.z, q.w};
+            uint32_t old[kFC];
+#pragma unroll
+            for (int j = 0; j < kFC; j++) {
+                const int b = (qw[j >> 2] >> (8 * (j & 3))) & 0xFF;
+                atomicAdd(&H.wgt[j][b], w);
+                old[j] = atomicAdd(&H.slo[j][b], lo);
+            }
+#pragma unroll
+            for (int j = 0; j < kFC; j++) {
+                const int b = (qw[j >> 2] >> (8 * (j & 3))) & 0xFF;
+                atomicAdd(&H.shi[j][b], hi + (old[j] + lo < old[j] ? 1 : 0));
+            }
+        } else {
+            for (int j = 0; j < nf; j++) H.feat(j).add(xb[j], w, sv);
+        }
     }
 }
 
 __device__ __forceinline__ void zero_hist(HistSmem &H) {
-    uint4 *a = reinterpret_cast<uint4 *>(&H.cnt[0][0]);  // the four word arrays are contiguous
-    for (int i = threadIdx.x; i < kFC * kBins; i += blockDim.x) a[i] = make_uint4(0, 0, 0, 0);
+    uint4 *a = reinterpret_cast<uint4 *>(&H.wgt[0][0]);  // the word arrays are contiguous
+    for (int i = threadIdx.x; i < 3 * kFC * kBins / 4; i += blockDim.x)
+        a[i] = make_uint4(0, 0, 0, 0);
 }
 
 // evaluate the kFC features in shared memory; fold into H.best[warp]
@@ -417,7 +450,7 @@ __device__ __forceinline__ void parent_proxy(HistSmem &H) {
     if (threadIdx.x < 32) {
         uint64_t c = 0;
         int64_t s = 0;
-        const BinsRef f0 = H.feat(0);
+        const Bins3 f0 = H.feat(0);
         for (int b = threadIdx.x; b < kBins; b += 32) {
             c += f0.cw(b);
             s += f0.sum(b);
@@ -450,7 +483,7 @@ struct MidSmem {
     int32_t row[kMidRows];
     uint32_t w[kMidRows];
     int64_t s[kMidRows];
-    uint32_t cnt[8][kBins], wgt[8][kBins], slo[8][kBins];
+    uint32_t wgt[8][kBins], slo[8][kBins];
     int32_t shi[8][kBins];
     uint16_t cbin[8][kBins];
     uint32_t bmap[8][8], bpre[8][8];
@@ -470,7 +503,7 @@ __device__ __noinline__ void split_mid(const RfTrainData &D, const RfTask &T,
         M.W = 0;
         M.S = 0;
     }
-    const BinsRef hb{M.cnt[warp], M.wgt[warp], M.slo[warp], M.shi[warp]};
+    const Bins3 hb{nullptr, M.wgt[warp], M.slo[warp], M.shi[warp]};
 #pragma unroll
     for (int j = 0; j < kBins / 32; j++) hb.clear(lane + 32 * j);
     if (lane < 8) M.bmap[warp][lane] = 0u;
@@ -602,7 +635,7 @@ __device__ __noinline__ void split_mid(const RfTrainData &D, const RfTask &T,
         finish_split(b, S * S / (double)M.W, out);
     }
 }
-static_assert(sizeof(MidSmem) <= sizeof(HistSmem), "the mid path reuses the medium smem");
+constexpr size_t kMedSmem = sizeof(MidSmem) > sizeof(HistSmem) ? sizeof(MidSmem) : sizeof(HistSmem);
 
 // medium tasks: one CTA per task, feature chunks in sequence
 #ifndef GK_MED_MINB
@@ -660,9 +693,9 @@ __global__ void __launch_bounds__(256) k5_hist_big(RfTrainData D, const RfTask *
     uint64_t *dcw = gcw + ((size_t)bi * D.F + f0) * kBins;
     int64_t *ds = gs + ((size_t)bi * D.F + f0) * kBins;
     for (int i = threadIdx.x; i < nf * kBins; i += blockDim.x) {
-        const BinsRef hb = H.feat(i / kBins);
+        const Bins3 hb = H.feat(i / kBins);
         const int b = i % kBins;
-        const uint64_t c = hb.cw(b);
+        const uint32_t c = hb.wgt[b];
         if (c) {
             atomicAdd((unsigned long long *)(dcw + i), (unsigned long long)c);
             atomicAdd((unsigned long long *)(ds + i), (unsigned long long)hb.sum(b));
@@ -830,11 +863,11 @@ __global__ void __launch_bounds__(128, GK_SMALL_MINB) k5_split_small(RfTrainData
     // (proxy, feature, bin) order as the 256-bin scan.
     constexpr int kE = kSmallRpl;
     constexpr int kN = 32 * kE;
-    __shared__ uint32_t ccnt[4][kN], cwgt[4][kN], cslo[4][kN];
+    __shared__ uint32_t cwgt[4][kN], cslo[4][kN];
     __shared__ int32_t cshi[4][kN];
     __shared__ uint16_t cbin[4][kN];
     __shared__ uint32_t bmap[4][8], bpre[4][8];
-    const BinsRef hb{ccnt[wib], cwgt[wib], cslo[wib], cshi[wib]};
+    const Bins3 hb{nullptr, cwgt[wib], cslo[wib], cshi[wib]};
 #pragma unroll
     for (int j = 0; j < kE; j++) hb.clear(lane * kE + j);
     if (lane < 8) bmap[wib][lane] = 0u;
@@ -947,8 +980,10 @@ __global__ void __launch_bounds__(128, GK_SMALL_MINB) k5_split_small(RfTrainData
 
 // ---------------------------------------------------------------- partition
 
-// CTA = (task, 4096-position chunk); rows of split tasks scatter to
-// [begin, begin + n_left) / [begin + n_left, end) of the other buffer
+// CTA = (task, 256-position chunk); rows of split tasks scatter to the other
+// buffer: left rows up from `begin`, right rows down from `end` (so no row
+// count is needed up front); the final left cursor is the split's n_left,
+// read by the next-level bookkeeping (k5_level_emit)
 __global__ void __launch_bounds__(256) k5_partition(RfTrainData D, const RfTask *__restrict__ tasks,
                                                     const RfSplit *__restrict__ split,
                                                     const int32_t *__restrict__ task_ids,
@@ -980,7 +1015,7 @@ __global__ void __launch_bounds__(256) k5_partition(RfTrainData D, const RfTask 
     rb = __shfl_sync(GK_FULL, rb, 0);
     const unsigned below = (1u << lane) - 1u;
     if (left) outp[T.begin + lb + __popc(bl & below)] = r;
-    if (right) outp[T.begin + sp.n_left + rb + __popc(br & below)] = r;
+    if (right) outp[T.end - 1 - (rb + __popc(br & below))] = r;
 }
 
 // ---------------------------------------------------------------- next level
@@ -1090,8 +1125,8 @@ __device__ __forceinline__ void append_class(int cls, int k, int32_t *__restrict
 __global__ void __launch_bounds__(kLvlThreads) k5_level_emit(
     const RfTask *__restrict__ tasks, const int32_t *__restrict__ node,
     const RfSplit *__restrict__ split, int n_tasks, const int32_t *__restrict__ block_excl,
-    const int32_t *__restrict__ lid_base, int child_depth, int max_depth,
-    int32_t *__restrict__ lid_out, RfTask *__restrict__ tasks_next,
+    const int32_t *__restrict__ lid_base, const int32_t *__restrict__ cursor, int child_depth,
+    int max_depth, int32_t *__restrict__ lid_out, RfTask *__restrict__ tasks_next,
     int32_t *__restrict__ node_next, int32_t *__restrict__ lists, int cap,
     int32_t *__restrict__ stats) {
     __shared__ int32_t wsum[kLvlThreads / 32];
@@ -1112,12 +1147,13 @@ __global__ void __launch_bounds__(kLvlThreads) k5_level_emit(
         const RfTask T = tasks[i];
         const int32_t lid = lid_base[T.tree] + 2 * excl;
         lid_out[i] = lid;
-        const int mid = T.begin + sp.n_left;
+        const int n_left = cursor[2 * i];   // the partition's final left count
+        const int mid = T.begin + n_left;
         tasks_next[2 * excl] = RfTask{T.tree, T.begin, mid, 1 - T.parity};
         tasks_next[2 * excl + 1] = RfTask{T.tree, mid, T.end, 1 - T.parity};
         node_next[2 * excl] = lid;
         node_next[2 * excl + 1] = lid + 1;
-        sz_l = sp.n_left;
+        sz_l = n_left;
         sz_r = T.end - mid;
         const bool deep_ok = child_depth < max_depth;
         cls_l = (deep_ok && sz_l >= 2) ? (sz_l > kSmallRows) + (sz_l > kMedRows) : -1;
@@ -1256,9 +1292,10 @@ int gk_rf_split_level(const uint8_t *Xb, const int64_t *yfp, const double *y,
     gk::RfTrainData D{Xb, yfp, y, counts, n_rows, n_feat};
     const gk::RfTask *T = (const gk::RfTask *)tasks;
     gk::RfSplit *out = (gk::RfSplit *)split_out;
-    const size_t smem = sizeof(gk::HistSmem);
-    static const bool attr = [smem] {  // thread-safe one-time init (concurrent tree batches)
-        cudaFuncSetAttribute(gk::k5_split_medium, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const size_t smem = sizeof(gk::HistSmem), smem_med = gk::kMedSmem;
+    static const bool attr = [smem, smem_med] {  // thread-safe one-time init (concurrent tree batches)
+        cudaFuncSetAttribute(gk::k5_split_medium, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem_med);
         cudaFuncSetAttribute(gk::k5_split_medium, cudaFuncAttributePreferredSharedMemoryCarveout,
                              cudaSharedmemCarveoutMaxShared);
         cudaFuncSetAttribute(gk::k5_hist_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1270,7 +1307,7 @@ int gk_rf_split_level(const uint8_t *Xb, const int64_t *yfp, const double *y,
         gk::k5_split_small<<<(n_small * 32 + 127) / 128, 128, 0, st>>>(D, T, small_ids, n_small,
                                                                        rows0, rows1, out);
     if (n_med > 0)
-        gk::k5_split_medium<<<n_med, 256, smem, st>>>(D, T, med_ids, rows0, rows1, out);
+        gk::k5_split_medium<<<n_med, 256, smem_med, st>>>(D, T, med_ids, rows0, rows1, out);
     if (n_big > 0) {
         uint64_t *gcw = (uint64_t *)hist_ws;
         int64_t *gs = (int64_t *)(gcw + (size_t)n_big * n_feat * gk::kBins);
@@ -1317,10 +1354,11 @@ size_t gk_rf_level_scratch_bytes(int32_t n_tasks, int32_t n_trees) {
     return sizeof(int32_t) * (nb + 2 * (size_t)n_trees + 8);
 }
 
-int gk_rf_next_level(const void *tasks, const int32_t *node, const void *split, int32_t n_tasks,
-                     int32_t n_trees, int32_t child_depth, int32_t max_depth, int32_t *next_id,
-                     int32_t *lid_out, void *tasks_next, int32_t *node_next, int32_t *lists,
-                     int32_t list_cap, int32_t *stats, void *scratch, void *stream) {
+int gk_rf_next_level(const void *tasks, const int32_t *node, const void *split,
+                     const int32_t *cursor, int32_t n_tasks, int32_t n_trees, int32_t child_depth,
+                     int32_t max_depth, int32_t *next_id, int32_t *lid_out, void *tasks_next,
+                     int32_t *node_next, int32_t *lists, int32_t list_cap, int32_t *stats,
+                     void *scratch, void *stream) {
     if (n_tasks < 0 || n_trees < 1 || list_cap < 2 * (int64_t)n_tasks) {
         gk_set_error("gk_rf_next_level: bad sizes (n_tasks %d, n_trees %d, list_cap %d)", n_tasks,
                      n_trees, list_cap);
@@ -1339,7 +1377,7 @@ int gk_rf_next_level(const void *tasks, const int32_t *node, const void *split, 
     gk::k5_level_count<<<nb, gk::kLvlThreads, 0, st>>>(T, S, n_tasks, block_cnt, tree_cnt);
     gk::k5_level_scan<<<1, 1024, 0, st>>>(block_cnt, nb, tree_cnt, n_trees, next_id, lid_base, stats);
     gk::k5_level_emit<<<nb, gk::kLvlThreads, 0, st>>>(T, node, S, n_tasks, block_cnt, lid_base,
-                                                       child_depth, max_depth, lid_out,
+                                                       cursor, child_depth, max_depth, lid_out,
                                                        (gk::RfTask *)tasks_next, node_next, lists,
                                                        list_cap, stats);
     return gk_check_launch("k5_next_level");

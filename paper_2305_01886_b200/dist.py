@@ -71,8 +71,12 @@ class ResultGather:
     def run(self, tensors: list) -> list:
         import torch.distributed as dist
 
+        nccl = dist.get_backend(self.group) == "nccl"
         for o, t in zip(self.out, tensors):
-            dist.all_gather_into_tensor(o, t.contiguous(), group=self.group)
+            if nccl:
+                dist.all_gather_into_tensor(o, t.contiguous(), group=self.group)
+            else:   # gloo (CPU tests, the 2-rank one-GPU bench test): list form
+                dist.all_gather(list(o.chunk(self.world)), t.contiguous(), group=self.group)
         return self.out
 
 
@@ -139,7 +143,12 @@ def broadcast_device_ensemble(de, src: int = 0, group=None):
         meta = [dict(base=float(de.desc.base_score), n_trees=int(de.desc.n_trees),
                      n_feat=int(de.desc.n_feat), max_depth=int(de.desc.max_depth))]
     dist.broadcast_object_list(meta, src=src, group=group)
-    bufs = broadcast_tensors(de.bufs if rank == src else None, src=src, group=group)
+    import torch
+
+    # the buffers stay device buffers whatever the backend (gloo ships CUDA
+    # tensors through the host; NCCL device to device)
+    bufs = broadcast_tensors(de.bufs if rank == src else None, src=src, group=group,
+                             device=torch.device("cuda", torch.cuda.current_device()))
     if rank == src:
         return de
     return DeviceEnsemble.from_buffers(bufs, **meta[0])

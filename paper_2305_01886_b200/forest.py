@@ -58,8 +58,8 @@ def _lib():
         L.gk_rf_leaf_stats.argtypes = [vp, i64, vp, vp, vp, i32, vp, vp, vp, i32, vp]
         L.gk_rf_level_scratch_bytes.argtypes = [i32, i32]
         L.gk_rf_level_scratch_bytes.restype = C.c_size_t
-        L.gk_rf_next_level.argtypes = [vp, vp, vp, i32, i32, i32, i32, vp, vp, vp, vp, vp, i32,
-                                       vp, vp, vp]
+        L.gk_rf_next_level.argtypes = [vp, vp, vp, vp, i32, i32, i32, i32, vp, vp, vp, vp, vp,
+                                       i32, vp, vp, vp]
         L.gk_rf_partition_lists.argtypes = [vp, vp, i64, i32, vp, i32, vp, vp, i32, vp, i32, i32,
                                             vp, i32, i32, vp, vp, vp, vp]
         L._rf_bound = True
@@ -443,7 +443,8 @@ class _LevelGrower:
             scratch = torch.empty(int(L.gk_rf_level_scratch_bytes(nt, TB)), dtype=torch.uint8,
                                   device=dev)
             _check(L.gk_rf_next_level(
-                _ptr(tasks_d), _ptr(node_d), _ptr(split_d), nt, TB, depth + 1, max_depth,
+                _ptr(tasks_d), _ptr(node_d), _ptr(split_d), _ptr(cursor), nt, TB, depth + 1,
+                max_depth,
                 _ptr(next_id_d), _ptr(lid_d), _ptr(tasks_n), _ptr(node_n), _ptr(lists_n),
                 2 * nt, _ptr(stats_d), _ptr(scratch), st))
             if _LEVEL_LOG is not None:
@@ -623,7 +624,7 @@ class _LevelGrower:
             lid = next_id[pt] + 2 * rank
             next_id += 2 * np.bincount(pt, minlength=TB)
             splits.append((pt, pn, sp["feat"][s], sp["bin"][s], lid))
-            nl = sp["n_left"][s].astype(np.int32)
+            nl = cursor[: 2 * nt].view(nt, 2)[:, 0].cpu().numpy()[s].astype(np.int32)
             cb = np.empty(2 * len(pt), np.int32)
             ce = np.empty(2 * len(pt), np.int32)
             cb[0::2], ce[0::2] = t_begin[s], t_begin[s] + nl

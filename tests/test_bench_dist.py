@@ -34,7 +34,8 @@ def test_bench_torchrun_two_ranks_gloo_on_one_gpu():
            "--no-c4", "--cpu-seconds", "1", "--e2e-steps", "1"]
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900,
                        env=dict(os.environ, OMP_NUM_THREADS="2"))
-    assert r.returncode == 0, r.stderr[-3000:]
+    errs = [ln for ln in r.stderr.splitlines() if "Error" in ln or "error" in ln]
+    assert r.returncode == 0, "\n".join(errs[:30]) + "\n" + r.stderr[-2000:]
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
     assert len(lines) == 1, r.stdout[-2000:]          # rank 0 prints one line
     d = json.loads(lines[0])
