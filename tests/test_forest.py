@@ -329,3 +329,34 @@ def test_device_resident_trees_predict_and_read_back(monkeypatch):
     assert t.value.shape == (t.node_count, 1, 1)
     m._flat = DeviceEnsemble.upload(m.flat(), layout="blocks")   # host arrays -> blocked walk
     assert np.array_equal(m.predict(X[:5000]), p_dev)
+
+
+def test_config3_golden_present():
+    ref = json.loads((G / "trainer_rf_c3.json").read_text())
+    assert ref["n_rows"] == 200_000 and ref["n_estimators"] == 32 and ref["max_depth"] == 16
+    assert len(ref["folds"]) == 5 and len(ref["fold_mape_pct"]) == 5
+    assert ref["generator"] == "paper_2305_01886_b200.workloads.config3_table"
+
+
+@pytest.mark.gpu
+def test_train_parity_config3_shape():
+    """BASELINE config #3's distribution (56 continuous columns with ~200k
+    distinct values each + 8 count columns; 256 quantile bins vs sklearn's
+    exact midpoints) at 200k x 64, 32 trees, depth 16: fold-mean R^2 within
+    0.005 and MAPE within 0.5 pp of the reference train() (golden
+    tests/golden/trainer_rf_c3.json, scikit-learn 1.9.0 behind the
+    reference's _make_model, same KFold folds)."""
+    from paper_2305_01886_b200.trainer import train
+    from paper_2305_01886_b200.workloads import config3_table
+
+    ref = json.loads((G / "trainer_rf_c3.json").read_text())
+    X, y = config3_table(ref["n_rows"], ref["frame_seed"])
+    names = tuple(f"f{i:02d}" for i in range(X.shape[1]))
+    res = train((X, y, names), "random_forest", n_estimators=ref["n_estimators"],
+                max_depth=ref["max_depth"], seed=ref["seed"])
+    r2 = res.mean_metrics.r2
+    mape = float(np.mean(res.fold_mape_pct))
+    assert abs(r2 - ref["mean"]["r2"]) <= 0.005, (r2, ref["mean"]["r2"])
+    assert abs(mape - ref["mean_mape_pct"]) <= 0.5, (mape, ref["mean_mape_pct"])
+    for got, want in zip(res.fold_metrics, ref["folds"]):   # every fold, not just the mean
+        assert abs(got.r2 - want["r2"]) <= 0.005
