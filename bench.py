@@ -51,18 +51,25 @@ BOUNDS_KERNELS = 500   # ensemble scaling bounds come from the corpus' first gen
 
 def ncu_traffic(workload: str, kernel: str, units: int):
     """DRAM bytes per launch of `kernel` from the committed ncu capture
-    (profiles/r2/traffic.json), scaled per unit to this launch's size."""
+    (profiles/r2/traffic.json), scaled per unit to this launch's size, and the
+    binding unit's utilisation in that capture."""
     try:
         rec = json.loads(TRAFFIC.read_text())[workload][kernel]
     except Exception:
-        return None, None
+        return None, None, None
     per_unit = (rec["read"] + rec["write"]) / rec["units"]
     src = f"ncu --set full, {rec['capture']}"
     if rec["units"] != units:
         src += f"; scaled from {rec['units']} to {units} {rec['unit']}s"
-    if rec.get("binding"):
-        src += f"; binding unit (ncu): {rec['binding']}"
-    return per_unit * units, src
+    binding = None
+    if rec.get("l1tex_pct_of_peak") is not None:
+        binding = {"unit": "L1/TEX (LSU data pipe: table loads + node gathers)",
+                   "frac": rec["l1tex_pct_of_peak"] / 100.0,
+                   "issue_active_frac": (rec.get("issue_active_pct") or 0) / 100.0,
+                   "l2_hit_pct": rec.get("l2_hit_pct"),
+                   "source": f"ncu l1tex__throughput.avg.pct_of_peak_sustained_elapsed, "
+                             f"{rec['capture']}"}
+    return per_unit * units, src, binding
 
 
 def hbm_peak():
@@ -613,7 +620,8 @@ def sweep_line(args, R, world, cyc, c4, rf):
     }
     peak, peak_kind = hbm_peak()
     achieved = alg[dom] / (split[dom] / 1e3) / 1e9
-    traffic, traffic_src = ncu_traffic(args.workload, dom, n_pts if dom != "k1_static" else n_k)
+    traffic, traffic_src, binding = ncu_traffic(args.workload, dom,
+                                                n_pts if dom != "k1_static" else n_k)
     flat = R["flats"][0]
     line = {
         "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world,
@@ -637,7 +645,7 @@ def sweep_line(args, R, world, cyc, c4, rf):
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                      "algorithmic_bytes": alg[dom], "traffic": traffic,
-                     "traffic_source": traffic_src},
+                     "traffic_source": traffic_src, "binding": binding},
         "clocks": R["clk"],
     }
     if world > 1:
@@ -714,7 +722,7 @@ def run_c4(args, rank, world, local_rank, threads, sub: bool = False):
     alg = n * (8 * F + 8) + flat.nodes.nbytes  # rows in + power out + ensemble once
     achieved = alg / (ms / steps / 1e3) / 1e9
     peak, peak_kind = hbm_peak()
-    traffic, traffic_src = ncu_traffic("c4", "k4_rf_predict", n)
+    traffic, traffic_src, binding = ncu_traffic("c4", "k4_rf_predict", n)
     line = {"metric": "RF inference rows/sec", "value": value, "unit": "rows/s",
             "n_gpus": world, "steps": steps, "warmup": warm,
             "ms_per_step": ms / steps, "higher_is_better": True, "scaling": "strong",
@@ -729,7 +737,7 @@ def run_c4(args, rank, world, local_rank, threads, sub: bool = False):
             "roofline": {"bound": "hbm", "kernel": "k4_rf_predict", "achieved": achieved,
                          "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": achieved / peak, "algorithmic_bytes": alg, "traffic": traffic,
-                         "traffic_source": traffic_src},
+                         "traffic_source": traffic_src, "binding": binding},
             "clocks": clk.summary()}
     # e2e: the same rows from pinned HOST memory, streamed in chunks through
     # runtime.HostRowsPredictor (H2D / K4 / D2H on three streams), power back

@@ -79,15 +79,47 @@ def _make_model(family: str, n_estimators: int, learning_rate: float, max_depth,
     raise TrainerError(f"unsupported model family '{family}'; choose from {', '.join(FAMILIES)}")
 
 
+def canonical_order(X: np.ndarray, y: np.ndarray) -> np.ndarray:
+    """The row order of ``training.py:82-91``: a stable lexicographic sort by
+    every feature column, then the target (pandas ``sort_values(by=manifest +
+    [target], kind="mergesort")``), computed most-significant key first: one
+    stable argsort of the first column, then only the runs of rows still tied
+    on all keys so far are re-sorted by the next key (continuous features
+    leave no ties after the first pass: one argsort instead of pandas' 65-key
+    factorisation, ~15 s at 1M x 64).  Values compare like pandas' (-0.0 ==
+    0.0; the Dataset forbids NaN)."""
+    F = X.shape[1]
+
+    def key(j):   # column j (the target after the features), no up-front copies
+        return X[:, j] if j < F else y
+
+    n = len(y)
+    order = np.argsort(key(0), kind="stable")
+    tied = np.ones(n, bool)     # position i tied with i - 1 on every key so far
+    tied[0] = False
+    for k in range(1, F + 1):
+        v = key(k - 1)[order]
+        tied[1:] &= v[1:] == v[:-1]
+        if not tied.any():
+            break
+        grp = np.cumsum(~tied)                  # group id per sorted position
+        multi = tied | np.r_[tied[1:], False]   # members of groups of size > 1
+        pos = np.flatnonzero(multi)
+        sub = order[pos]
+        # stable sort of those rows by (group, key k): lexsort's last key is primary
+        perm = np.lexsort((key(k)[sub], grp[pos]))
+        order[pos] = sub[perm]
+    return order
+
+
 def canonical_rows(X, y, manifest) -> tuple[np.ndarray, np.ndarray]:
     """Reference ``training.py:82-91``: stable sort by all features then target."""
-    import pandas as pd
-
-    frame = pd.DataFrame(np.asarray(X, dtype=float), columns=list(manifest))
-    target = "__target__"
-    frame[target] = np.asarray(y, dtype=float)
-    frame = frame.sort_values(by=list(manifest) + [target], kind="mergesort")
-    return frame[list(manifest)].to_numpy(dtype=float), frame[target].to_numpy(dtype=float)
+    X = np.asarray(X, dtype=float)
+    y = np.asarray(y, dtype=float)
+    if X.ndim != 2 or X.shape[1] != len(manifest) or len(y) != len(X):
+        raise TrainerError("feature matrix and target have different lengths")
+    order = canonical_order(X, y)
+    return X[order], y[order]
 
 
 def train(dataset, family: str = "gradient_boosted", *, n_estimators: int = 500,
