@@ -215,14 +215,19 @@ struct Slab {       // [row][32] tables of the current block (smem or global)
 #define ROW(a, r) (a)[(size_t)(r) * 32 + lane]
 
 #ifndef GK_DISCARD
-#define GK_DISCARD 0  // 1: drop dead reservation-table lines from L2 (measured: -34 % DRAM writes, +1 % time)
+#define GK_DISCARD 2  // 0: off; 1: dead tables dropped per work item; 2: span tables per block
 #endif
-// The per-warp reservation tables are dead once a work item's schedule is
-// composed (the next item writes every row before reading it).  Without this,
-// L2 writes the dirty lines back to HBM when the ensemble walk streams through
-// it (ncu: 1.66 GB of DRAM writes per config-#2 sweep).  `discard.global.L2`
-// invalidates a 128-byte line without write-back.  Rows are 256 B ([row][32]
-// doubles), i.e. two lines each; the warp's lanes split the lines.
+// The per-warp reservation tables are dead once their block is scheduled (the
+// next block writes every row it reads: schedule_block starts an empty table,
+// as the reference's ReservationTable per block, scheduler.py:137-145), and
+// the CFG rows once the item's schedule is composed.  Global stores write
+// through to L2; without discards L2 writes the dirty lines back to HBM when
+// the ensemble walk streams through it (ncu: 1.97 GB of DRAM writes per
+// config-#2 sweep against 16 MB of results).  `discard.global.L2` invalidates
+// a 128-byte line without write-back.  Rows are 256 B ([row][32] doubles),
+// i.e. two lines each; the warp's lanes split the lines.  Per item (mode 1)
+// many lines are already written back when the item ends (-34 % DRAM writes,
+// r1); per block (mode 2) they are dropped while still L2-resident.
 __device__ __forceinline__ void discard_rows(const double *base, uint32_t rows, int lane) {
 #if GK_DISCARD
     const char *p = reinterpret_cast<const char *>(base);
@@ -658,6 +663,15 @@ __global__ void __launch_bounds__(kWarps * 32, kFused ? GK_FUSED_MINB : GK_K23_M
                 write_trace ? O.trace.latency + trow : nullptr,
                 write_trace ? O.trace.n_batches + trow : nullptr);
             ROW(blk_delay, b) = dl;
+#if GK_DISCARD == 2
+            if (B.n > ns) {  // the block's tables are dead: drop them while L2-resident
+                __syncwarp();
+                discard_rows(glob_slab.fin, B.n, lane);
+                discard_rows(glob_slab.ss, B.n, lane);
+                discard_rows(glob_slab.se, B.n, lane);
+                __syncwarp();  // ordered before the next block's writes to these lines
+            }
+#endif
         }
         // schedule_cfg composition (scheduler.py:206-211)
         const uint32_t *topo = C.topo + K.topo0;
@@ -688,7 +702,7 @@ __global__ void __launch_bounds__(kWarps * 32, kFused ? GK_FUSED_MINB : GK_K23_M
         // the item's tables are dead: drop them from L2 before the walk streams
         // the ensemble through it (only the global slab; rows actually used)
         __syncwarp();
-        if (K.max_n > ns) {
+        if (GK_DISCARD == 1 && K.max_n > ns) {
             const uint32_t used = min(K.max_n, g_rows);
             discard_rows(glob_slab.fin, used, lane);
             discard_rows(glob_slab.ss, used, lane);

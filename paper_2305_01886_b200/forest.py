@@ -72,6 +72,89 @@ def _check(rc):
     chk(rc)
 
 
+class _Read:
+    """An asynchronous device -> pinned host read: the copy and an event are
+    queued on the current stream; `.get()` waits for that event only.  A batch
+    generator yields the read (so the driver can launch other batches' work
+    meanwhile) and calls `.get()` when resumed."""
+
+    def __init__(self, t):
+        import torch
+
+        self.h = torch.empty(tuple(t.shape), dtype=t.dtype, pin_memory=True)
+        self.h.copy_(t, non_blocking=True)
+        self.ev = torch.cuda.Event()
+        self.ev.record()
+
+    def ready(self) -> bool:
+        return self.ev.query()
+
+    def get(self) -> np.ndarray:
+        self.ev.synchronize()
+        return self.h.numpy()
+
+
+_STREAMS: dict = {}
+
+
+def _stream_pool(dev, n: int) -> list:
+    """Streams reused across fits: torch's caching allocator pools memory per
+    stream, so fresh streams per fit re-allocated every level buffer with
+    cudaMalloc (~150 ms of host time and GPU-idle gaps per 500-tree fit)."""
+    import torch
+
+    pool = _STREAMS.setdefault(str(dev), [])
+    while len(pool) < n:
+        pool.append(torch.cuda.Stream(device=dev))
+    return pool[:n]
+
+
+def _drive(gen):
+    """Run one batch generator to completion on the current stream."""
+    try:
+        while True:
+            next(gen).get()
+    except StopIteration as stop:
+        return stop.value
+
+
+def _drive_many(gens, streams):
+    """Round-robin the batch generators over `streams` from ONE host thread:
+    each resume launches a batch's next level (or assembly step) on its own
+    stream and returns at its next device -> host read; a batch is resumed
+    once that read has landed, ready ones first.  No host threads, so no GIL
+    hand-offs between the batches' Python bookkeeping."""
+    import collections
+
+    import torch
+
+    todo = collections.deque(enumerate(gens))
+    slots = []  # [index, generator, stream, pending read]
+    results = {}
+    free = list(streams)
+
+    def start():
+        while todo and free:
+            k, g = todo.popleft()
+            slots.append([k, g, free.pop(0), None])
+
+    start()
+    while slots:
+        pick = next((sl for sl in slots if sl[3] is None or sl[3].ready()), slots[0])
+        k, g, st, rd = pick
+        if rd is not None:
+            rd.ev.synchronize()
+        with torch.cuda.stream(st):
+            try:
+                pick[3] = g.send(None)
+            except StopIteration as stop:
+                results[k] = stop.value
+                slots.remove(pick)
+                free.append(st)
+                start()
+    return [results[k] for k in range(len(results))]
+
+
 def tree_seeds(random_state, n_estimators: int) -> np.ndarray:
     """Per-tree seeds as scikit-learn draws them (SK/ensemble/_base.py:77-81)."""
     rs = random_state if isinstance(random_state, np.random.RandomState) else \
@@ -357,9 +440,11 @@ class _LevelGrower:
         form it replaced (same trees, node for node -- kept for A/B tests)."""
         if os.environ.get("GK_RF_HOST_LEVELS", "0") == "1":
             return self._grow_host(counts, base, m, rows0, rows1, TB)
-        return self._grow_dev(counts, base, m, rows0, rows1, TB)
+        return _drive(self._grow_dev(counts, base, m, rows0, rows1, TB))
 
     def _grow_dev(self, counts, base, m, rows0, rows1, TB):
+        """Generator: yields a _Read before every host read of device results
+        (one per level, a few in the assembly); returns (trees, leaf records)."""
         import torch
 
         from .runtime import _ptr, device
@@ -450,7 +535,9 @@ class _LevelGrower:
             if _LEVEL_LOG is not None:
                 ev[4].record()
             prev = stats
-            stats = stats_d.cpu().numpy().astype(np.int64)  # the level's one sync
+            rd = _Read(stats_d)
+            yield rd
+            stats = rd.get().astype(np.int64)  # the level's one host read
             if _LEVEL_LOG is not None:
                 _LEVEL_LOG.append(dict(depth=depth, n_small=n_s, n_med=n_m, n_big=n_b,
                                        max_med=int(prev[4]), max_big=int(prev[5]),
@@ -464,8 +551,10 @@ class _LevelGrower:
                 break
             tasks_d, node_d, lists_d, cap = tasks_n, node_n, lists_n, 2 * nt
 
-        return self._assemble_dev(counts, rows0, rows1, TB, records,
-                                  next_id_d.cpu().numpy().astype(np.int64))
+        rd = _Read(next_id_d)
+        yield rd
+        return (yield from self._assemble_dev(counts, rows0, rows1, TB, records,
+                                              rd.get().astype(np.int64)))
 
     def _assemble_dev(self, counts, rows0, rows1, TB, records, next_id):
         """_assemble on the device: node arrays by scatter from the level records,
@@ -500,8 +589,11 @@ class _LevelGrower:
         tree = tk[:, 0].long()
         g = nb_d[tree] + nd
         s = sp[:, 0] >= 0
-        si = torch.nonzero(s).squeeze(1)
-        li = torch.nonzero(~s).squeeze(1)
+        # split / leaf counts from the level records (host); sizes known, so
+        # the compactions do not synchronise
+        n_split = int(sum(r[5] for r in records))
+        si = torch.nonzero_static(s, size=n_split).squeeze(1)
+        li = torch.nonzero_static(~s, size=int(s.numel()) - n_split).squeeze(1)
         gs = g[si]
         lid = lid_all[si]
         feat[gs] = sp[si, 0].long()
@@ -513,7 +605,10 @@ class _LevelGrower:
         lv_d = tk[li].contiguous()
         gl = g[li]
         nl = int(lv_d.shape[0])
-        max_leaf = int((lv_d[:, 2] - lv_d[:, 1]).max()) if nl else 0
+        rd = _Read((lv_d[:, 2] - lv_d[:, 1]).max() if nl else torch.zeros((), dtype=torch.int32,
+                                                                              device=dev))
+        yield rd
+        max_leaf = int(rd.get())
         stats_d = torch.empty(4 * max(nl, 1), dtype=i64, device=dev)
         _check(L.gk_rf_leaf_stats(_ptr(counts), n, _ptr(D["yfp"]), _ptr(D["y2fp"]), _ptr(lv_d),
                                   nl, _ptr(rows0), _ptr(rows1), _ptr(stats_d), max_leaf, st))
@@ -538,9 +633,10 @@ class _LevelGrower:
                           val, s3 / w - val * val, w])
         it = torch.stack([left, torch.where(is_split, left + 1, torch.full_like(left, TREE_LEAF)),
                           feat, ist[:, 0]])
-        leaf_value = (s2[gl] / w[gl]).cpu().numpy()
-        tree_depth = depth_d.cpu().numpy()
-        lv = lv_d.cpu().numpy().view(TASK_DT).reshape(-1)
+        reads = [_Read(s2[gl] / w[gl]), _Read(depth_d), _Read(lv_d)]
+        yield reads[-1]
+        leaf_value, tree_depth, lv = (r.get() for r in reads)
+        lv = lv.view(TASK_DT).reshape(-1)
         # the trees stay in HBM (predict walks them there); host arrays on demand
         batch = TreeBatch(fl, it, node_base, next_id, tree_depth)
         trees = [Tree(node_count=int(next_id[k]), max_depth=int(tree_depth[k]), batch=batch,
@@ -780,27 +876,17 @@ class RandomForestRegressor(_LevelGrower):
         # tree) must stay below 2^31 (checked exactly after the bootstrap)
         tpb = max(1, min(tpb, int(0.9 * 2 ** 31 / (0.64 * n + 1))))
         batches = [todo[b0: b0 + tpb] for b0 in range(0, len(todo), tpb)]
-        # two batches in flight on their own streams: one batch's host-side level
-        # bookkeeping (numpy, GIL released) overlaps the other's kernels
-        streams = [torch.cuda.Stream(device=dev)
-                   for _ in range(max(1, min(self.streams, len(batches))))]
+        # `streams` batches in flight, each on its own stream, driven round-robin
+        # from this thread: while one batch's level is read back, the others'
+        # kernels run (concurrent=False: one batch at a time, one stream)
+        n_str = max(1, min(self.streams, len(batches))) if self.concurrent else 1
+        streams = _stream_pool(dev, n_str)
         main = torch.cuda.current_stream(dev)
-
-        def grow(k):
-            s = streams[k % len(streams)]
-            s.wait_stream(main)
-            with torch.cuda.stream(s):
-                trees = self._grow_batch(seeds[batches[k]])
-            s.synchronize()
-            return trees
-
-        if len(batches) > 1 and self.concurrent:
-            from concurrent.futures import ThreadPoolExecutor
-
-            with ThreadPoolExecutor(max_workers=len(streams)) as ex:
-                results = list(ex.map(grow, range(len(batches))))
-        else:
-            results = [grow(k) for k in range(len(batches))]
+        for st_ in streams:
+            st_.wait_stream(main)
+        results = _drive_many([self._grow_batch(seeds[b]) for b in batches], streams)
+        for st_ in streams:
+            main.wait_stream(st_)
         for batch, trees in zip(batches, results):
             for t, tree in zip(batch, trees):
                 self.estimators_[t] = TreeEstimator(tree_=tree, random_state=int(seeds[t]))
@@ -810,6 +896,8 @@ class RandomForestRegressor(_LevelGrower):
         return self
 
     def _grow_batch(self, seeds):
+        """Generator (see _Read): bootstrap + compaction + level-wise growth +
+        assembly of one batch of trees on the current stream."""
         import torch
 
         from .runtime import _ptr, device
@@ -823,7 +911,9 @@ class RandomForestRegressor(_LevelGrower):
         seeds_d = torch.from_numpy(seeds.astype(np.uint32)).to(dev)
         counts = torch.empty(TB * n, dtype=torch.int32, device=dev)
         _check(L.gk_rf_bootstrap(_ptr(seeds_d), TB, n, _ptr(counts), st))
-        m = (counts.view(TB, n) > 0).sum(dim=1).cpu().numpy().astype(np.int64)
+        rd = _Read((counts.view(TB, n) > 0).sum(dim=1))
+        yield rd
+        m = rd.get().astype(np.int64)
         base = np.concatenate([[0], np.cumsum(m)[:-1]]).astype(np.int64)
         total = int(m.sum())
         if total >= 2 ** 31:
@@ -843,7 +933,10 @@ class RandomForestRegressor(_LevelGrower):
         rows1 = torch.empty_like(rows0)
         fill = torch.empty(TB, dtype=torch.int32, device=dev)
         _check(L.gk_rf_compact(_ptr(counts), TB, n, _ptr(base_d), _ptr(rows0), _ptr(fill), st))
-        return self._grow(counts, base, m, rows0, rows1, TB)[0]
+        if os.environ.get("GK_RF_HOST_LEVELS", "0") == "1":
+            return self._grow_host(counts, base, m, rows0, rows1, TB)[0]
+        trees, _ = yield from self._grow_dev(counts, base, m, rows0, rows1, TB)
+        return trees
 
     # -------------------------------------------------------------- predict
     def flat(self, leaf_scale: float = 1.0) -> FlatEnsemble:
