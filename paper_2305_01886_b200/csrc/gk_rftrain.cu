@@ -806,6 +806,90 @@ __device__ __forceinline__ void split_tiny(const RfTrainData &D, const RfTask &T
     if (lane == 0) finish_split(best, parent, out);
 }
 
+// Nodes of <= 32 rows, lane = feature (GK_SORT32): each lane packs its
+// feature's (bin << 8 | row) keys, sorts them with a register bitonic network
+// (compile-time compare-exchanges, 240 for 32 keys), then walks them in order
+// accumulating the rows' weights and fixed-point sums (broadcast shared loads
+// by row index); a candidate is each position whose bin differs from the
+// next one's -- "left = bins <= b" for every distinct bin b present but the
+// largest, with the exact integer sums the histogram paths form -- so the
+// chosen split is identical.  ~3x fewer instructions than the warp-wide
+// rank-histogram loop (64 feature iterations of scans and atomics) for the
+// 17..32-row nodes that dominate the deepest levels.
+#ifndef GK_SORT32
+#define GK_SORT32 1
+#endif
+template <int N>
+__device__ __forceinline__ void sort_keys(uint32_t (&k)[N]) {
+#pragma unroll
+    for (int size = 2; size <= N; size <<= 1)
+#pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1)
+#pragma unroll
+            for (int i = 0; i < N; i++) {
+                const int j = i ^ stride;
+                if (j > i) {
+                    const bool up = (i & size) == 0;
+                    const uint32_t a = k[i], b = k[j];
+                    const uint32_t lo = min(a, b), hi = max(a, b);
+                    k[i] = up ? lo : hi;
+                    k[j] = up ? hi : lo;
+                }
+            }
+}
+
+template <int N>
+__device__ __forceinline__ void split_sorted(const RfTrainData &D, int m, int lane, int wib,
+                                             uint32_t wv, int64_t sv, int32_t rv, RfSplit *out) {
+    __shared__ uint32_t tw[4][32];
+    __shared__ int64_t ts[4][32];
+    if (lane < m) {
+        tw[wib][lane] = wv;
+        ts[wib][lane] = sv;
+    }
+    uint32_t W = lane < m ? wv : 0u;
+    int64_t S = lane < m ? sv : 0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        W += __shfl_xor_sync(GK_FULL, W, o);
+        S += __shfl_xor_sync(GK_FULL, S, o);
+    }
+    __syncwarp();
+    const double parent = (double)S * (double)S / (double)W;
+    BestSplit best{-1.0, 0x7fffffff, 0x7fffffff, 0};
+    for (int f0 = 0; f0 < D.F; f0 += 32) {
+        const int f = f0 + lane;
+        const bool fv = f < D.F;
+        uint32_t k[N];
+#pragma unroll
+        for (int j = 0; j < N; j++) {
+            const int32_t rj = __shfl_sync(GK_FULL, rv, j);
+            // rows past m sort last (key 0xFFFF.. > any bin << 8 | row)
+            k[j] = (j < m && fv) ? ((uint32_t)D.Xb[(size_t)rj * D.F + f] << 8) | (uint32_t)j
+                                 : 0xFFFFFFFFu;
+        }
+        if (!fv) continue;
+        sort_keys<N>(k);
+        uint32_t WL = 0, CL = 0;
+        int64_t SL = 0;
+#pragma unroll
+        for (int p = 0; p < N - 1; p++) {
+            if (p + 1 >= m) break;   // the last present row closes no candidate
+            const int idx = (int)(k[p] & 0xFFu);
+            WL += tw[wib][idx];
+            SL += ts[wib][idx];
+            CL++;
+            const uint32_t b = k[p] >> 8;
+            if ((k[p + 1] >> 8) == b || b >= (uint32_t)(kBins - 1)) continue;
+            const double SLd = (double)SL, SRd = (double)(S - SL);
+            const double pr = SLd * SLd / (double)WL + SRd * SRd / (double)(W - WL);
+            if (better(pr, f, (int)b, best)) best = BestSplit{pr, f, (int)b, CL};
+        }
+    }
+    best = warp_best(best);
+    if (lane == 0) finish_split(best, parent, out);
+}
+
 // small tasks (<= 64 rows): one warp; tiny ones (<= kTiny rows) lane-per-
 // feature (split_tiny), the rest through per-warp 256-bin histograms
 #ifndef GK_SMALL_MINB
@@ -824,11 +908,16 @@ __global__ void __launch_bounds__(128, GK_SMALL_MINB) k5_split_small(RfTrainData
     const int32_t *rows = T.parity ? rows1 : rows0;
     const int m = T.end - T.begin;
     const uint32_t *cnt = D.counts + (size_t)T.tree * D.n;
-    if (m <= kTiny) {  // warp-uniform branch
+    if (m <= (GK_SORT32 ? 32 : kTiny)) {  // warp-uniform branch
         const int32_t rv = lane < m ? rows[T.begin + lane] : 0;
         const uint32_t wv = lane < m ? cnt[rv] : 0u;
         const int64_t sv = lane < m ? (int64_t)wv * D.yfp[rv] : 0;
-        split_tiny(D, T, rows, m, lane, threadIdx.x >> 5, wv, sv, rv, out + ti);
+        if (!GK_SORT32)
+            split_tiny(D, T, rows, m, lane, threadIdx.x >> 5, wv, sv, rv, out + ti);
+        else if (m <= 16)
+            split_sorted<16>(D, m, lane, threadIdx.x >> 5, wv, sv, rv, out + ti);
+        else
+            split_sorted<32>(D, m, lane, threadIdx.x >> 5, wv, sv, rv, out + ti);
         return;
     }
     int32_t r[kSmallRpl];

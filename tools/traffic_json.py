@@ -24,8 +24,16 @@ CAPS = {
 }
 
 
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
+         "ns": 1, "us": 1e3, "usecond": 1e3, "ms": 1e6, "msecond": 1e6, "s": 1e9, "second": 1e9,
+         "nsecond": 1}
+
+
 def num(v):
-    return float(str(v[0]).replace(",", "")) if v and v[0] not in (None, "", "n/a") else None
+    """(value, unit) from ncu_summary -> float in bytes / ns / plain units."""
+    if not v or v[0] in (None, "", "n/a"):
+        return None
+    return float(str(v[0]).replace(",", "")) * SCALE.get(v[1], 1)
 
 
 out = {"_doc": "dram__bytes_read.sum + dram__bytes_write.sum per launch and the binding "
