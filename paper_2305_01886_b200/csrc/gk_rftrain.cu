@@ -813,9 +813,10 @@ __device__ __forceinline__ void split_tiny(const RfTrainData &D, const RfTask &T
 // by row index); a candidate is each position whose bin differs from the
 // next one's -- "left = bins <= b" for every distinct bin b present but the
 // largest, with the exact integer sums the histogram paths form -- so the
-// chosen split is identical.  ~3x fewer instructions than the warp-wide
-// rank-histogram loop (64 feature iterations of scans and atomics) for the
-// 17..32-row nodes that dominate the deepest levels.
+// chosen split is identical (tools/k5_ab.py: 160 tree arrays equal with
+// GK_SORT32=0).  Fewer instructions than the warp-wide rank-histogram loop
+// (64 feature iterations of scans and atomics) for 17..32-row nodes (level
+// 14 of config #3: 11.1 -> 9.4 ms per 32 trees).
 #ifndef GK_SORT32
 #define GK_SORT32 1
 #endif
@@ -912,10 +913,10 @@ __global__ void __launch_bounds__(128, GK_SMALL_MINB) k5_split_small(RfTrainData
         const int32_t rv = lane < m ? rows[T.begin + lane] : 0;
         const uint32_t wv = lane < m ? cnt[rv] : 0u;
         const int64_t sv = lane < m ? (int64_t)wv * D.yfp[rv] : 0;
-        if (!GK_SORT32)
+        // <= 16 rows: the O(m^2) all-pairs form is cheaper than a 16-key sort
+        // (measured: level 15, mostly <= 16-row nodes, 17.0 vs 18.7 ms)
+        if (m <= kTiny)
             split_tiny(D, T, rows, m, lane, threadIdx.x >> 5, wv, sv, rv, out + ti);
-        else if (m <= 16)
-            split_sorted<16>(D, m, lane, threadIdx.x >> 5, wv, sv, rv, out + ti);
         else
             split_sorted<32>(D, m, lane, threadIdx.x >> 5, wv, sv, rv, out + ti);
         return;
