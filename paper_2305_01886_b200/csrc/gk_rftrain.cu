@@ -15,10 +15,13 @@
 // decisions are deterministic despite atomics.
 //
 // Level-wise growth over a batch of trees; a "task" is one node to split:
-//   rows <= 64       -> one warp, all-pairs prefix sums (k5_split_small)
+//   rows <= 64       -> one warp: sorted keys (<= 32 rows, k5_split_sorted) or
+//                       rank-compacted histograms (k5_split_rank)
 //   rows <= kMedRows -> one CTA, shared-memory histograms per 16-feature chunk
 //   larger           -> row-chunked CTAs accumulate global histograms, then
 //                       one CTA per task evaluates (k5_hist_big + k5_eval_big)
+#include <algorithm>
+
 #include "gk_internal.cuh"
 
 namespace gk {
@@ -195,6 +198,35 @@ __device__ __forceinline__ bool better(double p, int f, int b, const BestSplit &
     return p > o.proxy || (p == o.proxy && (f < o.feat || (f == o.feat && b < o.bin)));
 }
 
+// Float bound on the MSE proxy.  The exact proxy's two IEEE fp64 divisions
+// were the split search's largest instruction share (ncu, level 15 of config
+// #3: ~25 % of the warp-per-node kernel's stall samples).  pf = p * 2^-64 to
+// within ~1e-6 relative (each operand rounded once, __fdividef <= 2 ulp, both
+// terms >= 0; an integer SL != 0 keeps every term >= 2^-96, far from float
+// underflow).  A candidate whose pf is below the lane's exact best * (1 -
+// 2^-12) can neither beat nor tie it, so it is skipped and the chosen split is
+// unchanged; the others take the exact fp64 proxy and the (proxy, feature,
+// bin) order as before.
+__device__ __forceinline__ float proxy_f(int64_t SL, int64_t SR, uint32_t WL, uint32_t WR) {
+    const float a = __ll2float_rn(SL) * 0x1p-32f, b = __ll2float_rn(SR) * 0x1p-32f;
+    return __fdividef(a * a, __uint2float_rn(WL)) + __fdividef(b * b, __uint2float_rn(WR));
+}
+__device__ __forceinline__ float proxy_floor(double best) {
+    return best < 0.0 ? -1.0f : __double2float_rd(best * 0x1p-64) * (1.0f - 0x1p-12f);
+}
+// one candidate: left = (SL, WL, CL) of a node with totals (S, W); exact
+// proxy only past the float bound; thr tracks proxy_floor(best.proxy)
+__device__ __forceinline__ void consider(int64_t SL, int64_t S, uint32_t WL, uint32_t W,
+                                         uint32_t CL, int f, int b, BestSplit &best, float &thr) {
+    if (proxy_f(SL, S - SL, WL, W - WL) < thr) return;
+    const double SLd = (double)SL, SRd = (double)(S - SL);
+    const double p = SLd * SLd / (double)WL + SRd * SRd / (double)(W - WL);
+    if (better(p, f, b, best)) {
+        best = BestSplit{p, f, b, CL};
+        thr = proxy_floor(p);
+    }
+}
+
 // Evaluate all boundaries of one feature's histogram with one warp:
 // left = bins <= b; proxy = S_L^2 / W_L + S_R^2 / W_R (sklearn's MSE proxy).
 // The candidates are the non-empty bins (an empty bin repeats the previous
@@ -251,8 +283,8 @@ struct CandSmem {  // one warp's compacted split candidates (<= 64)
 };
 
 template <bool kCompact, class Bins>
-__device__ __forceinline__ BestSplit eval_feature(const Bins &H, int f, int lane,
-                                                  CandSmem *cc) {
+__device__ __forceinline__ void eval_feature(const Bins &H, int f, int lane, CandSmem *cc,
+                                             BestSplit &best) {
     uint64_t c8[8];
     int64_t s8[8];
     uint64_t cacc = 0;
@@ -297,7 +329,7 @@ __device__ __forceinline__ BestSplit eval_feature(const Bins &H, int f, int lane
         if (lane >= o) off += a;
     }
     const int total = __shfl_sync(GK_FULL, off, 31);
-    BestSplit best{-1.0, 0x7fffffff, 0x7fffffff, 0};
+    float thr = proxy_floor(best.proxy);
     if (kCompact && total <= 64) {
         // sparse (every node of <= 64 rows; small medium nodes): compact the
         // candidates so each division pair runs once per candidate, <= 2
@@ -314,27 +346,20 @@ __device__ __forceinline__ BestSplit eval_feature(const Bins &H, int f, int lane
         __syncwarp();
         for (int i = lane; i < total; i += 32) {
             const uint64_t cl = cc->c[i];
-            const uint32_t CL = (uint32_t)(cl >> 32), WL = (uint32_t)cl;
-            const double SL = (double)cc->s[i], SR = (double)(stot - cc->s[i]);
-            const double p = SL * SL / (double)WL + SR * SR / (double)(W - WL);
-            if (better(p, f, cc->b[i], best)) best = BestSplit{p, f, (int)cc->b[i], CL};
+            consider(cc->s[i], stot, (uint32_t)cl, W, (uint32_t)(cl >> 32), f, cc->b[i], best, thr);
         }
         __syncwarp();
     } else {
 #pragma unroll
         for (int j = 0; j < 8; j++) {
             if (!(mask >> j & 1u)) continue;
-            const int b = lane * 8 + j;
             const uint64_t cl = cpre + c8[j];
-            const uint32_t CL = (uint32_t)(cl >> 32), WL = (uint32_t)cl;
-            const double SL = (double)(spre + s8[j]), SR = (double)(stot - spre - s8[j]);
-            const double p = SL * SL / (double)WL + SR * SR / (double)(W - WL);
-            if (better(p, f, b, best)) best = BestSplit{p, f, b, CL};
+            consider(spre + s8[j], stot, (uint32_t)cl, W, (uint32_t)(cl >> 32), f, lane * 8 + j,
+                     best, thr);
         }
     }
-    // this lane's best only: callers fold lanes across features and reduce the
-    // warp once per task (better() is a total order, so the result is the same)
-    return best;
+    // folded into this lane's best only: callers reduce the warp once per task
+    // (better() is a total order, so the result is the same)
 }
 
 __device__ __forceinline__ BestSplit warp_best(BestSplit best) {
@@ -375,42 +400,77 @@ struct HistSmem {
     }
 };
 
+#ifndef GK_ACC_BIG
+#define GK_ACC_BIG 8  // rows per thread in flight, k5_hist_big (config #3: 4 -> 8, 12.1 -> 11.4 ms per 32 trees)
+#endif
+#ifndef GK_ACC_MED
+#define GK_ACC_MED 1  // rows per thread in flight, k5_split_medium (80-register budget)
+#endif
 // add one task's rows [p0, p1) to the shared histograms of feature chunk fc.
 // Per row: the 16 bins in one 16-byte load, then every feature's returning
 // low-word atomic is issued before any dependent high-word add -- 16
 // independent round trips in flight instead of a return-then-add chain per
 // feature (the SASS had one ATOMS latency per feature: issue active 7 %).
+template <int kAccRows>
 __device__ __forceinline__ void accumulate(HistSmem &H, const RfTrainData &D, const RfTask &T,
                                            const int32_t *__restrict__ rows, int p0, int p1,
                                            int fc) {
     const int f0 = fc * kFC, nf = min(kFC, D.F - f0);
     const uint32_t *cnt = D.counts + (size_t)T.tree * D.n;
     const bool vec = nf == kFC && (D.F & 15) == 0;  // CTA-uniform
+    if (vec) {
+        // kAccRows rows per thread in flight: their row ids, then all their
+        // weight / target / bin loads, then the atomics -- one dependent
+        // gather chain per kAccRows rows (ncu, level 7 of config #3: 67 % of
+        // the stall samples were long-scoreboard waits on one row at a time)
+        const int step = blockDim.x * kAccRows;
+        for (int pb = p0 + threadIdx.x; pb < p1; pb += step) {
+            int32_t r[kAccRows];
+#pragma unroll
+            for (int u = 0; u < kAccRows; u++) {
+                const int p = pb + u * blockDim.x;
+                r[u] = p < p1 ? rows[p] : -1;
+            }
+            uint32_t w[kAccRows];
+            int64_t y[kAccRows];
+            uint4 q[kAccRows];
+#pragma unroll
+            for (int u = 0; u < kAccRows; u++) {
+                if (r[u] >= 0) {
+                    w[u] = cnt[r[u]];
+                    y[u] = D.yfp[r[u]];
+                    q[u] = *reinterpret_cast<const uint4 *>(D.Xb + (size_t)r[u] * D.F + f0);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kAccRows; u++) {
+                if (r[u] < 0) continue;
+                const int64_t sv = (int64_t)w[u] * y[u];
+                const uint32_t lo = (uint32_t)sv;
+                const int32_t hi = (int32_t)(sv >> 32);
+                const uint32_t qw[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
+                uint32_t old[kFC];
+#pragma unroll
+                for (int j = 0; j < kFC; j++) {
+                    const int b = (qw[j >> 2] >> (8 * (j & 3))) & 0xFF;
+                    atomicAdd(&H.wgt[j][b], w[u]);
+                    old[j] = atomicAdd(&H.slo[j][b], lo);
+                }
+#pragma unroll
+                for (int j = 0; j < kFC; j++) {
+                    const int b = (qw[j >> 2] >> (8 * (j & 3))) & 0xFF;
+                    atomicAdd(&H.shi[j][b], hi + (old[j] + lo < old[j] ? 1 : 0));
+                }
+            }
+        }
+        return;
+    }
     for (int p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
         const int32_t r = rows[p];
         const uint32_t w = cnt[r];
         const int64_t sv = (int64_t)w * D.yfp[r];
         const uint8_t *xb = D.Xb + (size_t)r * D.F + f0;
-        const uint32_t lo = (uint32_t)sv;
-        const int32_t hi = (int32_t)(sv >> 32);
-        if (vec) {
-            const uint4 q = *reinterpret_cast<const uint4 *>(xb);
-            const uint32_t qw[4] = {q.x, q.y, q.z, q.w};
-            uint32_t old[kFC];
-#pragma unroll
-            for (int j = 0; j < kFC; j++) {
-                const int b = (qw[j >> 2] >> (8 * (j & 3))) & 0xFF;
-                atomicAdd(&H.wgt[j][b], w);
-                old[j] = atomicAdd(&H.slo[j][b], lo);
-            }
-#pragma unroll
-            for (int j = 0; j < kFC; j++) {
-                const int b = (qw[j >> 2] >> (8 * (j & 3))) & 0xFF;
-                atomicAdd(&H.shi[j][b], hi + (old[j] + lo < old[j] ? 1 : 0));
-            }
-        } else {
-            for (int j = 0; j < nf; j++) H.feat(j).add(xb[j], w, sv);
-        }
+        for (int j = 0; j < nf; j++) H.feat(j).add(xb[j], w, sv);
     }
 }
 
@@ -427,8 +487,7 @@ __device__ __forceinline__ void eval_chunk(HistSmem &H, int F, int fc, BestSplit
         const int f = fc * kFC + j;
         if (f >= F) break;
         // measured: compaction costs the CTA-per-node path more than it saves
-        const BestSplit b = eval_feature<false>(H.feat(j), f, lane, nullptr);
-        if (better(b.proxy, b.feat, b.bin, mine)) mine = b;
+        eval_feature<false>(H.feat(j), f, lane, nullptr, mine);
     }
 }
 
@@ -469,7 +528,7 @@ __device__ __forceinline__ void parent_proxy(HistSmem &H) {
 
 // Medium tasks of <= kMidRows rows: the CTA's rows are staged once in shared
 // memory and each warp owns every 8th feature with its own rank-compacted
-// histogram (as the warp-per-node path, k5_split_small): no block barriers per
+// histogram (as the warp-per-node path, k5_split_rank): no block barriers per
 // feature chunk, no 64 KB zeroing, and each entry scanned is a present bin.
 // Same candidates, proxies and (proxy, feature, bin) order as the 256-bin scan.
 #ifndef GK_MID_ROWS
@@ -492,7 +551,7 @@ struct MidSmem {
     long long S;
 };
 
-__device__ __noinline__ void split_mid(const RfTrainData &D, const RfTask &T,
+__device__ __forceinline__ void split_mid(const RfTrainData &D, const RfTask &T,
                                        const int32_t *__restrict__ rows, unsigned char *smem,
                                        RfSplit *out) {
     MidSmem &M = *reinterpret_cast<MidSmem *>(smem);
@@ -547,6 +606,7 @@ __device__ __noinline__ void split_mid(const RfTrainData &D, const RfTask &T,
     }
     __syncthreads();
     BestSplit best{-1.0, 0x7fffffff, 0x7fffffff, 0};
+    float thr = proxy_floor(best.proxy);
     for (int f = warp; f < D.F; f += 8) {
         int bin[kMidK];
 #pragma unroll
@@ -611,11 +671,8 @@ __device__ __noinline__ void split_mid(const RfTrainData &D, const RfTask &T,
             const int e = lane * kE + j;
             if (j >= kE || e >= nd - 1) break;
             const uint64_t cl = cpre + c8[j];
-            const uint32_t CL = (uint32_t)(cl >> 32), WL = (uint32_t)cl;
-            const double SL = (double)(spre + s8[j]), SR = (double)(stot - spre - s8[j]);
-            const double p = SL * SL / (double)WL + SR * SR / (double)(Wt - WL);
-            const int b = M.cbin[warp][e];
-            if (better(p, f, b, best)) best = BestSplit{p, f, b, CL};
+            consider(spre + s8[j], stot, (uint32_t)cl, Wt, (uint32_t)(cl >> 32), f,
+                     M.cbin[warp][e], best, thr);
         }
         __syncwarp();
 #pragma unroll
@@ -635,32 +692,46 @@ __device__ __noinline__ void split_mid(const RfTrainData &D, const RfTask &T,
         finish_split(b, S * S / (double)M.W, out);
     }
 }
-constexpr size_t kMedSmem = sizeof(MidSmem) > sizeof(HistSmem) ? sizeof(MidSmem) : sizeof(HistSmem);
 
-// medium tasks: one CTA per task, feature chunks in sequence
-#ifndef GK_MED_MINB
-#define GK_MED_MINB 3  // resident CTAs per SM of the medium path (64 KB histograms each)
+// Medium tasks, one CTA per task, in two kernels (each with its own register
+// budget and instruction footprint; both are launched over the whole medium
+// list and each CTA whose task belongs to the other kernel exits at once):
+//   <= kMidRows rows: k5_split_mid (staged rows, rank-compacted histograms);
+//   larger: k5_split_medium (shared-memory histograms per feature chunk).
+constexpr int kMedThreads = 256;
+#ifndef GK_MID_MINB
+#define GK_MID_MINB 3  // resident CTAs per SM of k5_split_mid (~50 KB shared memory each)
 #endif
-__global__ void __launch_bounds__(256, GK_MED_MINB) k5_split_medium(RfTrainData D, const RfTask *__restrict__ tasks,
-                                                       const int32_t *__restrict__ task_ids,
-                                                       const int32_t *__restrict__ rows0,
-                                                       const int32_t *__restrict__ rows1,
-                                                       RfSplit *__restrict__ out) {
+__global__ void __launch_bounds__(kMedThreads, GK_MID_MINB) k5_split_mid(
+    RfTrainData D, const RfTask *__restrict__ tasks, const int32_t *__restrict__ task_ids,
+    const int32_t *__restrict__ rows0, const int32_t *__restrict__ rows1,
+    RfSplit *__restrict__ out) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int ti = task_ids[blockIdx.x];
+    const RfTask T = tasks[ti];
+    if (T.end - T.begin > kMidRows) return;  // CTA-uniform: k5_split_medium's task
+    split_mid(D, T, T.parity ? rows1 : rows0, smem_raw, out + ti);
+}
+
+#ifndef GK_MED_MINB
+#define GK_MED_MINB 3  // resident CTAs per SM of k5_split_medium (48 KB histograms each)
+#endif
+__global__ void __launch_bounds__(kMedThreads, GK_MED_MINB) k5_split_medium(
+    RfTrainData D, const RfTask *__restrict__ tasks, const int32_t *__restrict__ task_ids,
+    const int32_t *__restrict__ rows0, const int32_t *__restrict__ rows1,
+    RfSplit *__restrict__ out) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     HistSmem &H = *reinterpret_cast<HistSmem *>(smem_raw);
     const int ti = task_ids[blockIdx.x];
     const RfTask T = tasks[ti];
+    if (GK_MID_ROWS > 0 && D.F <= 64 && T.end - T.begin <= kMidRows) return;  // k5_split_mid's
     const int32_t *rows = T.parity ? rows1 : rows0;
-    if (GK_MID_ROWS > 0 && D.F <= 64 && T.end - T.begin <= kMidRows) {  // CTA-uniform
-        split_mid(D, T, rows, smem_raw, out + ti);
-        return;
-    }
     BestSplit mine{-1.0, 0x7fffffff, 0x7fffffff, 0};
     const int n_fc = (D.F + kFC - 1) / kFC;
     for (int fc = 0; fc < n_fc; fc++) {
         zero_hist(H);
         __syncthreads();
-        accumulate(H, D, T, rows, T.begin, T.end, fc);
+        accumulate<GK_ACC_MED>(H, D, T, rows, T.begin, T.end, fc);
         __syncthreads();
         if (fc == 0) parent_proxy(H);
         eval_chunk(H, D.F, fc, mine);
@@ -687,7 +758,7 @@ __global__ void __launch_bounds__(256) k5_hist_big(RfTrainData D, const RfTask *
     const int p1 = min(T.end, p0 + kBigRows);
     zero_hist(H);
     __syncthreads();
-    accumulate(H, D, T, rows, p0, p1, fc);
+    accumulate<GK_ACC_BIG>(H, D, T, rows, p0, p1, fc);
     __syncthreads();
     const int f0 = fc * kFC, nf = min(kFC, D.F - f0);
     uint64_t *dcw = gcw + ((size_t)bi * D.F + f0) * kBins;
@@ -727,99 +798,26 @@ __global__ void __launch_bounds__(256) k5_eval_big(RfTrainData D, const int32_t 
     reduce_best(H, mine, out + task_ids[bi]);
 }
 
-// Tiny nodes (<= kTiny rows): lane = feature.  Each lane loads its feature's
-// bin for every row (a row's bins are one coalesced 32-byte read per warp) and
-// evaluates every row's bin as a boundary against all rows -- O(m^2) per
-// feature but m <= 16, instead of filling and scanning 256-bin histograms one
-// feature at a time.  Candidates, integer sums and proxies are the same as the
-// histogram path's (boundary b = a bin present in the node; left = bins <= b),
-// so the chosen split is identical.
+// Small nodes (<= kSmallRows = 64 rows): one warp per node, in two kernels by
+// node size so that each stays small in the instruction cache.  ncu on level
+// 15 of config #3 (973k nodes per 32 trees): the single kernel that held the
+// all-pairs, sorted and rank-histogram forms (9.9k SASS instructions, 158 KB)
+// spent 67 % of its stall samples on "no instructions".
+//   <= 32 rows (k5_split_sorted): lane = feature, sorted keys (split_sorted);
+//   33..64 rows (k5_split_rank): rank-compacted per-warp histograms.
+// Both loop over the small list (warp-strided) and skip the other kernel's
+// nodes.
 constexpr int kTiny = 16;
 #ifndef GK_SMALL_RPL
 #define GK_SMALL_RPL 2  // rows per lane of the warp-per-node path (host SMALL = 32 x this)
 #endif
 constexpr int kSmallRpl = GK_SMALL_RPL;
-#ifndef GK_SMALL_RANK
-#define GK_SMALL_RANK 1  // warp-per-node path: rank-compacted bins (0: 256-bin scan)
+constexpr int kSmallRows = 32 * kSmallRpl;  // host forest.SMALL
+#ifndef GK_SMALL_MINB
+#define GK_SMALL_MINB 6  // resident CTAs per SM of the warp-per-node kernels
 #endif
+constexpr int kSmallThreads = 128;
 
-__device__ __forceinline__ void split_tiny(const RfTrainData &D, const RfTask &T,
-                                           const int32_t *__restrict__ rows, int m, int lane,
-                                           int wib, uint32_t wv, int64_t sv, int32_t rv,
-                                           RfSplit *out) {
-    __shared__ uint32_t tw[4][kTiny];
-    __shared__ int64_t ts[4][kTiny];
-    if (lane < m) {
-        tw[wib][lane] = wv;
-        ts[wib][lane] = sv;
-    }
-    uint32_t W = lane < m ? wv : 0u;
-    int64_t S = lane < m ? sv : 0;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        W += __shfl_xor_sync(GK_FULL, W, o);
-        S += __shfl_xor_sync(GK_FULL, S, o);
-    }
-    __syncwarp();
-    const double parent = (double)S * (double)S / (double)W;
-    BestSplit best{-1.0, 0x7fffffff, 0x7fffffff, 0};
-    for (int f0 = 0; f0 < D.F; f0 += 32) {
-        const int f = f0 + lane;
-        const bool fv = f < D.F;
-        uint32_t bin[kTiny];
-#pragma unroll
-        for (int j = 0; j < kTiny; j++) {
-            const int32_t rj = __shfl_sync(GK_FULL, rv, j);
-            bin[j] = (j < m && fv) ? D.Xb[(size_t)rj * D.F + f] : 0xFFFFu;
-        }
-        if (fv) {
-#pragma unroll
-            for (int j = 0; j < kTiny; j++) {
-                if (j >= m) break;
-                const uint32_t b = bin[j];
-                uint32_t CL = 0, WL = 0;
-                int64_t SL = 0;
-#pragma unroll
-                for (int i = 0; i < kTiny; i++) {
-                    if (i < m && bin[i] <= b) {
-                        CL++;
-                        WL += tw[wib][i];
-                        SL += ts[wib][i];
-                    }
-                }
-                if (CL == (uint32_t)m || b >= (uint32_t)(kBins - 1)) continue;
-                const double SLd = (double)SL, SRd = (double)(S - SL);
-                const double p = SLd * SLd / (double)WL + SRd * SRd / (double)(W - WL);
-                if (better(p, f, (int)b, best)) best = BestSplit{p, f, (int)b, CL};
-            }
-        }
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        BestSplit q;
-        q.proxy = __shfl_xor_sync(GK_FULL, best.proxy, o);
-        q.feat = __shfl_xor_sync(GK_FULL, best.feat, o);
-        q.bin = __shfl_xor_sync(GK_FULL, best.bin, o);
-        q.n_left = __shfl_xor_sync(GK_FULL, best.n_left, o);
-        if (better(q.proxy, q.feat, q.bin, best)) best = q;
-    }
-    if (lane == 0) finish_split(best, parent, out);
-}
-
-// Nodes of <= 32 rows, lane = feature (GK_SORT32): each lane packs its
-// feature's (bin << 8 | row) keys, sorts them with a register bitonic network
-// (compile-time compare-exchanges, 240 for 32 keys), then walks them in order
-// accumulating the rows' weights and fixed-point sums (broadcast shared loads
-// by row index); a candidate is each position whose bin differs from the
-// next one's -- "left = bins <= b" for every distinct bin b present but the
-// largest, with the exact integer sums the histogram paths form -- so the
-// chosen split is identical (tools/k5_ab.py: 160 tree arrays equal with
-// GK_SORT32=0).  Fewer instructions than the warp-wide rank-histogram loop
-// (64 feature iterations of scans and atomics) for 17..32-row nodes (level
-// 14 of config #3: 11.1 -> 9.4 ms per 32 trees).
-#ifndef GK_SORT32
-#define GK_SORT32 1
-#endif
 template <int N>
 __device__ __forceinline__ void sort_keys(uint32_t (&k)[N]) {
 #pragma unroll
@@ -839,14 +837,27 @@ __device__ __forceinline__ void sort_keys(uint32_t (&k)[N]) {
             }
 }
 
+struct SortSmem {        // one warp's node of <= 32 rows
+    int64_t s[32];       // fixed-point w * y by local row
+    uint32_t w[32];      // bootstrap weight by local row
+    int32_t row[32];     // row id by local row
+    uint32_t key[32][32];  // [position][lane]: each lane's sorted keys
+};
+
+// Nodes of <= N rows (N = 16 or 32), lane = feature: each lane packs its
+// feature's (bin << 8 | row) keys, sorts them with a register bitonic network
+// (80 / 240 compare-exchanges), parks them in shared memory and walks them in
+// order accumulating the rows' weights and fixed-point sums; each position
+// whose bin differs from the next one's is a candidate -- "left = bins <= b"
+// for every distinct bin b present but the largest, with the exact integer
+// sums the histogram paths form -- so the chosen split is identical to theirs.
 template <int N>
-__device__ __forceinline__ void split_sorted(const RfTrainData &D, int m, int lane, int wib,
+__device__ __forceinline__ void split_sorted(const RfTrainData &D, int m, int lane, SortSmem &Z,
                                              uint32_t wv, int64_t sv, int32_t rv, RfSplit *out) {
-    __shared__ uint32_t tw[4][32];
-    __shared__ int64_t ts[4][32];
     if (lane < m) {
-        tw[wib][lane] = wv;
-        ts[wib][lane] = sv;
+        Z.w[lane] = wv;
+        Z.s[lane] = sv;
+        Z.row[lane] = rv;
     }
     uint32_t W = lane < m ? wv : 0u;
     int64_t S = lane < m ? sv : 0;
@@ -855,217 +866,202 @@ __device__ __forceinline__ void split_sorted(const RfTrainData &D, int m, int la
         W += __shfl_xor_sync(GK_FULL, W, o);
         S += __shfl_xor_sync(GK_FULL, S, o);
     }
-    __syncwarp();
     const double parent = (double)S * (double)S / (double)W;
     BestSplit best{-1.0, 0x7fffffff, 0x7fffffff, 0};
+    float thr = -1.0f;
+    __syncwarp();
+#pragma unroll 1
     for (int f0 = 0; f0 < D.F; f0 += 32) {
         const int f = f0 + lane;
         const bool fv = f < D.F;
         uint32_t k[N];
 #pragma unroll
         for (int j = 0; j < N; j++) {
-            const int32_t rj = __shfl_sync(GK_FULL, rv, j);
-            // rows past m sort last (key 0xFFFF.. > any bin << 8 | row)
-            k[j] = (j < m && fv) ? ((uint32_t)D.Xb[(size_t)rj * D.F + f] << 8) | (uint32_t)j
+            // rows past m sort last (key 0xFFFF.. > any bin << 8 | row); row
+            // ids by broadcast shared loads, not shuffles: shuffles in this
+            // loop made ptxas emit a second, divergence-safe copy of the sort
+            k[j] = (j < m && fv) ? ((uint32_t)D.Xb[(size_t)Z.row[j] * D.F + f] << 8) | (uint32_t)j
                                  : 0xFFFFFFFFu;
         }
-        if (!fv) continue;
         sort_keys<N>(k);
-        uint32_t WL = 0, CL = 0;
-        int64_t SL = 0;
+        __syncwarp();  // the previous feature group's reads of Z.key are done
 #pragma unroll
-        for (int p = 0; p < N - 1; p++) {
-            if (p + 1 >= m) break;   // the last present row closes no candidate
-            const int idx = (int)(k[p] & 0xFFu);
-            WL += tw[wib][idx];
-            SL += ts[wib][idx];
-            CL++;
-            const uint32_t b = k[p] >> 8;
-            if ((k[p + 1] >> 8) == b || b >= (uint32_t)(kBins - 1)) continue;
-            const double SLd = (double)SL, SRd = (double)(S - SL);
-            const double pr = SLd * SLd / (double)WL + SRd * SRd / (double)(W - WL);
-            if (better(pr, f, (int)b, best)) best = BestSplit{pr, f, (int)b, CL};
+        for (int j = 0; j < N; j++) Z.key[j][lane] = k[j];
+        __syncwarp();
+        if (fv) {
+            uint32_t WL = 0, CL = 0;
+            int64_t SL = 0;
+            uint32_t cur = k[0];
+            for (int p = 0; p + 1 < m; p++) {  // the last present row closes no candidate
+                const uint32_t nxt = Z.key[p + 1][lane];
+                const int idx = (int)(cur & 0xFFu);
+                WL += Z.w[idx];
+                SL += Z.s[idx];
+                CL++;
+                const uint32_t b = cur >> 8;
+                if ((nxt >> 8) != b && b < (uint32_t)(kBins - 1))
+                    consider(SL, S, WL, W, CL, f, (int)b, best, thr);
+                cur = nxt;
+            }
         }
     }
     best = warp_best(best);
     if (lane == 0) finish_split(best, parent, out);
 }
 
-// small tasks (<= 64 rows): one warp; tiny ones (<= kTiny rows) lane-per-
-// feature (split_tiny), the rest through per-warp 256-bin histograms
-#ifndef GK_SMALL_MINB
-#define GK_SMALL_MINB 6  // resident CTAs per SM of the warp-per-node path
-#endif
-__global__ void __launch_bounds__(128, GK_SMALL_MINB) k5_split_small(RfTrainData D, const RfTask *__restrict__ tasks,
-                                                     const int32_t *__restrict__ task_ids,
-                                                     int n_ids, const int32_t *__restrict__ rows0,
-                                                     const int32_t *__restrict__ rows1,
-                                                     RfSplit *__restrict__ out) {
-    const int lane = threadIdx.x & 31;
-    const int wi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (wi >= n_ids) return;
-    const int ti = task_ids[wi];
-    const RfTask T = tasks[ti];
-    const int32_t *rows = T.parity ? rows1 : rows0;
-    const int m = T.end - T.begin;
-    const uint32_t *cnt = D.counts + (size_t)T.tree * D.n;
-    if (m <= (GK_SORT32 ? 32 : kTiny)) {  // warp-uniform branch
+__global__ void __launch_bounds__(kSmallThreads, GK_SMALL_MINB) k5_split_sorted(
+    RfTrainData D, const RfTask *__restrict__ tasks, const int32_t *__restrict__ task_ids,
+    int n_ids, const int32_t *__restrict__ rows0, const int32_t *__restrict__ rows1,
+    RfSplit *__restrict__ out) {
+    __shared__ SortSmem Z[kSmallThreads / 32];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int nw = gridDim.x * (kSmallThreads / 32);
+    for (int wi = blockIdx.x * (kSmallThreads / 32) + wib; wi < n_ids; wi += nw) {
+        const int ti = task_ids[wi];
+        const RfTask T = tasks[ti];
+        const int m = T.end - T.begin;
+        if (m > 32) continue;  // warp-uniform: k5_split_rank's node
+        const int32_t *rows = T.parity ? rows1 : rows0;
+        const uint32_t *cnt = D.counts + (size_t)T.tree * D.n;
         const int32_t rv = lane < m ? rows[T.begin + lane] : 0;
         const uint32_t wv = lane < m ? cnt[rv] : 0u;
         const int64_t sv = lane < m ? (int64_t)wv * D.yfp[rv] : 0;
-        // <= 16 rows: the O(m^2) all-pairs form is cheaper than a 16-key sort
-        // (measured: level 15, mostly <= 16-row nodes, 17.0 vs 18.7 ms)
         if (m <= kTiny)
-            split_tiny(D, T, rows, m, lane, threadIdx.x >> 5, wv, sv, rv, out + ti);
+            split_sorted<16>(D, m, lane, Z[wib], wv, sv, rv, out + ti);
         else
-            split_sorted<32>(D, m, lane, threadIdx.x >> 5, wv, sv, rv, out + ti);
-        return;
+            split_sorted<32>(D, m, lane, Z[wib], wv, sv, rv, out + ti);
+        __syncwarp();  // Z reuse by the warp's next node
     }
-    int32_t r[kSmallRpl];
-    uint32_t w[kSmallRpl];
-    int64_t s[kSmallRpl];
-    uint32_t W = 0;
-    int64_t S = 0;
-#pragma unroll
-    for (int h = 0; h < kSmallRpl; h++) {
-        const int i = lane + 32 * h;
-        r[h] = i < m ? rows[T.begin + i] : -1;
-        w[h] = i < m ? cnt[r[h]] : 0u;
-        s[h] = i < m ? (int64_t)w[h] * D.yfp[r[h]] : 0;
-        W += w[h];
-        S += s[h];
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        W += __shfl_xor_sync(GK_FULL, W, o);
-        S += __shfl_xor_sync(GK_FULL, S, o);
-    }
-    const double parent = (double)S * (double)S / (double)W;
-    const int wib = threadIdx.x >> 5;
-    BestSplit best{-1.0, 0x7fffffff, 0x7fffffff, 0};
-#if GK_SMALL_RANK
-    // Rank-compacted histograms: a node of <= 32 * kE rows has at most that
-    // many distinct bins.  A 256-bit occupancy map gives each present bin its
-    // rank among them, the four-word bins are indexed by rank, and lane l scans
-    // entries [l * kE, (l + 1) * kE) -- kE per lane instead of 8, every entry
-    // non-empty, so entry e is a candidate iff a later entry exists (then its
-    // bin is < 255 and both sides hold rows): the same candidates, proxies and
-    // (proxy, feature, bin) order as the 256-bin scan.
+}
+
+// Nodes of 33..64 rows: rank-compacted histograms.  A node of <= 32 * kE rows
+// has at most that many distinct bins.  A 256-bit occupancy map gives each
+// present bin its rank among them, the three-word bins are indexed by rank,
+// and lane l scans entries [l * kE, (l + 1) * kE) -- kE per lane instead of 8,
+// every entry non-empty, so entry e is a candidate iff a later entry exists
+// (then its bin is < 255 and both sides hold rows): the same candidates,
+// proxies and (proxy, feature, bin) order as the 256-bin scan.
+__global__ void __launch_bounds__(kSmallThreads, GK_SMALL_MINB) k5_split_rank(
+    RfTrainData D, const RfTask *__restrict__ tasks, const int32_t *__restrict__ task_ids,
+    int n_ids, const int32_t *__restrict__ rows0, const int32_t *__restrict__ rows1,
+    RfSplit *__restrict__ out) {
     constexpr int kE = kSmallRpl;
     constexpr int kN = 32 * kE;
-    __shared__ uint32_t cwgt[4][kN], cslo[4][kN];
-    __shared__ int32_t cshi[4][kN];
-    __shared__ uint16_t cbin[4][kN];
-    __shared__ uint32_t bmap[4][8], bpre[4][8];
+    constexpr int kW = kSmallThreads / 32;
+    __shared__ uint32_t cwgt[kW][kN], cslo[kW][kN];
+    __shared__ int32_t cshi[kW][kN];
+    __shared__ uint16_t cbin[kW][kN];
+    __shared__ uint32_t bmap[kW][8], bpre[kW][8];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const Bins3 hb{nullptr, cwgt[wib], cslo[wib], cshi[wib]};
-#pragma unroll
-    for (int j = 0; j < kE; j++) hb.clear(lane * kE + j);
-    if (lane < 8) bmap[wib][lane] = 0u;
-    __syncwarp();
-    for (int f = 0; f < D.F; f++) {
-        int bin[kSmallRpl], rk[kSmallRpl];
-#pragma unroll
-        for (int h = 0; h < kSmallRpl; h++) {
-            bin[h] = r[h] >= 0 ? D.Xb[(size_t)r[h] * D.F + f] : -1;
-            if (bin[h] >= 0) atomicOr(&bmap[wib][bin[h] >> 5], 1u << (bin[h] & 31));
-        }
-        __syncwarp();
-        const uint32_t word = lane < 8 ? bmap[wib][lane] : 0u;
-        int pc = __popc(word);
-#pragma unroll
-        for (int o = 1; o < 8; o <<= 1) {
-            const int a = __shfl_up_sync(GK_FULL, pc, o);
-            if (lane >= o) pc += a;
-        }
-        const int nd = __shfl_sync(GK_FULL, pc, 7);  // distinct bins
-        if (lane < 8) bpre[wib][lane] = (uint32_t)(pc - __popc(word));
-        __syncwarp();
+    const int nw = gridDim.x * kW;
+    for (int wi = blockIdx.x * kW + wib; wi < n_ids; wi += nw) {
+        const int ti = task_ids[wi];
+        const RfTask T = tasks[ti];
+        const int m = T.end - T.begin;
+        if (m <= 32) continue;  // warp-uniform: k5_split_sorted's node
+        const int32_t *rows = T.parity ? rows1 : rows0;
+        const uint32_t *cnt = D.counts + (size_t)T.tree * D.n;
+        int32_t r[kSmallRpl];
+        uint32_t w[kSmallRpl];
+        int64_t s[kSmallRpl];
+        uint32_t W = 0;
+        int64_t S = 0;
 #pragma unroll
         for (int h = 0; h < kSmallRpl; h++) {
-            rk[h] = -1;
-            if (bin[h] >= 0) {
-                const int k = bin[h] >> 5;
-                rk[h] = (int)bpre[wib][k] + __popc(bmap[wib][k] & ((1u << (bin[h] & 31)) - 1u));
-                hb.add(rk[h], w[h], s[h]);
-                cbin[wib][rk[h]] = (uint16_t)bin[h];
-            }
+            const int i = lane + 32 * h;
+            r[h] = i < m ? rows[T.begin + i] : -1;
+            w[h] = i < m ? cnt[r[h]] : 0u;
+            s[h] = i < m ? (int64_t)w[h] * D.yfp[r[h]] : 0;
+            W += w[h];
+            S += s[h];
         }
-        __syncwarp();
-        uint64_t c8[kE];
-        int64_t s8[kE];
-        uint64_t cacc = 0;
-        int64_t sacc = 0;
 #pragma unroll
-        for (int j = 0; j < kE; j++) {
-            cacc += hb.cw(lane * kE + j);
-            sacc += hb.sum(lane * kE + j);
-            c8[j] = cacc;
-            s8[j] = sacc;
+        for (int o = 16; o; o >>= 1) {
+            W += __shfl_xor_sync(GK_FULL, W, o);
+            S += __shfl_xor_sync(GK_FULL, S, o);
         }
-        uint64_t cpre = cacc;
-        int64_t spre = sacc;
+        const double parent = (double)S * (double)S / (double)W;
+        BestSplit best{-1.0, 0x7fffffff, 0x7fffffff, 0};
+        float thr = -1.0f;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint64_t a = __shfl_up_sync(GK_FULL, cpre, o);
-            const int64_t b = __shfl_up_sync(GK_FULL, spre, o);
-            if (lane >= o) {
-                cpre += a;
-                spre += b;
-            }
-        }
-        const uint64_t ctot = __shfl_sync(GK_FULL, cpre, 31);
-        const int64_t stot = __shfl_sync(GK_FULL, spre, 31);
-        cpre -= cacc;
-        spre -= sacc;
-        const uint32_t Wt = (uint32_t)ctot;
-#pragma unroll
-        for (int j = 0; j < kE; j++) {
-            const int e = lane * kE + j;
-            if (e >= nd - 1) break;
-            const uint64_t cl = cpre + c8[j];
-            const uint32_t CL = (uint32_t)(cl >> 32), WL = (uint32_t)cl;
-            const double SL = (double)(spre + s8[j]), SR = (double)(stot - spre - s8[j]);
-            const double p = SL * SL / (double)WL + SR * SR / (double)(Wt - WL);
-            const int b = cbin[wib][e];
-            if (better(p, f, b, best)) best = BestSplit{p, f, b, CL};
-        }
-        __syncwarp();
-#pragma unroll
-        for (int h = 0; h < kSmallRpl; h++)
-            if (rk[h] >= 0) hb.clear(rk[h]);
+        for (int j = 0; j < kE; j++) hb.clear(lane * kE + j);
         if (lane < 8) bmap[wib][lane] = 0u;
         __syncwarp();
-    }
-#else
-    // per-warp 256-bin histogram, one feature at a time, evaluated by the same
-    // boundary scan as the larger nodes
-    __shared__ uint32_t hcnt[4][kBins], hwgt[4][kBins], hslo[4][kBins];
-    __shared__ int32_t hshi[4][kBins];
-    __shared__ CandSmem hcand[4];
-    const BinsRef hb{hcnt[wib], hwgt[wib], hslo[wib], hshi[wib]};
-    // zero once; after each feature every lane clears only the bins it filled
+        for (int f = 0; f < D.F; f++) {
+            int bin[kSmallRpl], rk[kSmallRpl];
 #pragma unroll
-    for (int j = 0; j < kBins / 32; j++) hb.clear(lane + 32 * j);
-    __syncwarp();
-    for (int f = 0; f < D.F; f++) {
-        int bin[kSmallRpl];
+            for (int h = 0; h < kSmallRpl; h++) {
+                bin[h] = r[h] >= 0 ? D.Xb[(size_t)r[h] * D.F + f] : -1;
+                if (bin[h] >= 0) atomicOr(&bmap[wib][bin[h] >> 5], 1u << (bin[h] & 31));
+            }
+            __syncwarp();
+            const uint32_t word = lane < 8 ? bmap[wib][lane] : 0u;
+            int pc = __popc(word);
 #pragma unroll
-        for (int h = 0; h < kSmallRpl; h++) {
-            bin[h] = r[h] >= 0 ? D.Xb[(size_t)r[h] * D.F + f] : -1;
-            if (bin[h] >= 0) hb.add(bin[h], w[h], s[h]);
+            for (int o = 1; o < 8; o <<= 1) {
+                const int a = __shfl_up_sync(GK_FULL, pc, o);
+                if (lane >= o) pc += a;
+            }
+            const int nd = __shfl_sync(GK_FULL, pc, 7);  // distinct bins
+            if (lane < 8) bpre[wib][lane] = (uint32_t)(pc - __popc(word));
+            __syncwarp();
+#pragma unroll
+            for (int h = 0; h < kSmallRpl; h++) {
+                rk[h] = -1;
+                if (bin[h] >= 0) {
+                    const int k = bin[h] >> 5;
+                    rk[h] = (int)bpre[wib][k] + __popc(bmap[wib][k] & ((1u << (bin[h] & 31)) - 1u));
+                    hb.add(rk[h], w[h], s[h]);
+                    cbin[wib][rk[h]] = (uint16_t)bin[h];
+                }
+            }
+            __syncwarp();
+            uint64_t c8[kE];
+            int64_t s8[kE];
+            uint64_t cacc = 0;
+            int64_t sacc = 0;
+#pragma unroll
+            for (int j = 0; j < kE; j++) {
+                cacc += hb.cw(lane * kE + j);
+                sacc += hb.sum(lane * kE + j);
+                c8[j] = cacc;
+                s8[j] = sacc;
+            }
+            uint64_t cpre = cacc;
+            int64_t spre = sacc;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint64_t a = __shfl_up_sync(GK_FULL, cpre, o);
+                const int64_t b = __shfl_up_sync(GK_FULL, spre, o);
+                if (lane >= o) {
+                    cpre += a;
+                    spre += b;
+                }
+            }
+            const uint64_t ctot = __shfl_sync(GK_FULL, cpre, 31);
+            const int64_t stot = __shfl_sync(GK_FULL, spre, 31);
+            cpre -= cacc;
+            spre -= sacc;
+            const uint32_t Wt = (uint32_t)ctot;
+#pragma unroll
+            for (int j = 0; j < kE; j++) {
+                const int e = lane * kE + j;
+                if (e >= nd - 1) break;
+                const uint64_t cl = cpre + c8[j];
+                consider(spre + s8[j], stot, (uint32_t)cl, Wt, (uint32_t)(cl >> 32), f,
+                         cbin[wib][e], best, thr);
+            }
+            __syncwarp();
+#pragma unroll
+            for (int h = 0; h < kSmallRpl; h++)
+                if (rk[h] >= 0) hb.clear(rk[h]);
+            if (lane < 8) bmap[wib][lane] = 0u;
+            __syncwarp();
         }
-        __syncwarp();
-        const BestSplit b = eval_feature<true>(hb, f, lane, &hcand[wib]);
-        if (better(b.proxy, b.feat, b.bin, best)) best = b;
-        __syncwarp();
-#pragma unroll
-        for (int h = 0; h < kSmallRpl; h++)
-            if (bin[h] >= 0) hb.clear(bin[h]);
-        __syncwarp();
+        best = warp_best(best);
+        if (lane == 0) finish_split(best, parent, out + ti);
     }
-#endif
-    best = warp_best(best);
-    if (lane == 0) finish_split(best, parent, out + ti);
 }
 
 // ---------------------------------------------------------------- partition
@@ -1122,7 +1118,6 @@ __global__ void __launch_bounds__(256) k5_partition(RfTrainData D, const RfTask 
 // atomics, so their order varies from run to run; every kernel that reads them
 // writes per-task results, so trees do not.
 constexpr int kLvlThreads = 256;
-constexpr int kSmallRows = 32 * kSmallRpl;  // host forest.SMALL
 
 enum : int {  // stats[] slots (int32)
     kStNext = 0, kStSmall = 1, kStMed = 2, kStBig = 3, kStMaxMed = 4, kStMaxBig = 5
@@ -1382,22 +1377,44 @@ int gk_rf_split_level(const uint8_t *Xb, const int64_t *yfp, const double *y,
     gk::RfTrainData D{Xb, yfp, y, counts, n_rows, n_feat};
     const gk::RfTask *T = (const gk::RfTask *)tasks;
     gk::RfSplit *out = (gk::RfSplit *)split_out;
-    const size_t smem = sizeof(gk::HistSmem), smem_med = gk::kMedSmem;
-    static const bool attr = [smem, smem_med] {  // thread-safe one-time init (concurrent tree batches)
+    const size_t smem = sizeof(gk::HistSmem), smem_mid = sizeof(gk::MidSmem);
+    static const bool attr = [smem, smem_mid] {  // thread-safe one-time init (concurrent tree batches)
         cudaFuncSetAttribute(gk::k5_split_medium, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem_med);
+                             (int)smem);
         cudaFuncSetAttribute(gk::k5_split_medium, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared);
+        cudaFuncSetAttribute(gk::k5_split_mid, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem_mid);
+        cudaFuncSetAttribute(gk::k5_split_mid, cudaFuncAttributePreferredSharedMemoryCarveout,
                              cudaSharedmemCarveoutMaxShared);
         cudaFuncSetAttribute(gk::k5_hist_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(gk::k5_eval_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         return true;
     }();
     (void)attr;
-    if (n_small > 0)
-        gk::k5_split_small<<<(n_small * 32 + 127) / 128, 128, 0, st>>>(D, T, small_ids, n_small,
-                                                                       rows0, rows1, out);
-    if (n_med > 0)
-        gk::k5_split_medium<<<n_med, 256, smem_med, st>>>(D, T, med_ids, rows0, rows1, out);
+    static const int n_sm = [] {
+        int dev = 0, v = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v > 0 ? v : 148;
+    }();
+    if (n_small > 0) {
+        // warp-strided over the small list: ~4 waves of resident CTAs
+        constexpr int wpb = gk::kSmallThreads / 32;
+        const int64_t want = ((int64_t)n_small + wpb - 1) / wpb;
+        const int64_t cap = (int64_t)n_sm * GK_SMALL_MINB * 4;
+        const unsigned blocks = (unsigned)(want < cap ? want : cap);
+        gk::k5_split_sorted<<<blocks, gk::kSmallThreads, 0, st>>>(D, T, small_ids, n_small, rows0,
+                                                                   rows1, out);
+        gk::k5_split_rank<<<blocks, gk::kSmallThreads, 0, st>>>(D, T, small_ids, n_small, rows0,
+                                                                 rows1, out);
+    }
+    if (n_med > 0) {
+        if (GK_MID_ROWS > 0 && n_feat <= 64)
+            gk::k5_split_mid<<<n_med, gk::kMedThreads, smem_mid, st>>>(D, T, med_ids, rows0, rows1,
+                                                                       out);
+        gk::k5_split_medium<<<n_med, gk::kMedThreads, smem, st>>>(D, T, med_ids, rows0, rows1, out);
+    }
     if (n_big > 0) {
         uint64_t *gcw = (uint64_t *)hist_ws;
         int64_t *gs = (int64_t *)(gcw + (size_t)n_big * n_feat * gk::kBins);
