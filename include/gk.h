@@ -274,28 +274,39 @@ int gk_predict_energy_sweep(const gk_corpus *corpus, const gk_grid *grid,
 /* counts[t][i] = bincount(RandomState(tree_seeds[t]).randint(0, n, n))[i] */
 int gk_rf_bootstrap(const uint32_t *tree_seeds, uint32_t n_trees, int64_t n_rows,
                     uint32_t *counts, void *stream);
-/* rows[tree_base[t] ..] = indices i with counts[t][i] > 0 (fill[t] = how many) */
-int gk_rf_compact(const uint32_t *counts, uint32_t n_trees, int64_t n_rows,
-                  const int64_t *tree_base, int32_t *rows, int32_t *fill, void *stream);
+/* Row records (gk_rftrain.cu): a node's rows are a contiguous run of
+ * gk_rf_record_bytes(n_feat)-byte records {row id i32, bootstrap weight u32,
+ * weight * yfp i64, the row's n_feat bins (zero-padded to 16 B)} in one of two
+ * ping-pong buffers (recs0 / recs1); the partition moves whole records. */
+size_t gk_rf_record_bytes(int32_t n_feat);
+/* recs[tree_base[t] ..] = the records of the rows i with counts[t][i] > 0
+ * (fill[t] = how many; order within a tree unspecified); Xb [n_rows][n_feat]
+ * bins, yfp [n_rows] fixed-point targets */
+int gk_rf_compact(const uint32_t *counts, uint32_t n_trees, int64_t n_rows, const uint8_t *Xb,
+                  int32_t n_feat, const int64_t *yfp, const int64_t *tree_base, void *recs,
+                  int32_t *fill, void *stream);
 /* Xb[i][f] = #{edges[f][j] < float32(X[i][f])}; per-bin min/max (order-mapped) */
 int gk_rf_bin(const double *X, int64_t n_rows, int32_t n_feat, int64_t ld, const float *edges,
               const int32_t *n_edges, uint8_t *Xb, uint32_t *bin_min, uint32_t *bin_max,
               void *stream);
-/* best split of every task (small / medium / big index lists); split.n_left is
- * NOT filled (the partition's cursor gives the left row count) */
+/* best split of every task (small / medium / big index lists).  Tasks of <= 256
+ * rows are partitioned by their split search (records moved to the other
+ * buffer): their split record has pad = 1 and n_left = the left row count;
+ * for the others (pad = 0) n_left is NOT filled -- gk_rf_partition_lists moves
+ * their records and its cursor gives the left row count */
 int gk_rf_split_level(const uint8_t *Xb, const int64_t *yfp, const double *y,
                       const uint32_t *counts, int64_t n_rows, int32_t n_feat,
                       const void *tasks, const int32_t *small_ids, int32_t n_small,
                       const int32_t *med_ids, int32_t n_med, const int32_t *big_ids,
-                      int32_t n_big, int32_t big_max_chunks, const int32_t *rows0,
-                      const int32_t *rows1, void *hist_ws, void *split_out, void *stream);
+                      int32_t n_big, int32_t big_max_chunks, void *recs0, void *recs1,
+                      void *hist_ws, void *split_out, void *stream);
 size_t gk_rf_hist_bytes(int32_t n_big, int32_t n_feat);
-/* move each split task's rows to the other buffer: left rows up from begin, right
- * rows down from end; cursor[2*i] ends as task i's left row count (n_left) */
+/* move each split task's records to the other buffer: left rows up from begin,
+ * right rows down from end; cursor[2*i] ends as task i's left row count (n_left) */
 int gk_rf_partition(const uint8_t *Xb, const int64_t *yfp, const double *y,
                     const uint32_t *counts, int64_t n_rows, int32_t n_feat, const void *tasks,
                     int32_t n_tasks, const void *split, const int32_t *ids, int32_t n_ids,
-                    int32_t max_rows, int32_t *rows0, int32_t *rows1, int32_t *cursor,
+                    int32_t max_rows, void *recs0, void *recs1, int32_t *cursor,
                     void *stream);
 /* The level loop's bookkeeping on the device (replaces the per-level host
  * bookkeeping of the tree builder; sklearn's BestFirst/DepthFirst builders,
@@ -322,13 +333,13 @@ int gk_rf_partition_lists(const uint8_t *Xb, const uint32_t *counts, int64_t n_r
                           int32_t n_feat, const void *tasks, int32_t n_tasks, const void *split,
                           const int32_t *small_ids, int32_t n_small, const int32_t *med_ids,
                           int32_t n_med, int32_t max_med, const int32_t *big_ids, int32_t n_big,
-                          int32_t max_big, int32_t *rows0, int32_t *rows1, int32_t *cursor,
+                          int32_t max_big, void *recs0, void *recs1, int32_t *cursor,
                           void *stream);
 /* per leaf segment: int64 {n, sum w, sum w*yfp, sum w*y2fp} (exact fixed-point
  * sums); max_leaf_rows (the largest segment) sizes the row-chunk grid */
-int gk_rf_leaf_stats(const uint32_t *counts, int64_t n_rows, const int64_t *yfp,
+int gk_rf_leaf_stats(const uint32_t *counts, int64_t n_rows, int32_t n_feat, const int64_t *yfp,
                      const int64_t *y2fp, const void *leaves, int32_t n_leaves,
-                     const int32_t *rows0, const int32_t *rows1, int64_t *out,
+                     const void *recs0, const void *recs1, int64_t *out,
                      int32_t max_leaf_rows, void *stream);
 
 /* One gradient-boosting update (sklearn GradientBoostingRegressor, squared
@@ -338,7 +349,7 @@ int gk_rf_leaf_stats(const uint32_t *counts, int64_t n_rows, const int64_t *yfp,
  * y - F (and its square) in fixed point 2^shift / 2^shift2, and *absmax =
  * max(*absmax, max |y - F|) as the bit pattern of a non-negative double. */
 int gk_gb_step(const void *leaves, int32_t n_leaves, const double *leaf_val,
-               const int32_t *rows0, const int32_t *rows1, const double *y, double *F,
+               const void *recs0, const void *recs1, int32_t n_feat, const double *y, double *F,
                int64_t *yfp, int64_t *y2fp, int32_t shift, int32_t shift2,
                uint64_t *absmax, int32_t max_leaf_rows, void *stream);
 

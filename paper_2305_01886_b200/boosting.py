@@ -84,7 +84,8 @@ class GradientBoostingRegressor(_LevelGrower):
         L = _lib()
         if not getattr(L, "_gb_bound", False):
             vp, i32 = C.c_void_p, C.c_int32
-            L.gk_gb_step.argtypes = [vp, i32, vp, vp, vp, vp, vp, vp, vp, i32, i32, vp, i32, vp]
+            L.gk_gb_step.argtypes = [vp, i32, vp, vp, vp, i32, vp, vp, vp, vp, i32, i32, vp, i32,
+                                     vp]
             L._gb_bound = True
         dev = device()
         st = torch.cuda.current_stream().cuda_stream
@@ -100,15 +101,21 @@ class GradientBoostingRegressor(_LevelGrower):
         Fd = torch.full((n,), f0, dtype=torch.float64, device=dev)
         self._dev = dict(Xb=Xb, yfp=yfp, y2fp=y2fp, y=yd, n=n, F=F, shift=shift, shift2=shift2)
         counts = torch.ones(n, dtype=torch.int32, device=dev)
-        rows_init = torch.arange(n, dtype=torch.int32, device=dev)
-        rows0, rows1 = torch.empty_like(rows_init), torch.empty_like(rows_init)
+        # row records (include/gk.h gk_rf_record_bytes), rebuilt every stage from
+        # the stage's targets; two ping-pong buffers
+        rs = int(L.gk_rf_record_bytes(F))
+        rows0 = torch.empty(n * rs, dtype=torch.uint8, device=dev)
+        rows1 = torch.empty_like(rows0)
+        base_d = torch.zeros(1, dtype=torch.int64, device=dev)
+        fill = torch.empty(1, dtype=torch.int32, device=dev)
         absmax = torch.zeros(1, dtype=torch.int64, device=dev)
         base, m = np.zeros(1, np.int64), np.array([n], np.int64)
         seeds = np.random.RandomState(self.random_state).randint(np.iinfo(np.int32).max,
                                                                    size=self.n_estimators)
         self.estimators_ = []
         for k in range(self.n_estimators):
-            rows0.copy_(rows_init)
+            _check(L.gk_rf_compact(_ptr(counts), 1, n, _ptr(Xb), F, _ptr(yfp), _ptr(base_d),
+                                   _ptr(rows0), _ptr(fill), st))
             trees, (lv, lv_d, leaf_value) = self._grow(counts, base, m, rows0, rows1, 1)
             self.estimators_.append([TreeEstimator(tree_=trees[0], random_state=int(seeds[k]))])
             if k + 1 == self.n_estimators:
@@ -119,7 +126,7 @@ class GradientBoostingRegressor(_LevelGrower):
             lvals = torch.from_numpy(self.learning_rate * leaf_value).to(dev)
             absmax.zero_()
             size = lv["end"] - lv["begin"]
-            _check(L.gk_gb_step(_ptr(lv_d), len(lv), _ptr(lvals), _ptr(rows0), _ptr(rows1),
+            _check(L.gk_gb_step(_ptr(lv_d), len(lv), _ptr(lvals), _ptr(rows0), _ptr(rows1), F,
                                 _ptr(yd), _ptr(Fd), _ptr(yfp), _ptr(y2fp), shift, shift2,
                                 _ptr(absmax), int(size.max()), st))
             rmax = float(absmax.cpu().numpy().view(np.float64)[0])

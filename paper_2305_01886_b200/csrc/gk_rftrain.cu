@@ -42,7 +42,29 @@ struct RfTrainData {
     const uint32_t *counts; // [n_trees][n] bootstrap counts
     int64_t n;
     int32_t F;
+    int32_t rs;             // row-record stride (bytes), rec_stride(F)
 };
+
+// Row records.  A node's rows are a contiguous range of records in one of two
+// ping-pong buffers, and the partition moves whole records, so every kernel
+// reads its node's rows as one contiguous stream: {row id i32, bootstrap
+// weight u32, w * y fixed point i64, the row's F bins (padded to 16 B)}.
+// Round 2 kept row ids only and gathered the weight, target and bins of every
+// row at every level from [n]-sized arrays: three random 32-byte sectors per
+// row and feature chunk (ncu, level 7 of config #3: 5.8 GB of DRAM reads per
+// level, 67 % of the stall samples waiting on them).
+constexpr int kRecHdr = 16;
+__host__ __device__ __forceinline__ int rec_stride(int F) { return kRecHdr + ((F + 15) & ~15); }
+struct RecView {
+    const uint8_t *p;
+    __device__ __forceinline__ int32_t row() const { return *reinterpret_cast<const int32_t *>(p); }
+    __device__ __forceinline__ uint32_t w() const { return *reinterpret_cast<const uint32_t *>(p + 4); }
+    __device__ __forceinline__ int64_t sv() const { return *reinterpret_cast<const int64_t *>(p + 8); }
+    __device__ __forceinline__ const uint8_t *bins() const { return p + kRecHdr; }
+};
+__device__ __forceinline__ RecView rec_at(const uint8_t *buf, int rs, int pos) {
+    return RecView{buf + (size_t)pos * rs};
+}
 
 struct RfTask {             // one node to split (or one leaf to summarise)
     int32_t tree, begin, end, parity;
@@ -140,20 +162,33 @@ __global__ void __launch_bounds__(kBootThreads) k5_bootstrap(const uint32_t *__r
     }
 }
 
-// rows with count > 0, per tree, compacted (order within a tree is not kept)
-__global__ void k5_compact(const uint32_t *__restrict__ counts, int n_trees, int64_t n,
-                           const int64_t *__restrict__ tree_base, int32_t *__restrict__ rows,
-                           int32_t *__restrict__ fill) {
+// records of the rows with count > 0, per tree, compacted (order within a
+// tree is not kept): row id, weight, w * yfp, the row's bins
+__global__ void k5_compact(RfTrainData D, int n_trees, const int64_t *__restrict__ tree_base,
+                           uint8_t *__restrict__ recs, int32_t *__restrict__ fill) {
     const int t = blockIdx.y;
+    const int64_t n = D.n;
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const bool in = i < n && counts[(size_t)t * n + i] > 0;
+    const uint32_t w = i < n ? D.counts[(size_t)t * n + i] : 0u;
+    const bool in = w > 0;
     const unsigned bal = __ballot_sync(GK_FULL, in);
     if (!bal) return;
     const int lane = threadIdx.x & 31;
     int base = 0;
     if (lane == __ffs(bal) - 1) base = atomicAdd(fill + t, __popc(bal));
     base = __shfl_sync(GK_FULL, base, __ffs(bal) - 1);
-    if (in) rows[tree_base[t] + base + __popc(bal & ((1u << lane) - 1u))] = (int32_t)i;
+    if (!in) return;
+    uint8_t *r = recs + (size_t)(tree_base[t] + base + __popc(bal & ((1u << lane) - 1u))) * D.rs;
+    const int64_t sv = (int64_t)w * D.yfp[i];
+    *reinterpret_cast<int4 *>(r) = make_int4((int32_t)i, (int32_t)w, (int32_t)(uint32_t)sv,
+                                             (int32_t)(sv >> 32));
+    const uint8_t *xb = D.Xb + (size_t)i * D.F;
+    if ((D.F & 15) == 0) {  // rows of Xb are 16-byte aligned
+        for (int k = 0; k < D.F; k += 16)
+            *reinterpret_cast<uint4 *>(r + kRecHdr + k) = *reinterpret_cast<const uint4 *>(xb + k);
+    } else {
+        for (int k = 0; k < D.F; k++) r[kRecHdr + k] = xb[k];
+    }
 }
 
 // ---------------------------------------------------------------- binning
@@ -376,7 +411,7 @@ __device__ __forceinline__ BestSplit warp_best(BestSplit best) {
 }
 
 // parent proxy S^2/W: a split must improve on it (else the node is pure)
-__device__ __forceinline__ void finish_split(const BestSplit &b, double parent, RfSplit *out) {
+__device__ __forceinline__ RfSplit make_split(const BestSplit &b, double parent) {
     RfSplit r;
     const bool ok = b.feat != 0x7fffffff && b.proxy > parent + 1e-12 * fabs(parent);
     r.feat = ok ? b.feat : -1;
@@ -384,7 +419,54 @@ __device__ __forceinline__ void finish_split(const BestSplit &b, double parent, 
     r.n_left = ok ? (int32_t)b.n_left : 0;
     r.pad = 0;
     r.proxy = ok ? b.proxy : 0.0;
-    *out = r;
+    return r;
+}
+__device__ __forceinline__ void finish_split(const BestSplit &b, double parent, RfSplit *out) {
+    *out = make_split(b, parent);
+}
+
+// Partition fused into the warp-per-node split search: the warp that chose the
+// split moves its node's records to the other buffer right away (left rows up
+// from the node's begin, right rows down from its end, as k5_partition) and
+// the split record carries n_left with pad = 1 (the level bookkeeping reads it
+// instead of the partition's cursor; k5_partition skips the task).  K rows
+// per lane: local row lane + 32 h.  Returns n_left.
+template <int K>
+__device__ __forceinline__ int warp_partition(const RfTrainData &D, const uint8_t *in_node,
+                                              uint8_t *out_node, int m, int lane, int feat,
+                                              int bin) {
+    const unsigned below = (1u << lane) - 1u;
+    int nl = 0, nr = 0;
+#pragma unroll
+    for (int h = 0; h < K; h++) {
+        const int i = lane + 32 * h;
+        const bool valid = i < m;
+        const uint8_t *src = in_node + (size_t)i * D.rs;
+        const bool left = valid && src[kRecHdr + feat] <= bin;
+        const unsigned bl = __ballot_sync(GK_FULL, left), br = __ballot_sync(GK_FULL, valid && !left);
+        if (valid) {
+            const int q = left ? nl + __popc(bl & below) : m - 1 - (nr + __popc(br & below));
+            const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
+            uint4 *d4 = reinterpret_cast<uint4 *>(out_node + (size_t)q * D.rs);
+            for (int k = 0; k < (D.rs >> 4); k++) d4[k] = s4[k];
+        }
+        nl += __popc(bl);
+        nr += __popc(br);
+    }
+    return nl;
+}
+
+// the warp's chosen split: partition (when it splits) and write the record
+template <int K>
+__device__ __forceinline__ void warp_finish(const RfTrainData &D, const BestSplit &best,
+                                            double parent, const uint8_t *in_node,
+                                            uint8_t *out_node, int m, int lane, RfSplit *out) {
+    RfSplit r = make_split(best, parent);  // warp-uniform (best is the warp's reduction)
+    if (r.feat >= 0) {
+        r.n_left = warp_partition<K>(D, in_node, out_node, m, lane, r.feat, r.bin);
+        r.pad = 1;
+    }
+    if (lane == 0) *out = r;
 }
 
 // CTA-per-node / multi-CTA histograms: three 32-bit words per bin (weight,
@@ -412,48 +494,36 @@ struct HistSmem {
 // independent round trips in flight instead of a return-then-add chain per
 // feature (the SASS had one ATOMS latency per feature: issue active 7 %).
 template <int kAccRows>
-__device__ __forceinline__ void accumulate(HistSmem &H, const RfTrainData &D, const RfTask &T,
-                                           const int32_t *__restrict__ rows, int p0, int p1,
+__device__ __forceinline__ void accumulate(HistSmem &H, const RfTrainData &D,
+                                           const uint8_t *__restrict__ recs, int p0, int p1,
                                            int fc) {
     const int f0 = fc * kFC, nf = min(kFC, D.F - f0);
-    const uint32_t *cnt = D.counts + (size_t)T.tree * D.n;
-    const bool vec = nf == kFC && (D.F & 15) == 0;  // CTA-uniform
-    if (vec) {
-        // kAccRows rows per thread in flight: their row ids, then all their
-        // weight / target / bin loads, then the atomics -- one dependent
-        // gather chain per kAccRows rows (ncu, level 7 of config #3: 67 % of
-        // the stall samples were long-scoreboard waits on one row at a time)
+    if (nf == kFC) {  // CTA-uniform; records are 16-byte aligned (rec_stride)
+        // kAccRows records per thread in flight: all their loads, then the
+        // atomics (one dependent chain per kAccRows rows)
         const int step = blockDim.x * kAccRows;
         for (int pb = p0 + threadIdx.x; pb < p1; pb += step) {
-            int32_t r[kAccRows];
+            uint4 h[kAccRows], q[kAccRows];
 #pragma unroll
             for (int u = 0; u < kAccRows; u++) {
                 const int p = pb + u * blockDim.x;
-                r[u] = p < p1 ? rows[p] : -1;
-            }
-            uint32_t w[kAccRows];
-            int64_t y[kAccRows];
-            uint4 q[kAccRows];
-#pragma unroll
-            for (int u = 0; u < kAccRows; u++) {
-                if (r[u] >= 0) {
-                    w[u] = cnt[r[u]];
-                    y[u] = D.yfp[r[u]];
-                    q[u] = *reinterpret_cast<const uint4 *>(D.Xb + (size_t)r[u] * D.F + f0);
+                if (p < p1) {
+                    const uint8_t *r = recs + (size_t)p * D.rs;
+                    h[u] = *reinterpret_cast<const uint4 *>(r);
+                    q[u] = *reinterpret_cast<const uint4 *>(r + kRecHdr + f0);
                 }
             }
 #pragma unroll
             for (int u = 0; u < kAccRows; u++) {
-                if (r[u] < 0) continue;
-                const int64_t sv = (int64_t)w[u] * y[u];
-                const uint32_t lo = (uint32_t)sv;
-                const int32_t hi = (int32_t)(sv >> 32);
+                if (pb + u * (int)blockDim.x >= p1) continue;
+                const uint32_t w = h[u].y, lo = h[u].z;
+                const int32_t hi = (int32_t)h[u].w;
                 const uint32_t qw[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
                 uint32_t old[kFC];
 #pragma unroll
                 for (int j = 0; j < kFC; j++) {
                     const int b = (qw[j >> 2] >> (8 * (j & 3))) & 0xFF;
-                    atomicAdd(&H.wgt[j][b], w[u]);
+                    atomicAdd(&H.wgt[j][b], w);
                     old[j] = atomicAdd(&H.slo[j][b], lo);
                 }
 #pragma unroll
@@ -466,10 +536,10 @@ __device__ __forceinline__ void accumulate(HistSmem &H, const RfTrainData &D, co
         return;
     }
     for (int p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
-        const int32_t r = rows[p];
-        const uint32_t w = cnt[r];
-        const int64_t sv = (int64_t)w * D.yfp[r];
-        const uint8_t *xb = D.Xb + (size_t)r * D.F + f0;
+        const RecView R = rec_at(recs, D.rs, p);
+        const uint32_t w = R.w();
+        const int64_t sv = R.sv();
+        const uint8_t *xb = R.bins() + f0;
         for (int j = 0; j < nf; j++) H.feat(j).add(xb[j], w, sv);
     }
 }
@@ -538,8 +608,7 @@ constexpr int kMidRows = GK_MID_ROWS > 0 ? GK_MID_ROWS : 32;
 constexpr int kMidK = kMidRows / 32;  // rows per lane
 constexpr int kMidXS = 68;  // staged bin row stride (17 words: lanes' rows on distinct banks)
 struct MidSmem {
-    uint8_t xb[kMidRows * kMidXS];  // the node's rows of Xb (F <= 64)
-    int32_t row[kMidRows];
+    uint8_t xb[kMidRows * kMidXS];  // the node's bins (F <= 64)
     uint32_t w[kMidRows];
     int64_t s[kMidRows];
     uint32_t wgt[8][kBins], slo[8][kBins];
@@ -547,17 +616,20 @@ struct MidSmem {
     uint16_t cbin[8][kBins];
     uint32_t bmap[8][8], bpre[8][8];
     BestSplit best[8];
+    RfSplit split;
+    int32_t nl[8], nr[8];  // per-warp left / right counts of the fused partition
     unsigned long long W;
     long long S;
 };
 
 __device__ __forceinline__ void split_mid(const RfTrainData &D, const RfTask &T,
-                                       const int32_t *__restrict__ rows, unsigned char *smem,
+                                       const uint8_t *__restrict__ recs,
+                                       uint8_t *__restrict__ out_recs, unsigned char *smem,
                                        RfSplit *out) {
     MidSmem &M = *reinterpret_cast<MidSmem *>(smem);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int m = T.end - T.begin;
-    const uint32_t *cnt = D.counts + (size_t)T.tree * D.n;
+    const uint8_t *node = recs + (size_t)T.begin * D.rs;
     if (threadIdx.x == 0) {
         M.W = 0;
         M.S = 0;
@@ -570,30 +642,21 @@ __device__ __forceinline__ void split_mid(const RfTrainData &D, const RfTask &T,
     unsigned long long wsum = 0;
     long long ssum = 0;
     for (int i = threadIdx.x; i < m; i += blockDim.x) {
-        const int32_t r = rows[T.begin + i];
-        const uint32_t w = cnt[r];
-        const int64_t sv = (int64_t)w * D.yfp[r];
-        M.row[i] = r;
+        const RecView R = rec_at(node, D.rs, i);
+        const uint32_t w = R.w();
+        const int64_t sv = R.sv();
         M.w[i] = w;
         M.s[i] = sv;
         wsum += w;
         ssum += sv;
     }
-    __syncthreads();
-    // stage the node's bin rows: 4-byte words (rows are 4-byte aligned when
-    // F % 4 == 0), 17-word stride
+    // stage the node's bins (one contiguous run of records): 4-byte words,
+    // 17-word stride in shared memory
     const int fw = (D.F + 3) >> 2;
-    if ((D.F & 3) == 0) {
-        for (int q = threadIdx.x; q < m * fw; q += blockDim.x) {
-            const int i = q / fw, k = q - i * fw;
-            reinterpret_cast<uint32_t *>(M.xb + i * kMidXS)[k] =
-                reinterpret_cast<const uint32_t *>(D.Xb + (size_t)M.row[i] * D.F)[k];
-        }
-    } else {
-        for (int q = threadIdx.x; q < m * D.F; q += blockDim.x) {
-            const int i = q / D.F, k = q - i * D.F;
-            M.xb[i * kMidXS + k] = D.Xb[(size_t)M.row[i] * D.F + k];
-        }
+    for (int q = threadIdx.x; q < m * fw; q += blockDim.x) {
+        const int i = q / fw, k = q - i * fw;
+        reinterpret_cast<uint32_t *>(M.xb + i * kMidXS)[k] =
+            reinterpret_cast<const uint32_t *>(node + (size_t)i * D.rs + kRecHdr)[k];
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
@@ -689,8 +752,39 @@ __device__ __forceinline__ void split_mid(const RfTrainData &D, const RfTask &T,
         for (int w = 1; w < (int)(blockDim.x >> 5); w++)
             if (better(M.best[w].proxy, M.best[w].feat, M.best[w].bin, b)) b = M.best[w];
         const double S = (double)M.S;
-        finish_split(b, S * S / (double)M.W, out);
+        M.split = make_split(b, S * S / (double)M.W);
     }
+    __syncthreads();
+    // fused partition (as warp_partition, CTA-wide): one row per thread, the
+    // bins from the staged tile, positions from per-warp ballot counts
+    RfSplit r = M.split;
+    if (r.feat >= 0) {
+        const int i = threadIdx.x;  // m <= kMidRows == blockDim.x
+        const bool valid = i < m;
+        const bool left = valid && M.xb[i * kMidXS + r.feat] <= r.bin;
+        const unsigned bl = __ballot_sync(GK_FULL, left), br = __ballot_sync(GK_FULL, valid && !left);
+        if (lane == 0) {
+            M.nl[warp] = __popc(bl);
+            M.nr[warp] = __popc(br);
+        }
+        __syncthreads();
+        int bL = 0, bR = 0, nL = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) {
+            bL += w < warp ? M.nl[w] : 0;
+            bR += w < warp ? M.nr[w] : 0;
+            nL += M.nl[w];
+        }
+        if (valid) {
+            const unsigned below = (1u << lane) - 1u;
+            const int q = left ? bL + __popc(bl & below) : m - 1 - (bR + __popc(br & below));
+            const uint4 *s4 = reinterpret_cast<const uint4 *>(recs + ((size_t)T.begin + i) * D.rs);
+            uint4 *d4 = reinterpret_cast<uint4 *>(out_recs + ((size_t)T.begin + q) * D.rs);
+            for (int k = 0; k < (D.rs >> 4); k++) d4[k] = s4[k];
+        }
+        r.n_left = nL;
+        r.pad = 1;
+    }
+    if (threadIdx.x == 0) *out = r;
 }
 
 // Medium tasks, one CTA per task, in two kernels (each with its own register
@@ -702,15 +796,15 @@ constexpr int kMedThreads = 256;
 #ifndef GK_MID_MINB
 #define GK_MID_MINB 3  // resident CTAs per SM of k5_split_mid (~50 KB shared memory each)
 #endif
+static_assert(kMidRows <= kMedThreads, "split_mid partitions one row per thread");
 __global__ void __launch_bounds__(kMedThreads, GK_MID_MINB) k5_split_mid(
     RfTrainData D, const RfTask *__restrict__ tasks, const int32_t *__restrict__ task_ids,
-    const int32_t *__restrict__ rows0, const int32_t *__restrict__ rows1,
-    RfSplit *__restrict__ out) {
+    uint8_t *__restrict__ rows0, uint8_t *__restrict__ rows1, RfSplit *__restrict__ out) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int ti = task_ids[blockIdx.x];
     const RfTask T = tasks[ti];
     if (T.end - T.begin > kMidRows) return;  // CTA-uniform: k5_split_medium's task
-    split_mid(D, T, T.parity ? rows1 : rows0, smem_raw, out + ti);
+    split_mid(D, T, T.parity ? rows1 : rows0, T.parity ? rows0 : rows1, smem_raw, out + ti);
 }
 
 #ifndef GK_MED_MINB
@@ -718,20 +812,20 @@ __global__ void __launch_bounds__(kMedThreads, GK_MID_MINB) k5_split_mid(
 #endif
 __global__ void __launch_bounds__(kMedThreads, GK_MED_MINB) k5_split_medium(
     RfTrainData D, const RfTask *__restrict__ tasks, const int32_t *__restrict__ task_ids,
-    const int32_t *__restrict__ rows0, const int32_t *__restrict__ rows1,
+    const uint8_t *__restrict__ rows0, const uint8_t *__restrict__ rows1,
     RfSplit *__restrict__ out) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     HistSmem &H = *reinterpret_cast<HistSmem *>(smem_raw);
     const int ti = task_ids[blockIdx.x];
     const RfTask T = tasks[ti];
     if (GK_MID_ROWS > 0 && D.F <= 64 && T.end - T.begin <= kMidRows) return;  // k5_split_mid's
-    const int32_t *rows = T.parity ? rows1 : rows0;
+    const uint8_t *rows = T.parity ? rows1 : rows0;
     BestSplit mine{-1.0, 0x7fffffff, 0x7fffffff, 0};
     const int n_fc = (D.F + kFC - 1) / kFC;
     for (int fc = 0; fc < n_fc; fc++) {
         zero_hist(H);
         __syncthreads();
-        accumulate<GK_ACC_MED>(H, D, T, rows, T.begin, T.end, fc);
+        accumulate<GK_ACC_MED>(H, D, rows, T.begin, T.end, fc);
         __syncthreads();
         if (fc == 0) parent_proxy(H);
         eval_chunk(H, D.F, fc, mine);
@@ -743,22 +837,22 @@ __global__ void __launch_bounds__(kMedThreads, GK_MED_MINB) k5_split_medium(
 // big tasks: CTA = (task, row chunk, feature chunk) -> global histograms
 __global__ void __launch_bounds__(256) k5_hist_big(RfTrainData D, const RfTask *__restrict__ tasks,
                                                    const int32_t *__restrict__ task_ids,
-                                                   const int32_t *__restrict__ rows0,
-                                                   const int32_t *__restrict__ rows1,
+                                                   const uint8_t *__restrict__ rows0,
+                                                   const uint8_t *__restrict__ rows1,
                                                    uint64_t *__restrict__ gcw,
                                                    int64_t *__restrict__ gs) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     HistSmem &H = *reinterpret_cast<HistSmem *>(smem_raw);
     const int bi = blockIdx.z;           // index among big tasks
     const RfTask T = tasks[task_ids[bi]];
-    const int32_t *rows = T.parity ? rows1 : rows0;
+    const uint8_t *rows = T.parity ? rows1 : rows0;
     const int fc = blockIdx.y;
     const int p0 = T.begin + blockIdx.x * kBigRows;
     if (p0 >= T.end) return;
     const int p1 = min(T.end, p0 + kBigRows);
     zero_hist(H);
     __syncthreads();
-    accumulate<GK_ACC_BIG>(H, D, T, rows, p0, p1, fc);
+    accumulate<GK_ACC_BIG>(H, D, rows, p0, p1, fc);
     __syncthreads();
     const int f0 = fc * kFC, nf = min(kFC, D.F - f0);
     uint64_t *dcw = gcw + ((size_t)bi * D.F + f0) * kBins;
@@ -840,7 +934,6 @@ __device__ __forceinline__ void sort_keys(uint32_t (&k)[N]) {
 struct SortSmem {        // one warp's node of <= 32 rows
     int64_t s[32];       // fixed-point w * y by local row
     uint32_t w[32];      // bootstrap weight by local row
-    int32_t row[32];     // row id by local row
     uint32_t key[32][32];  // [position][lane]: each lane's sorted keys
 };
 
@@ -853,11 +946,11 @@ struct SortSmem {        // one warp's node of <= 32 rows
 // sums the histogram paths form -- so the chosen split is identical to theirs.
 template <int N>
 __device__ __forceinline__ void split_sorted(const RfTrainData &D, int m, int lane, SortSmem &Z,
-                                             uint32_t wv, int64_t sv, int32_t rv, RfSplit *out) {
+                                             uint32_t wv, int64_t sv, const uint8_t *node,
+                                             uint8_t *out_node, RfSplit *out) {
     if (lane < m) {
         Z.w[lane] = wv;
         Z.s[lane] = sv;
-        Z.row[lane] = rv;
     }
     uint32_t W = lane < m ? wv : 0u;
     int64_t S = lane < m ? sv : 0;
@@ -877,10 +970,10 @@ __device__ __forceinline__ void split_sorted(const RfTrainData &D, int m, int la
         uint32_t k[N];
 #pragma unroll
         for (int j = 0; j < N; j++) {
-            // rows past m sort last (key 0xFFFF.. > any bin << 8 | row); row
-            // ids by broadcast shared loads, not shuffles: shuffles in this
-            // loop made ptxas emit a second, divergence-safe copy of the sort
-            k[j] = (j < m && fv) ? ((uint32_t)D.Xb[(size_t)Z.row[j] * D.F + f] << 8) | (uint32_t)j
+            // rows past m sort last (key 0xFFFF.. > any bin << 8 | row); the
+            // node's records are contiguous: row j's bin f is one coalesced
+            // byte per lane
+            k[j] = (j < m && fv) ? ((uint32_t)node[(size_t)j * D.rs + kRecHdr + f] << 8) | (uint32_t)j
                                  : 0xFFFFFFFFu;
         }
         sort_keys<N>(k);
@@ -906,12 +999,12 @@ __device__ __forceinline__ void split_sorted(const RfTrainData &D, int m, int la
         }
     }
     best = warp_best(best);
-    if (lane == 0) finish_split(best, parent, out);
+    warp_finish<1>(D, best, parent, node, out_node, m, lane, out);
 }
 
 __global__ void __launch_bounds__(kSmallThreads, GK_SMALL_MINB) k5_split_sorted(
     RfTrainData D, const RfTask *__restrict__ tasks, const int32_t *__restrict__ task_ids,
-    int n_ids, const int32_t *__restrict__ rows0, const int32_t *__restrict__ rows1,
+    int n_ids, uint8_t *__restrict__ rows0, uint8_t *__restrict__ rows1,
     RfSplit *__restrict__ out) {
     __shared__ SortSmem Z[kSmallThreads / 32];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -921,15 +1014,19 @@ __global__ void __launch_bounds__(kSmallThreads, GK_SMALL_MINB) k5_split_sorted(
         const RfTask T = tasks[ti];
         const int m = T.end - T.begin;
         if (m > 32) continue;  // warp-uniform: k5_split_rank's node
-        const int32_t *rows = T.parity ? rows1 : rows0;
-        const uint32_t *cnt = D.counts + (size_t)T.tree * D.n;
-        const int32_t rv = lane < m ? rows[T.begin + lane] : 0;
-        const uint32_t wv = lane < m ? cnt[rv] : 0u;
-        const int64_t sv = lane < m ? (int64_t)wv * D.yfp[rv] : 0;
+        const uint8_t *node = (T.parity ? rows1 : rows0) + (size_t)T.begin * D.rs;
+        uint8_t *out_node = (T.parity ? rows0 : rows1) + (size_t)T.begin * D.rs;
+        uint32_t wv = 0u;
+        int64_t sv = 0;
+        if (lane < m) {
+            const uint4 h = *reinterpret_cast<const uint4 *>(node + (size_t)lane * D.rs);
+            wv = h.y;
+            sv = (int64_t)(((uint64_t)h.w << 32) | h.z);
+        }
         if (m <= kTiny)
-            split_sorted<16>(D, m, lane, Z[wib], wv, sv, rv, out + ti);
+            split_sorted<16>(D, m, lane, Z[wib], wv, sv, node, out_node, out + ti);
         else
-            split_sorted<32>(D, m, lane, Z[wib], wv, sv, rv, out + ti);
+            split_sorted<32>(D, m, lane, Z[wib], wv, sv, node, out_node, out + ti);
         __syncwarp();  // Z reuse by the warp's next node
     }
 }
@@ -943,7 +1040,7 @@ __global__ void __launch_bounds__(kSmallThreads, GK_SMALL_MINB) k5_split_sorted(
 // proxies and (proxy, feature, bin) order as the 256-bin scan.
 __global__ void __launch_bounds__(kSmallThreads, GK_SMALL_MINB) k5_split_rank(
     RfTrainData D, const RfTask *__restrict__ tasks, const int32_t *__restrict__ task_ids,
-    int n_ids, const int32_t *__restrict__ rows0, const int32_t *__restrict__ rows1,
+    int n_ids, uint8_t *__restrict__ rows0, uint8_t *__restrict__ rows1,
     RfSplit *__restrict__ out) {
     constexpr int kE = kSmallRpl;
     constexpr int kN = 32 * kE;
@@ -960,9 +1057,9 @@ __global__ void __launch_bounds__(kSmallThreads, GK_SMALL_MINB) k5_split_rank(
         const RfTask T = tasks[ti];
         const int m = T.end - T.begin;
         if (m <= 32) continue;  // warp-uniform: k5_split_sorted's node
-        const int32_t *rows = T.parity ? rows1 : rows0;
-        const uint32_t *cnt = D.counts + (size_t)T.tree * D.n;
-        int32_t r[kSmallRpl];
+        const uint8_t *node = (T.parity ? rows1 : rows0) + (size_t)T.begin * D.rs;
+        uint8_t *out_node = (T.parity ? rows0 : rows1) + (size_t)T.begin * D.rs;
+        const uint8_t *xb[kSmallRpl];  // this lane's rows' bins (nullptr past m)
         uint32_t w[kSmallRpl];
         int64_t s[kSmallRpl];
         uint32_t W = 0;
@@ -970,9 +1067,16 @@ __global__ void __launch_bounds__(kSmallThreads, GK_SMALL_MINB) k5_split_rank(
 #pragma unroll
         for (int h = 0; h < kSmallRpl; h++) {
             const int i = lane + 32 * h;
-            r[h] = i < m ? rows[T.begin + i] : -1;
-            w[h] = i < m ? cnt[r[h]] : 0u;
-            s[h] = i < m ? (int64_t)w[h] * D.yfp[r[h]] : 0;
+            xb[h] = nullptr;
+            w[h] = 0u;
+            s[h] = 0;
+            if (i < m) {
+                const uint8_t *rp = node + (size_t)i * D.rs;
+                const uint4 hd = *reinterpret_cast<const uint4 *>(rp);
+                xb[h] = rp + kRecHdr;
+                w[h] = hd.y;
+                s[h] = (int64_t)(((uint64_t)hd.w << 32) | hd.z);
+            }
             W += w[h];
             S += s[h];
         }
@@ -992,7 +1096,7 @@ __global__ void __launch_bounds__(kSmallThreads, GK_SMALL_MINB) k5_split_rank(
             int bin[kSmallRpl], rk[kSmallRpl];
 #pragma unroll
             for (int h = 0; h < kSmallRpl; h++) {
-                bin[h] = r[h] >= 0 ? D.Xb[(size_t)r[h] * D.F + f] : -1;
+                bin[h] = xb[h] ? xb[h][f] : -1;
                 if (bin[h] >= 0) atomicOr(&bmap[wib][bin[h] >> 5], 1u << (bin[h] & 31));
             }
             __syncwarp();
@@ -1060,35 +1164,35 @@ __global__ void __launch_bounds__(kSmallThreads, GK_SMALL_MINB) k5_split_rank(
             __syncwarp();
         }
         best = warp_best(best);
-        if (lane == 0) finish_split(best, parent, out + ti);
+        warp_finish<kSmallRpl>(D, best, parent, node, out_node, m, lane, out + ti);
     }
 }
 
 // ---------------------------------------------------------------- partition
 
-// CTA = (task, 256-position chunk); rows of split tasks scatter to the other
-// buffer: left rows up from `begin`, right rows down from `end` (so no row
-// count is needed up front); the final left cursor is the split's n_left,
+// CTA = (task, 256-position chunk); the records of split tasks move to the
+// other buffer: left rows up from `begin`, right rows down from `end` (so no
+// row count is needed up front); the final left cursor is the split's n_left,
 // read by the next-level bookkeeping (k5_level_emit)
 __global__ void __launch_bounds__(256) k5_partition(RfTrainData D, const RfTask *__restrict__ tasks,
                                                     const RfSplit *__restrict__ split,
                                                     const int32_t *__restrict__ task_ids,
-                                                    const int32_t *__restrict__ rows0,
-                                                    int32_t *__restrict__ rows1_out0,
-                                                    const int32_t *__restrict__ rows1,
-                                                    int32_t *__restrict__ rows0_out1,
+                                                    const uint8_t *__restrict__ rows0,
+                                                    uint8_t *__restrict__ rows1_out0,
+                                                    const uint8_t *__restrict__ rows1,
+                                                    uint8_t *__restrict__ rows0_out1,
                                                     int32_t *__restrict__ cursor) {
     const int ti = task_ids[blockIdx.x];  // tasks on x (can exceed 65535), chunks on y
     const RfTask T = tasks[ti];
     if (T.begin + (int)(blockIdx.y * blockDim.x) >= T.end) return;  // whole CTA past the node
     const RfSplit sp = split[ti];
-    if (sp.feat < 0) return;  // searched but kept as a leaf
-    const int32_t *in = T.parity ? rows1 : rows0;
-    int32_t *outp = T.parity ? rows0_out1 : rows1_out0;
+    if (sp.feat < 0 || sp.pad == 1) return;  // kept as a leaf / partitioned by its split search
+    const uint8_t *in = T.parity ? rows1 : rows0;
+    uint8_t *outp = T.parity ? rows0_out1 : rows1_out0;
     const int p = T.begin + blockIdx.y * blockDim.x + threadIdx.x;
     const bool valid = p < T.end;
-    const int32_t r = valid ? in[p] : 0;
-    const bool left = valid && D.Xb[(size_t)r * D.F + sp.feat] <= sp.bin;
+    const uint8_t *src = in + (size_t)p * D.rs;
+    const bool left = valid && src[kRecHdr + sp.feat] <= sp.bin;
     const bool right = valid && !left;
     const int lane = threadIdx.x & 31;
     const unsigned bl = __ballot_sync(GK_FULL, left), br = __ballot_sync(GK_FULL, right);
@@ -1100,8 +1204,11 @@ __global__ void __launch_bounds__(256) k5_partition(RfTrainData D, const RfTask 
     lb = __shfl_sync(GK_FULL, lb, 0);
     rb = __shfl_sync(GK_FULL, rb, 0);
     const unsigned below = (1u << lane) - 1u;
-    if (left) outp[T.begin + lb + __popc(bl & below)] = r;
-    if (right) outp[T.end - 1 - (rb + __popc(br & below))] = r;
+    if (!valid) return;
+    const int q = left ? T.begin + lb + __popc(bl & below) : T.end - 1 - (rb + __popc(br & below));
+    const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
+    uint4 *d4 = reinterpret_cast<uint4 *>(outp + (size_t)q * D.rs);
+    for (int k = 0; k < (D.rs >> 4); k++) d4[k] = s4[k];
 }
 
 // ---------------------------------------------------------------- next level
@@ -1232,7 +1339,9 @@ __global__ void __launch_bounds__(kLvlThreads) k5_level_emit(
         const RfTask T = tasks[i];
         const int32_t lid = lid_base[T.tree] + 2 * excl;
         lid_out[i] = lid;
-        const int n_left = cursor[2 * i];   // the partition's final left count
+        // the partition's final left count (the fused warp / mid partitions
+        // leave it in the split record)
+        const int n_left = sp.pad == 1 ? sp.n_left : cursor[2 * i];
         const int mid = T.begin + n_left;
         tasks_next[2 * excl] = RfTask{T.tree, T.begin, mid, 1 - T.parity};
         tasks_next[2 * excl + 1] = RfTask{T.tree, mid, T.end, 1 - T.parity};
@@ -1259,21 +1368,20 @@ __global__ void __launch_bounds__(kLvlThreads) k5_level_emit(
 // y2fp = y^2 in its own fixed-point scale; out must be zeroed.
 __global__ void k5_leaf_stats(RfTrainData D, const int64_t *__restrict__ y2fp,
                               const RfTask *__restrict__ leaves, int n_leaves,
-                              const int32_t *__restrict__ rows0, const int32_t *__restrict__ rows1,
+                              const uint8_t *__restrict__ rows0, const uint8_t *__restrict__ rows1,
                               int64_t *__restrict__ out /*[n_leaves][4]*/) {
     const int lane = threadIdx.x & 31;
     const int li = blockIdx.x;
     const RfTask T = leaves[li];
-    const int32_t *rows = T.parity ? rows1 : rows0;
-    const uint32_t *cnt = D.counts + (size_t)T.tree * D.n;
+    const uint8_t *rows = T.parity ? rows1 : rows0;
     long long w = 0, sy = 0, sy2 = 0;
     const int stride = gridDim.y * blockDim.x;
     for (int p = T.begin + blockIdx.y * blockDim.x + threadIdx.x; p < T.end; p += stride) {
-        const int32_t r = rows[p];
-        const long long ww = cnt[r];
+        const RecView R = rec_at(rows, D.rs, p);
+        const long long ww = R.w();
         w += ww;
-        sy += ww * D.yfp[r];
-        sy2 += ww * y2fp[r];
+        sy += R.sv();
+        sy2 += ww * y2fp[R.row()];
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
@@ -1299,19 +1407,19 @@ __global__ void k5_leaf_stats(RfTrainData D, const int64_t *__restrict__ y2fp,
 // bits of a non-negative double order like the double) for the next shift.
 __global__ void __launch_bounds__(256) k5_gb_step(const RfTask *__restrict__ leaves,
                                                   const double *__restrict__ leaf_val,
-                                                  const int32_t *__restrict__ rows0,
-                                                  const int32_t *__restrict__ rows1,
+                                                  const uint8_t *__restrict__ rows0,
+                                                  const uint8_t *__restrict__ rows1, int rs,
                                                   const double *__restrict__ y,
                                                   double *__restrict__ F, int64_t *__restrict__ yfp,
                                                   int64_t *__restrict__ y2fp, int shift, int shift2,
                                                   unsigned long long *__restrict__ absmax) {
     const RfTask T = leaves[blockIdx.x];
-    const int32_t *rows = T.parity ? rows1 : rows0;
+    const uint8_t *rows = T.parity ? rows1 : rows0;
     const double v = leaf_val[blockIdx.x];
     double m = 0.0;
     for (int p = T.begin + (int)(blockIdx.y * blockDim.x + threadIdx.x); p < T.end;
          p += (int)(gridDim.y * blockDim.x)) {
-        const int32_t r = rows[p];
+        const int32_t r = rec_at(rows, rs, p).row();
         const double f = __dadd_rn(F[r], v);
         F[r] = f;
         const double g = __dsub_rn(y[r], f);
@@ -1343,12 +1451,17 @@ int gk_rf_bootstrap(const uint32_t *tree_seeds, uint32_t n_trees, int64_t n_rows
     return gk_check_launch("k5_bootstrap");
 }
 
-int gk_rf_compact(const uint32_t *counts, uint32_t n_trees, int64_t n_rows,
-                  const int64_t *tree_base, int32_t *rows, int32_t *fill, void *stream) {
+size_t gk_rf_record_bytes(int32_t n_feat) { return (size_t)gk::rec_stride(n_feat); }
+
+int gk_rf_compact(const uint32_t *counts, uint32_t n_trees, int64_t n_rows, const uint8_t *Xb,
+                  int32_t n_feat, const int64_t *yfp, const int64_t *tree_base, void *recs,
+                  int32_t *fill, void *stream) {
     const cudaStream_t st = (cudaStream_t)stream;
     cudaMemsetAsync(fill, 0, sizeof(int32_t) * n_trees, st);
+    if (n_trees == 0 || n_rows <= 0) return 0;
+    gk::RfTrainData D{Xb, yfp, nullptr, counts, n_rows, n_feat, gk::rec_stride(n_feat)};
     dim3 grid((unsigned)((n_rows + 255) / 256), n_trees);
-    gk::k5_compact<<<grid, 256, 0, st>>>(counts, (int)n_trees, n_rows, tree_base, rows, fill);
+    gk::k5_compact<<<grid, 256, 0, st>>>(D, (int)n_trees, tree_base, (uint8_t *)recs, fill);
     return gk_check_launch("k5_compact");
 }
 
@@ -1371,10 +1484,11 @@ int gk_rf_split_level(const uint8_t *Xb, const int64_t *yfp, const double *y,
                       const uint32_t *counts, int64_t n_rows, int32_t n_feat,
                       const void *tasks, const int32_t *small_ids, int32_t n_small,
                       const int32_t *med_ids, int32_t n_med, const int32_t *big_ids,
-                      int32_t n_big, int32_t big_max_chunks, const int32_t *rows0,
-                      const int32_t *rows1, void *hist_ws, void *split_out, void *stream) {
+                      int32_t n_big, int32_t big_max_chunks, void *recs0, void *recs1,
+                      void *hist_ws, void *split_out, void *stream) {
     const cudaStream_t st = (cudaStream_t)stream;
-    gk::RfTrainData D{Xb, yfp, y, counts, n_rows, n_feat};
+    gk::RfTrainData D{Xb, yfp, y, counts, n_rows, n_feat, gk::rec_stride(n_feat)};
+    uint8_t *rows0 = (uint8_t *)recs0, *rows1 = (uint8_t *)recs1;
     const gk::RfTask *T = (const gk::RfTask *)tasks;
     gk::RfSplit *out = (gk::RfSplit *)split_out;
     const size_t smem = sizeof(gk::HistSmem), smem_mid = sizeof(gk::MidSmem);
@@ -1435,11 +1549,12 @@ size_t gk_rf_hist_bytes(int32_t n_big, int32_t n_feat) {
 int gk_rf_partition(const uint8_t *Xb, const int64_t *yfp, const double *y,
                     const uint32_t *counts, int64_t n_rows, int32_t n_feat, const void *tasks,
                     int32_t n_tasks, const void *split, const int32_t *ids, int32_t n_ids,
-                    int32_t max_rows, int32_t *rows0, int32_t *rows1, int32_t *cursor,
+                    int32_t max_rows, void *recs0, void *recs1, int32_t *cursor,
                     void *stream) {
     if (n_ids <= 0) return 0;
     const cudaStream_t st = (cudaStream_t)stream;
-    gk::RfTrainData D{Xb, yfp, y, counts, n_rows, n_feat};
+    gk::RfTrainData D{Xb, yfp, y, counts, n_rows, n_feat, gk::rec_stride(n_feat)};
+    uint8_t *rows0 = (uint8_t *)recs0, *rows1 = (uint8_t *)recs1;
     cudaMemsetAsync(cursor, 0, sizeof(int32_t) * 2 * (size_t)n_tasks, st);
     const int64_t chunks = ((int64_t)max_rows + 255) / 256;
     if (chunks > 65535) {
@@ -1496,15 +1611,16 @@ int gk_rf_partition_lists(const uint8_t *Xb, const uint32_t *counts, int64_t n_r
                           int32_t n_feat, const void *tasks, int32_t n_tasks, const void *split,
                           const int32_t *small_ids, int32_t n_small, const int32_t *med_ids,
                           int32_t n_med, int32_t max_med, const int32_t *big_ids, int32_t n_big,
-                          int32_t max_big, int32_t *rows0, int32_t *rows1, int32_t *cursor,
+                          int32_t max_big, void *recs0, void *recs1, int32_t *cursor,
                           void *stream) {
     const cudaStream_t st = (cudaStream_t)stream;
-    gk::RfTrainData D{Xb, nullptr, nullptr, counts, n_rows, n_feat};
+    gk::RfTrainData D{Xb, nullptr, nullptr, counts, n_rows, n_feat, gk::rec_stride(n_feat)};
+    uint8_t *rows0 = (uint8_t *)recs0, *rows1 = (uint8_t *)recs1;
     cudaMemsetAsync(cursor, 0, sizeof(int32_t) * 2 * (size_t)n_tasks, st);
     const int32_t *ids[3] = {small_ids, med_ids, big_ids};
     const int32_t nid[3] = {n_small, n_med, n_big};
     const int32_t mx[3] = {gk::kSmallRows, max_med, max_big};
-    for (int c = 0; c < 3; c++) {
+    for (int c = 1; c < 3; c++) {  // small tasks: partitioned by k5_split_sorted / _rank
         if (nid[c] <= 0) continue;
         const int64_t chunks = ((int64_t)mx[c] + 255) / 256;
         if (chunks < 1 || chunks > 65535) {
@@ -1519,13 +1635,14 @@ int gk_rf_partition_lists(const uint8_t *Xb, const uint32_t *counts, int64_t n_r
     return gk_check_launch("k5_partition_lists");
 }
 
-int gk_rf_leaf_stats(const uint32_t *counts, int64_t n_rows, const int64_t *yfp,
+int gk_rf_leaf_stats(const uint32_t *counts, int64_t n_rows, int32_t n_feat, const int64_t *yfp,
                      const int64_t *y2fp, const void *leaves, int32_t n_leaves,
-                     const int32_t *rows0, const int32_t *rows1, int64_t *out,
+                     const void *recs0, const void *recs1, int64_t *out,
                      int32_t max_leaf_rows, void *stream) {
     if (n_leaves <= 0) return 0;
     const cudaStream_t st = (cudaStream_t)stream;
-    gk::RfTrainData D{nullptr, yfp, nullptr, counts, n_rows, 0};
+    gk::RfTrainData D{nullptr, yfp, nullptr, counts, n_rows, n_feat, gk::rec_stride(n_feat)};
+    const uint8_t *rows0 = (const uint8_t *)recs0, *rows1 = (const uint8_t *)recs1;
     cudaMemsetAsync(out, 0, sizeof(int64_t) * 4 * (size_t)n_leaves, st);
     // chunks sized by the largest leaf (one 32-lane warp per 2048 rows, <= 64)
     int max_rows = 0;
@@ -1539,7 +1656,7 @@ int gk_rf_leaf_stats(const uint32_t *counts, int64_t n_rows, const int64_t *yfp,
 }
 
 int gk_gb_step(const void *leaves, int32_t n_leaves, const double *leaf_val,
-               const int32_t *rows0, const int32_t *rows1, const double *y, double *F,
+               const void *recs0, const void *recs1, int32_t n_feat, const double *y, double *F,
                int64_t *yfp, int64_t *y2fp, int32_t shift, int32_t shift2,
                uint64_t *absmax, int32_t max_leaf_rows, void *stream) {
     if (n_leaves <= 0) return 0;
@@ -1552,7 +1669,9 @@ int gk_gb_step(const void *leaves, int32_t n_leaves, const double *leaf_val,
     if (chunks > 1024) chunks = 1024;
     if (chunks < 1) chunks = 1;
     dim3 grid((unsigned)n_leaves, (unsigned)chunks);
-    gk::k5_gb_step<<<grid, 256, 0, st>>>((const gk::RfTask *)leaves, leaf_val, rows0, rows1, y, F,
+    gk::k5_gb_step<<<grid, 256, 0, st>>>((const gk::RfTask *)leaves, leaf_val,
+                                        (const uint8_t *)recs0, (const uint8_t *)recs1,
+                                        gk::rec_stride(n_feat), y, F,
                                         yfp, y2fp, shift, shift2,
                                         (unsigned long long *)absmax);
     return gk_check_launch("k5_gb_step");

@@ -47,7 +47,9 @@ def _lib():
     if not getattr(L, "_rf_bound", False):
         vp, i32, i64, u32 = C.c_void_p, C.c_int32, C.c_int64, C.c_uint32
         L.gk_rf_bootstrap.argtypes = [vp, u32, i64, vp, vp]
-        L.gk_rf_compact.argtypes = [vp, u32, i64, vp, vp, vp, vp]
+        L.gk_rf_compact.argtypes = [vp, u32, i64, vp, i32, vp, vp, vp, vp, vp]
+        L.gk_rf_record_bytes.argtypes = [i32]
+        L.gk_rf_record_bytes.restype = C.c_size_t
         L.gk_rf_bin.argtypes = [vp, i64, i32, i64, vp, vp, vp, vp, vp, vp]
         L.gk_rf_split_level.argtypes = [vp, vp, vp, vp, i64, i32, vp, vp, i32, vp, i32, vp, i32,
                                         i32, vp, vp, vp, vp, vp]
@@ -55,7 +57,7 @@ def _lib():
         L.gk_rf_hist_bytes.restype = C.c_size_t
         L.gk_rf_partition.argtypes = [vp, vp, vp, vp, i64, i32, vp, i32, vp, vp, i32, i32, vp,
                                       vp, vp, vp]
-        L.gk_rf_leaf_stats.argtypes = [vp, i64, vp, vp, vp, i32, vp, vp, vp, i32, vp]
+        L.gk_rf_leaf_stats.argtypes = [vp, i64, i32, vp, vp, vp, i32, vp, vp, vp, i32, vp]
         L.gk_rf_level_scratch_bytes.argtypes = [i32, i32]
         L.gk_rf_level_scratch_bytes.restype = C.c_size_t
         L.gk_rf_next_level.argtypes = [vp, vp, vp, vp, i32, i32, i32, i32, vp, vp, vp, vp, vp,
@@ -610,7 +612,7 @@ class _LevelGrower:
         yield rd
         max_leaf = int(rd.get())
         stats_d = torch.empty(4 * max(nl, 1), dtype=i64, device=dev)
-        _check(L.gk_rf_leaf_stats(_ptr(counts), n, _ptr(D["yfp"]), _ptr(D["y2fp"]), _ptr(lv_d),
+        _check(L.gk_rf_leaf_stats(_ptr(counts), n, D["F"], _ptr(D["yfp"]), _ptr(D["y2fp"]), _ptr(lv_d),
                                   nl, _ptr(rows0), _ptr(rows1), _ptr(stats_d), max_leaf, st))
         # split tasks per level (host counts from the level loop) bound the
         # bottom-up segments of gs / glid
@@ -721,6 +723,9 @@ class _LevelGrower:
             next_id += 2 * np.bincount(pt, minlength=TB)
             splits.append((pt, pn, sp["feat"][s], sp["bin"][s], lid))
             nl = cursor[: 2 * nt].view(nt, 2)[:, 0].cpu().numpy()[s].astype(np.int32)
+            # tasks partitioned inside their split search carry n_left (pad = 1)
+            fused = sp["pad"][s] == 1
+            nl = np.where(fused, sp["n_left"][s], nl).astype(np.int32)
             cb = np.empty(2 * len(pt), np.int32)
             ce = np.empty(2 * len(pt), np.int32)
             cb[0::2], ce[0::2] = t_begin[s], t_begin[s] + nl
@@ -760,7 +765,7 @@ class _LevelGrower:
         lv["tree"], lv["begin"], lv["end"], lv["parity"] = lt, lb, le, lp
         lv_d = torch.from_numpy(lv.view(np.uint8)).to(dev)
         stats_d = torch.empty(4 * len(lt), dtype=torch.int64, device=dev)
-        _check(L.gk_rf_leaf_stats(_ptr(counts), n, _ptr(D["yfp"]), _ptr(D["y2fp"]), _ptr(lv_d),
+        _check(L.gk_rf_leaf_stats(_ptr(counts), n, D["F"], _ptr(D["yfp"]), _ptr(D["y2fp"]), _ptr(lv_d),
                                   len(lt), _ptr(rows0), _ptr(rows1), _ptr(stats_d),
                                   int((le - lb).max()) if len(lt) else 0, st))
         # exactly-sized node arrays
@@ -929,10 +934,13 @@ class RandomForestRegressor(_LevelGrower):
         except torch.OutOfMemoryError:
             pass
         base_d = torch.from_numpy(base).to(dev)
-        rows0 = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
+        # two ping-pong buffers of row records (include/gk.h gk_rf_record_bytes)
+        rs = int(L.gk_rf_record_bytes(F))
+        rows0 = torch.empty(max(total, 1) * rs, dtype=torch.uint8, device=dev)
         rows1 = torch.empty_like(rows0)
         fill = torch.empty(TB, dtype=torch.int32, device=dev)
-        _check(L.gk_rf_compact(_ptr(counts), TB, n, _ptr(base_d), _ptr(rows0), _ptr(fill), st))
+        _check(L.gk_rf_compact(_ptr(counts), TB, n, _ptr(D["Xb"]), F, _ptr(D["yfp"]), _ptr(base_d),
+                               _ptr(rows0), _ptr(fill), st))
         if os.environ.get("GK_RF_HOST_LEVELS", "0") == "1":
             return self._grow_host(counts, base, m, rows0, rows1, TB)[0]
         trees, _ = yield from self._grow_dev(counts, base, m, rows0, rows1, TB)
