@@ -543,6 +543,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline (profiling)")
     ap.add_argument("--no-rf", action="store_true", help="skip the config #3 forest fit")
     ap.add_argument("--no-c4", action="store_true", help="skip the config #4 sub-line")
+    ap.add_argument("--no-c1", action="store_true", help="skip the config #1 sub-line")
     ap.add_argument("--no-e2e", action="store_true", help="c4: skip the host-row e2e leg")
     ap.add_argument("--no-train", action="store_true", help="rf: skip the 6-fit train()")
     ap.add_argument("--rf-rows", type=int, default=1_000_000)
@@ -579,7 +580,7 @@ def main():
     try:
         if args.workload == "c1":
             if rank == 0:
-                run_c1(args, threads)
+                print(json.dumps(run_c1(args, threads)), flush=True)
             return
         if args.workload == "c4":
             line = run_c4(args, rank, world, local_rank, threads)
@@ -592,8 +593,14 @@ def main():
         if not args.no_c4 and args.workload == "c5":
             c4 = run_c4(args, rank, world, local_rank, threads, sub=True)
         rf = None if args.no_rf else rf_fit_measure(args, rank, world, threads)
+        c1 = None
+        if rank == 0 and not args.no_c1 and args.workload == "c5":
+            c1 = run_c1(args, threads, steps=min(args.steps, 3))
         if rank == 0:
-            print(json.dumps(sweep_line(args, R, world, cyc, c4, rf)), flush=True)
+            line = sweep_line(args, R, world, cyc, c4, rf)
+            if c1 is not None:
+                line["c1"] = c1
+            print(json.dumps(line), flush=True)
     finally:
         if world > 1:
             dist.destroy_process_group()
@@ -787,7 +794,7 @@ def run_c4(args, rank, world, local_rank, threads, sub: bool = False):
     return line
 
 
-def run_c1(args, threads):
+def run_c1(args, threads, steps=None):
     """BASELINE configs[0], the reference's own CPU-runnable case, end to end
     through this package's public API: 100 synthetic PTX kernels x the 4
     config #1 launches on tesla_k20 -> parse + pack (native front-end) ->
@@ -852,11 +859,12 @@ def run_c1(args, threads):
 
     gpu_once()  # warm-up (library load, first-touch allocations)
     torch.cuda.synchronize()
-    runs = [gpu_once() for _ in range(args.steps)]
+    steps = steps or args.steps
+    runs = [gpu_once() for _ in range(steps)]
     tot = [sum(r[0].values()) for r in runs]
     best = runs[int(np.argmin(tot))]
     line = {"metric": "config #1 end-to-end pipeline seconds", "value": float(np.median(tot)),
-            "unit": "s", "n_gpus": 1, "steps": args.steps, "warmup": 1,
+            "unit": "s", "n_gpus": 1, "steps": steps, "warmup": 1,
             "ms_per_step": float(np.median(tot)) * 1e3, "higher_is_better": False,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "BASELINE configs[0]: 100 synthetic PTX kernels x 4 launch "
@@ -906,7 +914,7 @@ def run_c1(args, threads):
                                           "all threads) + scikit-learn RandomForestRegressor "
                                           "(the reference trainer's model, n_jobs=None) + "
                                           "Python JSON export / load"}
-    print(json.dumps(line), flush=True)
+    return line
 
 
 def rf_table(rows: int, seed: int = 3):
