@@ -950,10 +950,13 @@ def rf_fit_measure(args, rank, world, threads):
 
     Xraw, y = config3_table(args.rf_rows)
     X = (Xraw - Xraw.min(0)) / (Xraw.max(0) - Xraw.min(0))
-    # warm-up at the full table: 4 batches of 32 trees on the 4 persistent
-    # streams allocate every batch-sized buffer (records, counts) once, so the
-    # timed fits measure the steady state, not torch's first cudaMalloc calls
-    RandomForestRegressor(128, max_depth=3, random_state=1).fit(X, y)
+    # the sweep / config #4 legs leave tens of GB in torch's cache: hand them
+    # back, then warm up at the full table and depth -- 4 batches of 32 trees
+    # on the 4 persistent streams allocate every batch- and level-sized
+    # buffer once, so the timed fits measure the steady state, not cudaMalloc
+    # (or the allocator's free-and-retry under memory pressure)
+    torch.cuda.empty_cache()
+    RandomForestRegressor(128, max_depth=16, random_state=1).fit(X, y)
     torch.cuda.synchronize()
 
     def timed_fit():
