@@ -342,6 +342,27 @@ int gk_rf_leaf_stats(const uint32_t *counts, int64_t n_rows, int32_t n_feat, con
                      const void *recs0, const void *recs1, int64_t *out,
                      int32_t max_leaf_rows, void *stream);
 
+/* Tree assembly of a batch from its level records (tasks / splits / BFS ids
+ * `node` / child ids `lid` (-1 for leaves) / level of every task, all levels
+ * concatenated; node g = node_base[tree] + BFS id):
+ *  nodes: split nodes' feat / nbin / left (tree-local left child id) and
+ *         depth[tree] = max(level of a split + 1) (int64, zeroed by the caller);
+ *  up:    one level, children before parents: ist[g] (int64 {n, w, w*yfp,
+ *         w*y2fp}) of every split node = ist[left] + ist[left + 1];
+ *  final: fl [4][N] f64 {threshold (-2 leaf), value, impurity, weighted_n}
+ *         and it [4][N] i64 {left, right (-1 leaf), feature, n_node_samples}
+ *         with thr [F][256] the bins' midpoint thresholds. */
+int gk_rf_assemble_nodes(const void *tasks, const void *split, const int32_t *node,
+                         const int32_t *lid, const int32_t *level, int32_t n,
+                         const int64_t *node_base, int64_t *feat, int64_t *nbin, int64_t *left,
+                         int64_t *depth, void *stream);
+int gk_rf_assemble_up(const void *tasks, const void *split, const int32_t *node,
+                      const int32_t *lid, int32_t n, const int64_t *node_base, int64_t *ist,
+                      void *stream);
+int gk_rf_assemble_final(int64_t n_nodes, const int64_t *ist, const int64_t *feat,
+                         const int64_t *nbin, const int64_t *left, const double *thr,
+                         int32_t shift, int32_t shift2, double *fl, int64_t *it, void *stream);
+
 /* One gradient-boosting update (sklearn GradientBoostingRegressor, squared
  * error; reference training.py:67-72 via _make_model("gradient_boosted")):
  * rows of leaf k (tasks as for gk_rf_leaf_stats) get F += leaf_val[k]

@@ -21,6 +21,7 @@
 //   larger           -> row-chunked CTAs accumulate global histograms, then
 //                       one CTA per task evaluates (k5_hist_big + k5_eval_big)
 #include <algorithm>
+#include <cmath>
 
 #include "gk_internal.cuh"
 
@@ -1544,6 +1545,74 @@ __global__ void k5_leaf_stats(RfTrainData D, const int64_t *__restrict__ y2fp,
     if (blockIdx.y == 0 && threadIdx.x == 0) out[4 * li + 0] = T.end - T.begin;
 }
 
+// ---------------------------------------------------------- tree assembly
+//
+// The sklearn-shaped arrays of a batch from its level records (all levels'
+// tasks / BFS ids / splits / child ids concatenated in level order; node g of
+// the batch = node_base[tree] + BFS id).  Replaces ~100 small torch launches
+// per batch (gathers, index_put, where, stack per level).
+
+// split nodes: feature, bin, left child id; per-tree depth = deepest level
+// holding a split + 1
+__global__ void k5_asm_nodes(const RfTask *__restrict__ tk, const RfSplit *__restrict__ sp,
+                             const int32_t *__restrict__ nd, const int32_t *__restrict__ lid,
+                             const int32_t *__restrict__ lvl, int n,
+                             const int64_t *__restrict__ node_base, int64_t *__restrict__ feat,
+                             int64_t *__restrict__ nbin, int64_t *__restrict__ left,
+                             unsigned long long *__restrict__ depth) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const RfSplit s = sp[i];
+    if (s.feat < 0) return;
+    const int t = tk[i].tree;
+    const int64_t g = node_base[t] + nd[i];
+    feat[g] = s.feat;
+    nbin[g] = s.bin;
+    left[g] = lid[i];
+    atomicMax(depth + t, (unsigned long long)(lvl[i] + 1));
+}
+
+// one level bottom-up: every split node's {n, w, w*y, w*y^2} = the sum of its
+// two children's (exact integers)
+__global__ void k5_asm_up(const RfTask *__restrict__ tk, const RfSplit *__restrict__ sp,
+                          const int32_t *__restrict__ nd, const int32_t *__restrict__ lid, int n,
+                          const int64_t *__restrict__ node_base, int64_t *__restrict__ ist) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n || sp[i].feat < 0) return;
+    const int64_t nb = node_base[tk[i].tree];
+    const int64_t g = nb + nd[i], c = nb + lid[i];
+    const longlong4 a = *reinterpret_cast<const longlong4 *>(ist + 4 * c);
+    const longlong4 b = *reinterpret_cast<const longlong4 *>(ist + 4 * (c + 1));
+    *reinterpret_cast<longlong4 *>(ist + 4 * g) =
+        make_longlong4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+}
+
+// fl [4][N] f64 = {threshold (-2 for leaves), value, impurity, weighted_n},
+// it [4][N] i64 = {left, right, feature, n_node_samples}; the same float64
+// expressions as the host form (ldexp by a power of two, IEEE division)
+__global__ void k5_asm_final(int64_t N, const int64_t *__restrict__ ist,
+                             const int64_t *__restrict__ feat, const int64_t *__restrict__ nbin,
+                             const int64_t *__restrict__ left, const double *__restrict__ thr,
+                             double sc2, double sc3, double *__restrict__ fl,
+                             int64_t *__restrict__ it) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= N) return;
+    const longlong4 v = *reinterpret_cast<const longlong4 *>(ist + 4 * g);
+    const int64_t l = left[g], f = feat[g];
+    const bool split = l >= 0;
+    const double w = (double)v.y;
+    const double s2 = __dmul_rn((double)v.z, sc2), s3 = __dmul_rn((double)v.w, sc3);
+    const double val = __ddiv_rn(s2, w);
+    fl[g] = split ? thr[f * kBins + nbin[g]] : -2.0;
+    fl[N + g] = val;
+    fl[2 * N + g] = __dsub_rn(__ddiv_rn(s3, w), __dmul_rn(val, val));
+    fl[3 * N + g] = w;
+    it[g] = l;
+    it[N + g] = split ? l + 1 : -1;
+    it[2 * N + g] = f;
+    it[3 * N + g] = v.x;
+}
+
 // ---------------------------------------------------------- gradient boosting
 
 // One boosting update (sklearn GradientBoostingRegressor, squared error): for
@@ -1804,6 +1873,35 @@ int gk_rf_leaf_stats(const uint32_t *counts, int64_t n_rows, int32_t n_feat, con
     gk::k5_leaf_stats<<<dim3((unsigned)n_leaves, (unsigned)chunks), 32, 0, st>>>(
         D, y2fp, (const gk::RfTask *)leaves, n_leaves, rows0, rows1, out);
     return gk_check_launch("k5_leaf_stats");
+}
+
+int gk_rf_assemble_nodes(const void *tasks, const void *split, const int32_t *node,
+                         const int32_t *lid, const int32_t *level, int32_t n,
+                         const int64_t *node_base, int64_t *feat, int64_t *nbin, int64_t *left,
+                         int64_t *depth, void *stream) {
+    if (n <= 0) return 0;
+    gk::k5_asm_nodes<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
+        (const gk::RfTask *)tasks, (const gk::RfSplit *)split, node, lid, level, n, node_base,
+        feat, nbin, left, (unsigned long long *)depth);
+    return gk_check_launch("k5_asm_nodes");
+}
+
+int gk_rf_assemble_up(const void *tasks, const void *split, const int32_t *node,
+                      const int32_t *lid, int32_t n, const int64_t *node_base, int64_t *ist,
+                      void *stream) {
+    if (n <= 0) return 0;
+    gk::k5_asm_up<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
+        (const gk::RfTask *)tasks, (const gk::RfSplit *)split, node, lid, n, node_base, ist);
+    return gk_check_launch("k5_asm_up");
+}
+
+int gk_rf_assemble_final(int64_t n_nodes, const int64_t *ist, const int64_t *feat,
+                         const int64_t *nbin, const int64_t *left, const double *thr,
+                         int32_t shift, int32_t shift2, double *fl, int64_t *it, void *stream) {
+    if (n_nodes <= 0) return 0;
+    gk::k5_asm_final<<<(unsigned)((n_nodes + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        n_nodes, ist, feat, nbin, left, thr, ldexp(1.0, -shift), ldexp(1.0, -shift2), fl, it);
+    return gk_check_launch("k5_asm_final");
 }
 
 int gk_gb_step(const void *leaves, int32_t n_leaves, const double *leaf_val,

@@ -58,6 +58,9 @@ def _lib():
         L.gk_rf_partition.argtypes = [vp, vp, vp, vp, i64, i32, vp, i32, vp, vp, i32, i32, vp,
                                       vp, vp, vp]
         L.gk_rf_leaf_stats.argtypes = [vp, i64, i32, vp, vp, vp, i32, vp, vp, vp, i32, vp]
+        L.gk_rf_assemble_nodes.argtypes = [vp, vp, vp, vp, vp, i32, vp, vp, vp, vp, vp, vp]
+        L.gk_rf_assemble_up.argtypes = [vp, vp, vp, vp, i32, vp, vp, vp]
+        L.gk_rf_assemble_final.argtypes = [i64, vp, vp, vp, vp, vp, i32, i32, vp, vp, vp]
         L.gk_rf_level_scratch_bytes.argtypes = [i32, i32]
         L.gk_rf_level_scratch_bytes.restype = C.c_size_t
         L.gk_rf_next_level.argtypes = [vp, vp, vp, vp, i32, i32, i32, i32, vp, vp, vp, vp, vp,
@@ -578,34 +581,27 @@ class _LevelGrower:
         feat = torch.full((N,), TREE_UNDEFINED, dtype=i64, device=dev)
         nbin = torch.zeros(N, dtype=i64, device=dev)
         left = torch.full((N,), TREE_LEAF, dtype=i64, device=dev)
-        # all levels at once (level order kept), two compactions: split tasks and
-        # leaves -- a few syncs per batch instead of several per level
+        depth_d = torch.zeros(TB, dtype=i64, device=dev)
+        # all levels at once (level order kept); node arrays, leaf statistics and
+        # the bottom-up sums in native kernels (include/gk.h gk_rf_assemble_*)
         tk = torch.cat([r[0][: 4 * r[4]].view(r[4], 4) for r in records])
         sp = torch.cat([r[2][: 6 * r[4]].view(r[4], 6) for r in records])
-        nd = torch.cat([r[1][: r[4]] for r in records]).long()
+        nd = torch.cat([r[1][: r[4]] for r in records])
         lid_all = torch.cat([r[3][: r[4]] if r[3] is not None else
                              torch.full((r[4],), -1, dtype=torch.int32, device=dev)
-                             for r in records]).long()
-        lvl_all = torch.cat([torch.full((r[4],), k + 1, dtype=i64, device=dev)
+                             for r in records])
+        lvl_all = torch.cat([torch.full((r[4],), k, dtype=torch.int32, device=dev)
                              for k, r in enumerate(records)])
-        tree = tk[:, 0].long()
-        g = nb_d[tree] + nd
-        s = sp[:, 0] >= 0
-        # split / leaf counts from the level records (host); sizes known, so
-        # the compactions do not synchronise
+        n_all = int(tk.shape[0])
+        _check(L.gk_rf_assemble_nodes(_ptr(tk), _ptr(sp), _ptr(nd), _ptr(lid_all), _ptr(lvl_all),
+                                      n_all, _ptr(nb_d), _ptr(feat), _ptr(nbin), _ptr(left),
+                                      _ptr(depth_d), st))
+        # leaves: their tasks (level order) and node indices; sizes known on the
+        # host (split counts from the level loop), so nothing synchronises
         n_split = int(sum(r[5] for r in records))
-        si = torch.nonzero_static(s, size=n_split).squeeze(1)
-        li = torch.nonzero_static(~s, size=int(s.numel()) - n_split).squeeze(1)
-        gs = g[si]
-        lid = lid_all[si]
-        feat[gs] = sp[si, 0].long()
-        nbin[gs] = sp[si, 1].long()
-        left[gs] = lid
-        glid = nb_d[tree[si]] + lid
-        depth_d = torch.zeros(TB, dtype=i64, device=dev).scatter_reduce_(
-            0, tree[si], lvl_all[si], reduce="amax")
+        li = torch.nonzero_static(sp[:, 0] < 0, size=n_all - n_split).squeeze(1)
         lv_d = tk[li].contiguous()
-        gl = g[li]
+        gl = nb_d[lv_d[:, 0].long()] + nd[li].long()
         nl = int(lv_d.shape[0])
         rd = _Read((lv_d[:, 2] - lv_d[:, 1]).max() if nl else torch.zeros((), dtype=torch.int32,
                                                                               device=dev))
@@ -614,28 +610,23 @@ class _LevelGrower:
         stats_d = torch.empty(4 * max(nl, 1), dtype=i64, device=dev)
         _check(L.gk_rf_leaf_stats(_ptr(counts), n, D["F"], _ptr(D["yfp"]), _ptr(D["y2fp"]), _ptr(lv_d),
                                   nl, _ptr(rows0), _ptr(rows1), _ptr(stats_d), max_leaf, st))
-        # split tasks per level (host counts from the level loop) bound the
-        # bottom-up segments of gs / glid
-        seg = np.concatenate([[0], np.cumsum([r[5] for r in records])]).astype(np.int64)
-        lvl_split = [(gs[seg[k]: seg[k + 1]], glid[seg[k]: seg[k + 1]])
-                     for k in range(len(records)) if seg[k + 1] > seg[k]]
-        # exact integer sums bottom-up, converted to float64 once per node
+        # exact integer sums bottom-up, one native launch per level
         ist = torch.zeros((N, 4), dtype=i64, device=dev)
         ist[gl] = stats_d[: 4 * nl].view(nl, 4)
-        for pa, ch in reversed(lvl_split):
-            ist[pa] = ist[ch] + ist[ch + 1]
-        is_split = left >= 0
-        thr_t = self._dev_thr
-        w = ist[:, 1].double()
-        s2 = ist[:, 2].double() * (2.0 ** -D["shift"])  # == np.ldexp (power-of-two scale)
-        s3 = ist[:, 3].double() * (2.0 ** -D["shift2"])
-        val = s2 / w
-        fl = torch.stack([torch.where(is_split, thr_t[feat.clamp(min=0), nbin],
-                                      torch.full_like(w, float(TREE_UNDEFINED))),
-                          val, s3 / w - val * val, w])
-        it = torch.stack([left, torch.where(is_split, left + 1, torch.full_like(left, TREE_LEAF)),
-                          feat, ist[:, 0]])
-        reads = [_Read(s2[gl] / w[gl]), _Read(depth_d), _Read(lv_d)]
+        off = np.concatenate([[0], np.cumsum([r[4] for r in records])]).astype(np.int64)
+        for k in range(len(records) - 1, -1, -1):
+            if records[k][5] == 0:
+                continue
+            o, c = int(off[k]), int(records[k][4])
+            _check(L.gk_rf_assemble_up(_ptr(tk[o:]), _ptr(sp[o:]), _ptr(nd[o:]), _ptr(lid_all[o:]),
+                                       c, _ptr(nb_d), _ptr(ist), st))
+        fl = torch.empty((4, N), dtype=torch.float64, device=dev)
+        it = torch.empty((4, N), dtype=i64, device=dev)
+        _check(L.gk_rf_assemble_final(N, _ptr(ist), _ptr(feat), _ptr(nbin), _ptr(left),
+                                      _ptr(self._dev_thr), D["shift"], D["shift2"], _ptr(fl),
+                                      _ptr(it), st))
+        leaf_val_d = fl[1][gl]
+        reads = [_Read(leaf_val_d), _Read(depth_d), _Read(lv_d)]
         yield reads[-1]
         leaf_value, tree_depth, lv = (r.get() for r in reads)
         lv = lv.view(TASK_DT).reshape(-1)
