@@ -187,8 +187,8 @@ __global__ void k5_compact(RfTrainData D, int n_trees, const int64_t *__restrict
     if ((D.F & 15) == 0) {  // rows of Xb are 16-byte aligned
         for (int k = 0; k < D.F; k += 16)
             *reinterpret_cast<uint4 *>(r + kRecHdr + k) = *reinterpret_cast<const uint4 *>(xb + k);
-    } else {
-        for (int k = 0; k < D.F; k++) r[kRecHdr + k] = xb[k];
+    } else {  // the zero padding is written too (whole 16-byte groups move later)
+        for (int k = 0; k < rec_stride(D.F) - kRecHdr; k++) r[kRecHdr + k] = k < D.F ? xb[k] : 0;
     }
 }
 

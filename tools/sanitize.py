@@ -37,6 +37,8 @@ for layout in ("nodes", "nodes8", "blocks"):
     rt.rf_predict(de, torch.tensor(X, device="cuda"))      # K4 (+ compact walks)
 Xf, y = rng.random((3000, 8)), rng.random(3000)
 RandomForestRegressor(5, max_depth=6, random_state=0).fit(Xf, y)   # K5 (medium / mid / small / tiny)
+X64, y64 = rng.random((20000, 64)), rng.random(20000)
+RandomForestRegressor(3, max_depth=14, random_state=0).fit(X64, y64)  # K5 F = 64: vector paths, fused partitions
 Xb, yb = rng.random((60000, 8)), rng.random(60000)
 RandomForestRegressor(2, max_depth=2, random_state=0).fit(Xb, yb)  # K5 big-node path
 GradientBoostingRegressor(5, random_state=0).fit(Xf, y)            # K5 + gb_step
