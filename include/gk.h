@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define GK_ABI_VERSION 4
+#define GK_ABI_VERSION 5
 
 /* resource / class codes (reference ptx/types.py:12-24) */
 enum { GK_SP = 0, GK_SFU = 1, GK_DPU = 2, GK_LSU = 3, GK_WS = 4, GK_NRES = 5 };
@@ -192,6 +192,29 @@ typedef struct { uint32_t t; uint32_t meta; } gk_node8;
 #define GK_LEAF 0x80000000u
 typedef struct { uint32_t t[3]; uint32_t f; uint32_t e[4]; } gk_block2;
 
+/* Three-level walk block (32 B, optional; one 256-bit load per lane per three
+ * levels).  Keys: k(v) = the top 16 bits of the order-preserving bits of
+ * round-toward-(-inf)-f32(v), -0.0 taken as +0.0, NaN -> 0xFFFF (a NaN
+ * threshold -> 0: x <= NaN is false for every x).  Decision
+ * at a node: a = k(x[f]) vs t = k(threshold); a < t -> left, a > t -> right,
+ * a == t -> the exact fp64 test x <= thr64[7 * block + node] (equals `x <=
+ * threshold` for every x incl. NaN, +-inf, -0.0).  Blocks sit at depths 0, 3,
+ * 6, ... of a tree (ids level by level in (parent, slot) order), of two kinds
+ * (type = byte 22):
+ *   type 0, a 3-level subtree: nodes 0..6 (node k's children 2k+1, 2k+2),
+ *     w[0..3] = 16-bit keys t[0..6] (t[k] at halfword k), features f[0..6]
+ *     at bytes 14..20, leaf mask at byte 21 (bit s: exit slot s is a leaf),
+ *     w[6] = first child block id, w[7] = first leaf id; exit slot s = 4 b0 +
+ *     2 b1 + b2 (b = went right) is leaf_base + #leaf slots below s or
+ *     block_base + #block slots below s.  A leaf inside the subtree is padded
+ *     (its nodes route anywhere, all of its slots name that leaf).
+ *   type 1, terminal (a node whose children are both leaves): its key and
+ *     feature where type 0 keeps node 0's (halfword 0, byte 14), the left /
+ *     right leaf values (f64) in w[1..2] / w[6..7].
+ * Leaf ids (leaf_val index) stay below 2^30. */
+typedef struct { uint32_t w[8]; } gk_block3;
+#define GK_B3_TERMINAL 1u
+
 typedef struct {
     const gk_node *nodes;
     const int64_t *tree_off;    /* n_trees                        */
@@ -207,6 +230,9 @@ typedef struct {
     const double    *thr64;     /* 3 per block: exact thresholds (tie test)  */
     const double    *leaf_val;  /* per leaf id                               */
     const uint32_t  *root;      /* n_trees: root block id or GK_LEAF | leaf  */
+    /* gk_block3 form (thr64 then 7 per block, leaf_val / root its own); the
+     * walks use it when set */
+    const gk_block3 *blocks3;
 } gk_ensemble;
 
 /* ------------------------------------------------------------------------ */

@@ -33,7 +33,7 @@ class GkEnsemble(C.Structure):
     _fields_ = [("nodes", P), ("tree_off", P), ("tree_depth", P), ("scale_lo", P), ("scale_hi", P),
                 ("base_score", C.c_double), ("n_trees", C.c_uint32), ("n_feat", C.c_uint32),
                 ("max_depth", C.c_uint32), ("nodes8", P), ("blocks", P), ("thr64", P), ("leaf_val", P),
-                ("root", P)]
+                ("root", P), ("blocks3", P)]
 
 
 NSI, NSF, NFEAT = 6, 9, 32
@@ -43,4 +43,4 @@ SF_NAMES = ("gm_latency", "d_kernel", "overhead_cycles", "gm_penalty", "sm_penal
             "cm_penalty", "d_total", "time_us", "cfg_delay")
 STATUS_OK, STATUS_INFEASIBLE_LAUNCH, STATUS_INFEASIBLE_OCCUPANCY = 0, 1, 2
 
-assert C.sizeof(GkCorpus) == 72 and C.sizeof(GkGrid) == 80 and C.sizeof(GkEnsemble) == 104
+assert C.sizeof(GkCorpus) == 72 and C.sizeof(GkGrid) == 80 and C.sizeof(GkEnsemble) == 112

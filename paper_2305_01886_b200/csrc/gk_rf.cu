@@ -130,21 +130,30 @@ __global__ void __launch_bounds__(kRfThreads) k4_rf_predict(RfArgs R) {
 // [feature][row] (stride kRfThreads: each walk read -- lane-varying feature,
 // one row per lane -- hits 32 distinct banks).
 // The exact fp64 feature is recomputed from X only for the rare a == t visit.
-template <bool kBlocks>
+#ifndef GK_RF_B3_ILP
+#define GK_RF_B3_ILP 8  // trees in lock-step per thread, gk_block3 walk
+#endif
+// kMode 0: gk_node8, 1: gk_block2 (f32 key tile), 2: gk_block3 (16-bit key
+// tile, include/gk.h: half the shared memory per row)
+template <int kMode>
 __device__ __forceinline__ void rf_tile_c(const RfArgs &R, int64_t tile, float *xf_raw) {
     constexpr int S = kRfThreads;
     float *xf = xf_raw + S;  // row -1: the +inf slot of the leaf step
+    uint16_t *xk = reinterpret_cast<uint16_t *>(xf_raw);
     const int64_t row0 = tile * kRfThreads;
     const int nr = (int)min((int64_t)kRfThreads, R.n_rows - row0);
     const int nf = (int)R.ens[0].n_feat;
-    xf_raw[threadIdx.x] = __int_as_float(0x7f800000);
+    if (kMode != 2) xf_raw[threadIdx.x] = __int_as_float(0x7f800000);
     for (int q = threadIdx.x; q < nr * nf; q += kRfThreads) {
         const int r = q / nf, f = q - r * nf;
         const int64_t row = row0 + r;
         const uint32_t ai = R.n_cfg ? (uint32_t)((row / R.n_cfg) % R.n_arch) : 0u;
         const gk_ensemble &Er = R.ens[ai < R.n_ens ? ai : 0];
         const double v = scale_feature(R.X[row * R.ld + f], Er.scale_lo[f], Er.scale_hi[f]);
-        xf[f * S + r] = __double2float_rd(v);
+        if (kMode == 2)
+            xk[f * S + r] = (uint16_t)key16(v);
+        else
+            xf[f * S + r] = __double2float_rd(v);
     }
     __syncthreads();
     if ((int)threadIdx.x >= nr) return;
@@ -159,16 +168,17 @@ __device__ __forceinline__ void rf_tile_c(const RfArgs &R, int64_t tile, float *
     }
     const double *xrow = R.X + row * R.ld;
     auto x64 = [&](int f) { return scale_feature(xrow[f], E.scale_lo[f], E.scale_hi[f]); };
-    const double total = kBlocks ? walk_ensemble_b2<GK_RF_B2_ILP>(E, xf + threadIdx.x, S, x64)
-                                 : walk_ensemble8<GK_RF_ILP>(E, xf + threadIdx.x, S, x64);
+    const double total = kMode == 2 ? walk_ensemble_b3<GK_RF_B3_ILP>(E, xk + threadIdx.x, S, x64)
+                       : kMode == 1 ? walk_ensemble_b2<GK_RF_B2_ILP>(E, xf + threadIdx.x, S, x64)
+                                    : walk_ensemble8<GK_RF_ILP>(E, xf + threadIdx.x, S, x64);
     R.power[row] = total;
     if (R.energy) R.energy[row] = __dmul_rn(total, R.time_us[row]);
 }
 
-template <bool kBlocks>
+template <int kMode>
 __global__ void __launch_bounds__(kRfThreads) k4_rf_predict_c(RfArgs R) {
     extern __shared__ __align__(16) float xf_raw[];
-    rf_tile_c<kBlocks>(R, blockIdx.x, xf_raw);
+    rf_tile_c<kMode>(R, blockIdx.x, xf_raw);
 }
 
 // Persistent form for large row tables: every resident CTA takes one tile per
@@ -176,14 +186,14 @@ __global__ void __launch_bounds__(kRfThreads) k4_rf_predict_c(RfArgs R) {
 // walks the same few trees at any time -- the working set is a handful of
 // trees (L2-resident) instead of the entire ensemble (> L2), which turns the
 // deep-level node gathers from DRAM into L2 hits.
-template <bool kBlocks>
+template <int kMode>
 __global__ void __launch_bounds__(kRfThreads) k4_rf_predict_rounds(RfArgs R, int64_t n_tiles) {
     extern __shared__ __align__(16) float xf_raw[];
     cg::grid_group grid = cg::this_grid();
     const int64_t rounds = (n_tiles + gridDim.x - 1) / gridDim.x;
     for (int64_t k = 0; k < rounds; k++) {
         const int64_t tile = k * gridDim.x + blockIdx.x;
-        if (tile < n_tiles) rf_tile_c<kBlocks>(R, tile, xf_raw);
+        if (tile < n_tiles) rf_tile_c<kMode>(R, tile, xf_raw);
         grid.sync();
     }
 }
@@ -222,14 +232,18 @@ int gk_launch_rf(const gk_ensemble *ens, uint32_t n_ens, const double *X, int64_
     R.energy = energy;
     R.n_cfg = n_cfg;
     R.n_arch = n_arch ? n_arch : 1;
-    bool all_blocks = true, all_n8 = true;
+    bool all_b3 = true, all_blocks = true, all_n8 = true;
     for (uint32_t a = 0; a < n_ens; a++) {
+        all_b3 &= ens[a].blocks3 != nullptr;
         all_blocks &= ens[a].blocks != nullptr;
         all_n8 &= ens[a].nodes8 != nullptr;
     }
-    if (all_blocks || all_n8) {
-        const size_t smem8 = ((size_t)nf + 1) * gk::kRfThreads * sizeof(float);
-        const auto k8 = all_blocks ? gk::k4_rf_predict_c<true> : gk::k4_rf_predict_c<false>;
+    if (all_b3 || all_blocks || all_n8) {
+        const int mode = all_b3 ? 2 : all_blocks ? 1 : 0;
+        const size_t smem8 = mode == 2 ? (size_t)nf * gk::kRfThreads * sizeof(uint16_t)
+                                       : ((size_t)nf + 1) * gk::kRfThreads * sizeof(float);
+        const auto k8 = mode == 2 ? gk::k4_rf_predict_c<2>
+                      : mode == 1 ? gk::k4_rf_predict_c<1> : gk::k4_rf_predict_c<0>;
         if (smem8 > 48 * 1024)
             cudaFuncSetAttribute(k8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem8);
         int per_sm = 0;
@@ -244,7 +258,8 @@ int gk_launch_rf(const gk_ensemble *ens, uint32_t n_ens, const double *X, int64_
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
         cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
-        const auto kp = all_blocks ? gk::k4_rf_predict_rounds<true> : gk::k4_rf_predict_rounds<false>;
+        const auto kp = mode == 2 ? gk::k4_rf_predict_rounds<2>
+                      : mode == 1 ? gk::k4_rf_predict_rounds<1> : gk::k4_rf_predict_rounds<0>;
         int per_sm_p = 0;
         if (smem8 > 48 * 1024)
             cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem8);
@@ -267,7 +282,8 @@ int gk_launch_rf(const gk_ensemble *ens, uint32_t n_ens, const double *X, int64_
             return gk_check_launch("k4_rf_predict_rounds");
         }
         k8<<<(unsigned)tiles, gk::kRfThreads, smem8, st>>>(R);
-        return gk_check_launch(all_blocks ? "k4_rf_predict_c<blocks>" : "k4_rf_predict_c<nodes8>");
+        return gk_check_launch(mode == 2 ? "k4_rf_predict_c<blocks3>"
+                               : mode == 1 ? "k4_rf_predict_c<blocks>" : "k4_rf_predict_c<nodes8>");
     }
     // one tile: leading +inf row + [feature][thread] (the staged raw rows are
     // transposed in place through registers)

@@ -233,6 +233,121 @@ __device__ __forceinline__ double walk_ensemble_b2(const gk_ensemble &E, const f
     return total;
 }
 
+// ---- three-level blocks with 16-bit keys (gk_block3, include/gk.h)
+// One 256-bit load per tree per three levels, and the last split level's
+// leaves inline (terminal blocks): a depth-16 path is 6 scattered 32-byte
+// loads instead of the two-level blocks' 8 + a leaf-value load.  Scattered
+// per-lane loads cost one L1/TEX wavefront per distinct 128-byte line
+// (tools/ubench/gather.cu: 0.99 per SM-cycle on every load path), so the
+// walk's ceiling rises with the lines it avoids.
+__device__ __forceinline__ uint32_t key16(double v) {  // include/gk.h gk_block3 keys
+    float a = __double2float_rd(v);
+    if (a == 0.0f) a = 0.0f;  // -0.0 == +0.0
+    const uint32_t u = __float_as_uint(a);
+    const uint32_t o = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+    return a != a ? 0xFFFFu : o >> 16;
+}
+
+#define GK_B3_INLINE 0x40000000u  // done, value in val[] (terminal block)
+
+// one block step of one tree: the fast decisions (ties flagged), the exact
+// redo of a block with a tie out of line
+template <class KeyAt, class X64>
+__device__ __forceinline__ void b3_step(const gk_ensemble &E, const uint32_t (&w)[8],
+                                        uint32_t &ref, double &val, const KeyAt &key,
+                                        const X64 &x64) {
+    const uint32_t blk = ref;
+    const uint32_t f0 = (w[3] >> 16) & 0xFFu, t0 = w[0] & 0xFFFFu;
+    const uint32_t a0 = key(f0);
+    uint32_t b0 = a0 > t0;
+    if (((w[5] >> 16) & 0xFFu) == GK_B3_TERMINAL) {  // node 0 only; leaves inline
+        if (__builtin_expect(a0 == t0, 0)) b0 = !(x64((int)f0) <= E.thr64[7 * (size_t)blk]);
+        val = __hiloint2double(b0 ? w[7] : w[2], b0 ? w[6] : w[1]);
+        ref = GK_LEAF | GK_B3_INLINE;
+        return;
+    }
+    uint32_t tie = a0 == t0;
+    // level 1: node 1 + b0; level 2: node 3 + 2 b0 + b1 (halfwords 3..6 and
+    // feature bytes 17..20 as one 64-bit / 32-bit funnel each)
+    const uint32_t t1 = b0 ? (w[1] & 0xFFFFu) : (w[0] >> 16);
+    const uint32_t f1 = b0 ? (w[4] & 0xFFu) : (w[3] >> 24);
+    const uint32_t a1 = key(f1);
+    uint32_t b1 = a1 > t1;
+    tie |= a1 == t1;
+    const uint64_t T2 = (uint64_t)(w[1] >> 16) | ((uint64_t)w[2] << 16) |
+                        ((uint64_t)(w[3] & 0xFFFFu) << 48);
+    const uint32_t F2 = __funnelshift_r(w[4], w[5], 8);
+    uint32_t j = 2 * b0 + b1;
+    uint32_t t2 = (uint32_t)(T2 >> (16 * j)) & 0xFFFFu, f2 = (F2 >> (8 * j)) & 0xFFu;
+    const uint32_t a2 = key(f2);
+    uint32_t b2 = a2 > t2;
+    tie |= a2 == t2;
+    if (__builtin_expect(tie != 0, 0)) {  // exact fp64 tests, in path order
+        const double *th = E.thr64 + 7 * (size_t)blk;
+        b0 = a0 == t0 ? !(x64((int)f0) <= th[0]) : a0 > t0;
+        const uint32_t tt1 = b0 ? (w[1] & 0xFFFFu) : (w[0] >> 16);
+        const uint32_t ff1 = b0 ? (w[4] & 0xFFu) : (w[3] >> 24);
+        const uint32_t aa1 = key(ff1);
+        b1 = aa1 == tt1 ? !(x64((int)ff1) <= th[1 + b0]) : aa1 > tt1;
+        j = 2 * b0 + b1;
+        t2 = (uint32_t)(T2 >> (16 * j)) & 0xFFFFu;
+        f2 = (F2 >> (8 * j)) & 0xFFu;
+        const uint32_t aa2 = key(f2);
+        b2 = aa2 == t2 ? !(x64((int)f2) <= th[3 + j]) : aa2 > t2;
+    }
+    const uint32_t s = 4 * b0 + 2 * b1 + b2;
+    const uint32_t mask = (w[5] >> 8) & 0xFFu, below = (1u << s) - 1u;
+    ref = (mask >> s & 1u) ? (GK_LEAF | (w[7] + __popc(mask & below)))
+                           : (w[6] + __popc(~mask & below & 0xFFu));
+}
+
+// trees t .. t + nq - 1 (kIlp in lock-step); xk: this row's 16-bit keys,
+// feature f at xk[f * stride]
+template <int kIlp, bool kTail, class X64>
+__device__ __forceinline__ void walk_b3_group(const gk_ensemble &E, uint32_t t, int nq,
+                                              const uint16_t *xk, int stride, const X64 &x64,
+                                              double &total) {
+    const gk_block3 *__restrict__ B = E.blocks3;
+    uint32_t ref[kIlp];
+    double val[kIlp];
+    int d = 0;
+#pragma unroll
+    for (int q = 0; q < kIlp; q++) {  // idle slots of a partial group start done
+        const bool on = !kTail || q < nq;
+        ref[q] = on ? __ldg(E.root + t + q) : (GK_LEAF | GK_B3_INLINE);
+        val[q] = 0.0;
+        if (on) d = max(d, __ldg(E.tree_depth + t + q));
+    }
+    auto key = [&](uint32_t f) { return (uint32_t)xk[f * stride]; };
+    const int steps = d > 0 ? (d - 1) / 3 + 1 : 0;
+    for (int st = 0; st < steps; st++) {
+        uint32_t w[kIlp][8];
+#pragma unroll
+        for (int q = 0; q < kIlp; q++)
+            if (!(ref[q] & GK_LEAF)) ld_block2(reinterpret_cast<const gk_block2 *>(B + ref[q]), w[q]);
+#pragma unroll
+        for (int q = 0; q < kIlp; q++)
+            if (!(ref[q] & GK_LEAF)) b3_step(E, w[q], ref[q], val[q], key, x64);
+    }
+#pragma unroll
+    for (int q = 0; q < kIlp; q++)
+        if (!kTail || q < nq)
+            total = __dadd_rn(total, (ref[q] & GK_B3_INLINE)
+                                         ? val[q]
+                                         : __ldg(E.leaf_val + (ref[q] & ~(GK_LEAF | GK_B3_INLINE))));
+}
+
+template <int kIlp, class X64>
+__device__ __forceinline__ double walk_ensemble_b3(const gk_ensemble &E, const uint16_t *xk,
+                                                   int stride, const X64 &x64) {
+    double total = E.base_score;
+    uint32_t t = 0;
+    for (; t + kIlp <= E.n_trees; t += kIlp)
+        walk_b3_group<kIlp, false>(E, t, kIlp, xk, stride, x64, total);
+    if (t < E.n_trees) walk_b3_group<kIlp, true>(E, t, (int)(E.n_trees - t), xk, stride, x64, total);
+    return total;
+}
+
 // power.py:144 -- (v - lo) / (hi - lo), or 0 when hi <= lo
 __device__ __forceinline__ double scale_feature(double v, double lo, double hi) {
     return hi > lo ? __ddiv_rn(__dsub_rn(v, lo), __dsub_rn(hi, lo)) : 0.0;

@@ -481,6 +481,160 @@ def blocked(flat: FlatEnsemble) -> Blocked | None:
                    root=ref(flat.tree_off.astype(np.int64)))
 
 
+# ---------------------------------------------------------------- gk_block3
+# Three-level blocks with 16-bit keys (include/gk.h gk_block3): one 32-byte load
+# per three levels, the last split level's leaves inline ("terminal" blocks),
+# so a depth-16 path costs 6 scattered 32-byte loads instead of the 2-level
+# blocks' 8 + a leaf-value load (the walks are bound by one distinct L1 line per
+# lane per load, tools/ubench/gather.cu).
+BLOCK3_DT = np.dtype([("w", "<u4", (8,))])
+B3_TERMINAL = 1
+BLOCK3_MAX_FEAT = 255
+
+
+def key16(v: np.ndarray) -> np.ndarray:
+    """16-bit order key of round-down-f32(v): the top half of the f32's
+    order-preserving bits, -0.0 taken as +0.0, NaN -> 0xFFFF (above +inf).
+    a = key16(x) vs t = key16(thr): a < t -> x < thr, a > t -> x > thr (or x
+    NaN), a == t -> the exact fp64 test decides (gk_block3 walk)."""
+    f = f32_round_down(np.asarray(v, dtype=np.float64))
+    f = np.where(f == 0, np.float32(0.0), f).astype(np.float32)
+    u = f.view(np.uint32).astype(np.uint64)
+    o = np.where(u & 0x80000000, ~u & 0xFFFFFFFF, u | 0x80000000) >> 16
+    return np.where(np.isnan(f), 0xFFFF, o).astype(np.uint16)
+
+
+@dataclass
+class Blocked3:
+    """Three-level blocked walk form of a FlatEnsemble (gk_block3, include/gk.h)."""
+
+    blocks: np.ndarray     # BLOCK3_DT [n_blocks]
+    thr64: np.ndarray      # f64 [7 * n_blocks]
+    leaf_val: np.ndarray   # f64 [n_leaf_slots]
+    root: np.ndarray       # u32 [n_trees]: block id, or GK_LEAF | leaf id
+
+
+def blocked3(flat: FlatEnsemble) -> Blocked3 | None:
+    """gk_block3 form of `flat`: a block per internal node at depth 0, 3, 6, ...
+    A node whose two children are leaves becomes a terminal block {key,
+    feature, both leaf values}; any other holds its 3-level subtree (7 nodes;
+    a leaf above the third level is padded: its subtree's nodes route
+    anywhere and all of its slots name that leaf) and 8 exit slots, each a
+    child block (contiguous from block_base in slot order) or a leaf
+    (contiguous from leaf_base).  Blocks are numbered level by level in (parent,
+    slot) order.  None if the ensemble does not fit (> 255 features, >= 2^31
+    blocks or leaf slots)."""
+    nd = flat.nodes
+    N = len(nd)
+    if flat.n_feat > BLOCK3_MAX_FEAT or N == 0 or flat.n_trees == 0:
+        return None
+    sizes = np.diff(np.append(flat.tree_off, N))
+    base = np.repeat(flat.tree_off, sizes)
+    leaf = nd["feature"] < 0
+    left = np.where(leaf, 0, base + nd["left"].astype(np.int64))
+    # height (0 for leaves): children follow their parent in a tree's BFS order
+    depth = np.full(N, -1, np.int64)
+    frontier = flat.tree_off.astype(np.int64)
+    levels = []
+    d = 0
+    while len(frontier):
+        depth[frontier] = d
+        levels.append(frontier)
+        inner = frontier[~leaf[frontier]]
+        frontier = np.concatenate([left[inner], left[inner] + 1])
+        d += 1
+    height = np.zeros(N, np.int64)
+    for fr in reversed(levels):
+        inner = fr[~leaf[fr]]
+        height[inner] = 1 + np.maximum(height[left[inner]], height[left[inner] + 1])
+    # a NaN threshold (x <= NaN is always false) takes key 0, below every
+    # row's key (-inf is 0x007F, a NaN row 0xFFFF): always right, never a tie
+    K = np.where(np.isnan(nd["v"]), 0, key16(nd["v"])).astype(np.uint32)
+    F = np.where(leaf, 0, nd["feature"]).astype(np.uint32)
+    THR = np.where(leaf, np.inf, nd["v"])
+
+    blocks, thr64, leaf_vals = [], [], []
+    n_blocks = 0
+    n_leaves = 0
+    root = np.zeros(flat.n_trees, np.uint32)
+    roots = flat.tree_off.astype(np.int64)
+    rl = leaf[roots]
+    # single-leaf trees: their leaf slots first
+    root[rl] = GK_LEAF | (np.arange(int(rl.sum()), dtype=np.uint32))
+    leaf_vals.append(nd["v"][roots[rl]])
+    n_leaves += int(rl.sum())
+    cur = roots[~rl]                                       # this level's block roots, id order
+    root[~rl] = np.arange(len(cur), dtype=np.uint32)
+    while len(cur):
+        nb = len(cur)
+        w = np.zeros((nb, 8), np.uint32)
+        t64 = np.full((nb, 7), np.inf)
+        term = height[cur] == 1
+        # terminal blocks: key and feature where a 3-level block keeps node 0's
+        # (halfword 0, byte 14), the left / right leaf values in w[1..2] / w[6..7]
+        tc = cur[term]
+        w[term, 0] = K[tc]
+        w[term, 3] = F[tc] << 16
+        lv = nd["v"][left[tc]].view(np.uint64)
+        rv = nd["v"][left[tc] + 1].view(np.uint64)
+        w[term, 1], w[term, 2] = (lv & 0xFFFFFFFF).astype(np.uint32), (lv >> 32).astype(np.uint32)
+        w[term, 6], w[term, 7] = (rv & 0xFFFFFFFF).astype(np.uint32), (rv >> 32).astype(np.uint32)
+        w[term, 5] = B3_TERMINAL << 16
+        t64[term, 0] = THR[tc]
+        # three-level blocks
+        full = ~term
+        r = cur[full]
+        n = np.empty((len(r), 7), np.int64)
+        n[:, 0] = r
+        n[:, 1], n[:, 2] = left[r], left[r] + 1
+        for k in (1, 2):                                  # block-depth 2 (padded under leaves)
+            c = n[:, k]
+            lf = leaf[c]
+            n[:, 3 + 2 * (k - 1)] = np.where(lf, c, left[c])
+            n[:, 4 + 2 * (k - 1)] = np.where(lf, c, left[c] + 1)
+        slots = np.empty((len(r), 8), np.int64)
+        for j in range(4):
+            c = n[:, 3 + j]
+            lf = leaf[c]
+            slots[:, 2 * j] = np.where(lf, c, left[c])
+            slots[:, 2 * j + 1] = np.where(lf, c, left[c] + 1)
+        kk = np.where(leaf[n], 0xFFFF, K[n])              # padded / leaf entries never decide
+        ff = np.where(leaf[n], 0, F[n])
+        t64[full] = np.where(leaf[n], np.inf, THR[n])
+        wf = np.zeros((len(r), 8), np.uint32)
+        wf[:, 0] = kk[:, 0] | (kk[:, 1] << 16)
+        wf[:, 1] = kk[:, 2] | (kk[:, 3] << 16)
+        wf[:, 2] = kk[:, 4] | (kk[:, 5] << 16)
+        wf[:, 3] = kk[:, 6] | (ff[:, 0] << 16) | (ff[:, 1] << 24)
+        wf[:, 4] = ff[:, 2] | (ff[:, 3] << 8) | (ff[:, 4] << 16) | (ff[:, 5] << 24)
+        sl = leaf[slots]                                  # [nb_full, 8]
+        mask = (sl.astype(np.uint32) << np.arange(8, dtype=np.uint32)).sum(axis=1).astype(np.uint32)
+        wf[:, 5] = ff[:, 6] | (mask << 8)
+        n_child = (~sl).sum(axis=1)
+        n_lf = sl.sum(axis=1)
+        wf[:, 6] = (n_blocks + nb + np.concatenate([[0], np.cumsum(n_child)[:-1]])).astype(np.uint32)
+        wf[:, 7] = (n_leaves + np.concatenate([[0], np.cumsum(n_lf)[:-1]])).astype(np.uint32)
+        w[full] = wf
+        blocks.append(w)
+        thr64.append(t64)
+        leaf_vals.append(nd["v"][slots[sl]])             # (parent, slot) order
+        n_leaves += int(n_lf.sum())
+        n_blocks += nb
+        cur = slots[~sl]                                  # next level's roots, (parent, slot) order
+        if n_blocks + len(cur) >= GK_LEAF or n_leaves >= GK_LEAF >> 1:
+            return None
+    out = np.zeros(max(n_blocks, 1), BLOCK3_DT)
+    if n_blocks:
+        out["w"] = np.concatenate(blocks)
+        t = np.concatenate(thr64).reshape(-1)
+    else:   # all trees are single leaves: keep block 0 addressable
+        t = np.full(7, np.inf)
+    return Blocked3(blocks=out, thr64=np.ascontiguousarray(t),
+                    leaf_val=np.ascontiguousarray(np.concatenate(leaf_vals) if leaf_vals
+                                                  else np.zeros(1)),
+                    root=root)
+
+
 def flat_to_document(flat: FlatEnsemble) -> dict:
     """FlatEnsemble -> reference JSON document (for cross-checks on small ensembles)."""
     trees = []

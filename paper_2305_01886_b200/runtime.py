@@ -51,7 +51,7 @@ def load_library(path: Path | None = None):
     L.gk_predict_energy_sweep.argtypes = [vp, vp, vp, vp, u32, vp, vp, vp, vp, vp, vp]
     L.gk_set_stage_timing.argtypes = [C.c_int]
     L.gk_get_stage_ms.argtypes = [vp]
-    if L.gk_abi_version() != 4:
+    if L.gk_abi_version() != 5:
         raise DeviceError("libgk ABI version mismatch")
     if path is None:
         _lib = L
@@ -183,7 +183,7 @@ class DeviceEnsemble:
     bufs: dict = field(default_factory=dict)
     desc: abi.GkEnsemble | None = None
 
-    LAYOUTS = ("nodes", "nodes8", "blocks")
+    LAYOUTS = ("nodes", "nodes8", "blocks", "blocks3")
 
     @classmethod
     def upload(cls, flat, layout: str | None = None) -> "DeviceEnsemble":
@@ -198,7 +198,7 @@ class DeviceEnsemble:
         layout (leaf values, exact tie thresholds)."""
         import os
 
-        from .ensemble import blocked, nodes8
+        from .ensemble import blocked, blocked3, nodes8
 
         layout = layout or os.environ.get("GK_WALK_LAYOUT", "blocks")
         if layout not in cls.LAYOUTS:
@@ -217,6 +217,11 @@ class DeviceEnsemble:
             if bl is not None:
                 de.bufs.update(blocks=_dev(bl.blocks), thr64=_dev(bl.thr64),
                                leaf_val=_dev(bl.leaf_val), root=_dev(bl.root))
+        elif layout == "blocks3":
+            b3 = blocked3(flat)
+            if b3 is not None:
+                de.bufs.update(blocks3=_dev(b3.blocks), thr64=_dev(b3.thr64),
+                               leaf_val=_dev(b3.leaf_val), root=_dev(b3.root))
         de.desc = cls._desc(de.bufs, float(flat.base_score), flat.n_trees, flat.n_feat,
                             flat.max_depth)
         return de
@@ -227,7 +232,8 @@ class DeviceEnsemble:
                               _ptr(b["lo"]), _ptr(b["hi"]), float(base), int(n_trees),
                               int(n_feat), int(max_depth), _ptr(b.get("nodes8")),
                               _ptr(b.get("blocks")), _ptr(b.get("thr64")),
-                              _ptr(b.get("leaf_val")), _ptr(b.get("root")))
+                              _ptr(b.get("leaf_val")), _ptr(b.get("root")),
+                              _ptr(b.get("blocks3")))
 
     @classmethod
     def from_buffers(cls, bufs: dict, *, base: float, n_trees: int, n_feat: int,
@@ -241,7 +247,10 @@ class DeviceEnsemble:
 
     @property
     def layout(self) -> str:
-        return "blocks" if "blocks" in self.bufs else ("nodes8" if "nodes8" in self.bufs else "nodes")
+        for name in ("blocks3", "blocks", "nodes8"):
+            if name in self.bufs:
+                return name
+        return "nodes"
 
 
 # ------------------------------------------------------------------ calls

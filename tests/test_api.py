@@ -113,7 +113,7 @@ def test_c_abi_library_exports_every_header_symbol():
     lib = ctypes.CDLL(str(runtime.LIB_PATH))
     missing = [n for n in sorted(names) if not hasattr(lib, n)]
     assert not missing, missing
-    assert runtime.load_library().gk_abi_version() == 4
+    assert runtime.load_library().gk_abi_version() == 5
 
 
 # ------------------------------------------------------------------ GPU

@@ -17,9 +17,10 @@ import pytest
 from goldens import bits_equal, load_set
 from paper_2305_01886_b200 import pack
 from paper_2305_01886_b200.ensemble import (BLOCK2_MAX_FEAT, GK_LEAF, NODE8_MAX_FEAT, blocked,
-                                            f32_round_down, nodes8, random_forest_flat)
+                                            blocked3, f32_round_down, key16, nodes8,
+                                            random_forest_flat)
 
-LAYOUTS = ("nodes", "nodes8", "blocks")
+LAYOUTS = ("nodes", "nodes8", "blocks", "blocks3")
 
 
 def _adversarial_pairs(rng, n=200_000):
@@ -48,6 +49,21 @@ def test_decision_rule_equals_fp64_compare():
     assert np.array_equal(le, want)
     tie = (a == t)
     assert tie.sum() > 1000  # the exact path is exercised
+
+
+def test_key16_decision_rule_equals_fp64_compare():
+    """gk_block3: 16-bit order keys of round-down-f32 (zeros canonical, NaN
+    top) with the exact test on equal keys == `x <= thr` for every pair."""
+    rng = np.random.default_rng(5)
+    x, T = _adversarial_pairs(rng)
+    ok = ~np.isnan(T)              # thresholds are never NaN
+    x, T = x[ok], T[ok]
+    a, t = key16(x).astype(np.int64), key16(T).astype(np.int64)
+    with np.errstate(invalid="ignore"):
+        le = (a < t) | ((a == t) & (x <= T))
+        want = x <= T
+    assert np.array_equal(le, want)
+    assert (a == t).sum() > 1000 and ((x == 0) & (T == 0)).sum() > 0
 
 
 def test_f32_round_down_is_the_largest_float_below():
@@ -116,6 +132,50 @@ def _walk_nodes(flat, X):
     return out
 
 
+def _walk_blocks3(b3, flat, X):
+    """numpy emulation of walk_ensemble_b3 (device) for a few rows."""
+    from paper_2305_01886_b200.ensemble import B3_TERMINAL, key16
+    out = np.full(len(X), float(flat.base_score))
+    for i, x in enumerate(X):
+        kx = key16(x).astype(np.int64)
+
+        def le(key, f, ref, j):  # x[f] <= threshold j of block ref
+            if kx[f] == key:
+                return bool(x[f] <= b3.thr64[7 * ref + j])
+            return bool(kx[f] < key)
+
+        for t in range(flat.n_trees):
+            ref = int(b3.root[t])
+            val = None
+            while val is None:
+                if ref & GK_LEAF:
+                    val = b3.leaf_val[ref & ~GK_LEAF]
+                    break
+                w = [int(v) for v in b3.blocks[ref]["w"]]
+                if (w[5] >> 16) & 0xFF == B3_TERMINAL:
+                    go_l = le(w[0] & 0xFFFF, (w[3] >> 16) & 0xFF, ref, 0)
+                    lo, hi = (w[1], w[2]) if go_l else (w[6], w[7])
+                    val = np.array([lo | (hi << 32)], np.uint64).view(np.float64)[0]
+                    break
+                keys = [w[0] & 0xFFFF, w[0] >> 16, w[1] & 0xFFFF, w[1] >> 16, w[2] & 0xFFFF,
+                        w[2] >> 16, w[3] & 0xFFFF]
+                feats = [(w[3] >> 16) & 0xFF, w[3] >> 24, w[4] & 0xFF, (w[4] >> 8) & 0xFF,
+                         (w[4] >> 16) & 0xFF, w[4] >> 24, w[5] & 0xFF]
+                k, s = 0, 0
+                for _ in range(3):
+                    b = 0 if le(keys[k], feats[k], ref, k) else 1
+                    s = 2 * s + b
+                    k = 2 * k + 1 + b
+                mask = (w[5] >> 8) & 0xFF
+                below = (1 << s) - 1
+                if mask >> s & 1:
+                    ref = GK_LEAF | (w[7] + bin(mask & below).count("1"))
+                else:
+                    ref = w[6] + bin(~mask & below & 0xFF).count("1")
+            out[i] = out[i] + val
+    return out
+
+
 def test_block_encoding_walks_like_the_nodes():
     rng = np.random.default_rng(3)
     nf = 6
@@ -127,12 +187,34 @@ def test_block_encoding_walks_like_the_nodes():
     want = _walk_nodes(flat, X)
     assert bits_equal(_walk_blocks(bl, flat, X), want)
     assert bits_equal(_walk_nodes8(nodes8(flat), flat, X), want)
+    assert bits_equal(_walk_blocks3(blocked3(flat), flat, X), want)
     wide = random_forest_flat(2, 3, [f"f{i}" for i in range(BLOCK2_MAX_FEAT + 1)],
                               np.zeros(BLOCK2_MAX_FEAT + 1), np.ones(BLOCK2_MAX_FEAT + 1), seed=1)
     assert blocked(wide) is None and nodes8(wide) is None
     mid = random_forest_flat(2, 3, [f"f{i}" for i in range(NODE8_MAX_FEAT + 1)],
                              np.zeros(NODE8_MAX_FEAT + 1), np.ones(NODE8_MAX_FEAT + 1), seed=1)
     assert nodes8(mid) is None and blocked(mid) is not None
+
+
+@pytest.mark.parametrize("n_trees,depth,split_p", [(5, 10, 0.9), (9, 4, 0.5), (3, 16, 0.95),
+                                                   (4, 1, 1.0), (3, 0, 1.0)])
+def test_block3_encoding_walks_like_the_nodes(n_trees, depth, split_p):
+    """terminal blocks, padded subtrees, single-leaf trees, NaN / +-inf / -0.0
+    rows and exact threshold ties"""
+    rng = np.random.default_rng(depth)
+    nf = 6
+    flat = random_forest_flat(n_trees, depth, [f"f{i}" for i in range(nf)], np.zeros(nf),
+                              np.ones(nf), seed=depth, split_p=split_p)
+    X = rng.random((40, nf))
+    X[:15] = flat.nodes["v"][rng.integers(0, len(flat.nodes), (15, nf))]
+    X[15:18] = np.nan
+    X[18, 0], X[19, 1], X[20, 2] = -0.0, np.inf, -np.inf
+    nd = flat.nodes.copy()       # a NaN threshold: x <= NaN is always false
+    sp = np.flatnonzero(nd["feature"] >= 0)
+    if len(sp):
+        nd["v"][sp[len(sp) // 2]] = np.nan
+    flat.nodes = nd
+    assert bits_equal(_walk_blocks3(blocked3(flat), flat, X), _walk_nodes(flat, X))
 
 
 def test_fixture_ensembles_block_like_the_nodes():
@@ -243,7 +325,8 @@ def test_fused_sweep_compact_layouts_tie_heavy_match_oracle():
 
 
 @pytest.mark.gpu
-def test_k4_persistent_rounds_match_oracle():
+@pytest.mark.parametrize("layout", ["blocks", "blocks3"])
+def test_k4_persistent_rounds_match_oracle(layout):
     """Tables spanning several waves of resident CTAs take the grid-synchronised
     persistent path (k4_rf_predict_rounds); same bits as the oracle and as the
     one-tile-per-CTA launch."""
@@ -260,7 +343,8 @@ def test_k4_persistent_rounds_match_oracle():
     flat = random_forest_flat(30, 10, [f"f{i}" for i in range(nf)], np.zeros(nf), np.ones(nf), seed=4)
     flat = _tie_heavy(flat, X[:5000], rng)
     Xd = torch.tensor(X, device="cuda")
-    de = rt.DeviceEnsemble.upload(flat, layout="blocks")
+    de = rt.DeviceEnsemble.upload(flat, layout=layout)
+    assert de.layout == layout
     p_rounds, _ = rt.rf_predict(de, Xd)
     os.environ["GK_RF_ROUNDS"] = "0"
     try:
