@@ -551,6 +551,9 @@ struct FusedArgs {
 #ifndef GK_FUSED_B2_SINK
 #define GK_FUSED_B2_SINK 1
 #endif
+#ifndef GK_FUSED_B2_LDS2
+#define GK_FUSED_B2_LDS2 1  // 2 shared feature loads per block (gk_walk.cuh): c5 127.2 -> 134.3 M points/s
+#endif
 #ifndef GK_FUSED_B2_ILP
 #define GK_FUSED_B2_ILP 5  // blocked walk: trees in lock-step (each step = 2 levels); c2 at MINB 8: 6.22 ms (4: 6.40, 6: 6.49)
 #endif
@@ -739,7 +742,7 @@ __global__ void __launch_bounds__(kWarps * 32, kFused ? GK_FUSED_MINB : GK_K23_M
                     // once its loads are unpredicated (sink) and its feature
                     // offsets are one PRMT: 6.36 vs 6.44 ms; nodes8 loses
                     pw = F.compact && Ep->blocks
-                             ? walk_ensemble_b2<GK_FUSED_B2_ILP, true, GK_FUSED_B2_SINK>(*Ep, xf, kXfStride, x64)
+                             ? walk_ensemble_b2<GK_FUSED_B2_ILP, true, GK_FUSED_B2_SINK, GK_FUSED_B2_LDS2>(*Ep, xf, kXfStride, x64)
                          : F.compact && Ep->nodes8 ? walk_ensemble8<GK_FUSED_ILP>(*Ep, xf, kXfStride, x64)
                                                    : walk_ensemble<GK_FUSED_ILP>(*Ep, xw, 32);
                     en = __dmul_rn(pw, t_ok);

@@ -145,7 +145,7 @@ __device__ __forceinline__ void ld_block2(const gk_block2 *p, uint32_t (&w)[8]) 
 // instructions and registers for more L1 wavefronts.  Measured on B200: the
 // fused sweep (issue-bound with this walk) wants both; K4 on config #4
 // (L1-wavefront-bound) loses 10 % with kSink and gains nothing from kS64.
-template <int kIlp, bool kTail, bool kS64, bool kSink, class X64>
+template <int kIlp, bool kTail, bool kS64, bool kSink, bool kLds2, class X64>
 __device__ __forceinline__ void walk_b2_group(const gk_ensemble &E, uint32_t t, int nq,
                                               const float *xf, int stride, const X64 &x64,
                                               double &total) {
@@ -177,22 +177,34 @@ __device__ __forceinline__ void walk_b2_group(const gk_ensemble &E, uint32_t t, 
                 for (int k = 0; k < 8; k++) w[q][k] = 0;
             }
         }
+        auto feat = [&](uint32_t fw, uint32_t k) {  // feature byte k of fw -> its tile value
+            return kS64 ? *reinterpret_cast<const float *>(reinterpret_cast<const char *>(xf) +
+                                                           __byte_perm(fw, 0u, 0x4404u | (k << 4)))
+                        : xf[((fw >> (8 * k)) & 0xFFu) * stride];
+        };
         float a[kIlp][3];
+        if (kLds2) {
+            // two shared loads per block: the second level's feature after the
+            // first decision (each LDS is an L1/TEX data-pipe wavefront, shared
+            // with the block loads' lines)
 #pragma unroll
-        for (int q = 0; q < kIlp; q++)
+            for (int q = 0; q < kIlp; q++) a[q][0] = feat(w[q][3], 0u);
 #pragma unroll
-            for (int k = 0; k < 3; k++)
-                a[q][k] = kS64 ? *reinterpret_cast<const float *>(
-                                     reinterpret_cast<const char *>(xf) +
-                                     __byte_perm(w[q][3], 0u, 0x4404u | (k << 4)))
-                               : xf[((w[q][3] >> (8 * k)) & 0xFFu) * stride];
+            for (int q = 0; q < kIlp; q++)
+                a[q][1] = feat(w[q][3], a[q][0] < __uint_as_float(w[q][0]) ? 1u : 2u);
+        } else {
+#pragma unroll
+            for (int q = 0; q < kIlp; q++)
+#pragma unroll
+                for (int k = 0; k < 3; k++) a[q][k] = feat(w[q][3], (uint32_t)k);
+        }
         uint32_t tie = 0;
         uint32_t nref[kIlp];
 #pragma unroll
         for (int q = 0; q < kIlp; q++) {
             const float t0 = __uint_as_float(w[q][0]);
             const bool c0 = a[q][0] < t0;
-            const float as = c0 ? a[q][1] : a[q][2];
+            const float as = kLds2 ? a[q][1] : (c0 ? a[q][1] : a[q][2]);
             const float ts = __uint_as_float(c0 ? w[q][1] : w[q][2]);
             const bool c1 = as < ts;
             tie |= (((a[q][0] == t0) | (as == ts)) && !(ref[q] & GK_LEAF) ? 1u : 0u) << q;
@@ -221,15 +233,21 @@ __device__ __forceinline__ void walk_b2_group(const gk_ensemble &E, uint32_t t, 
         if (!kTail || q < nq) total = __dadd_rn(total, __ldg(E.leaf_val + (ref[q] & ~GK_LEAF)));
 }
 
-template <int kIlp, bool kS64 = false, bool kSink = false, class X64>
+// kLds2: two shared feature loads per block instead of three (the second
+// after the first decision).  Measured on B200: the fused sweep on config #5
+// 127.2 -> 134.3 M points/s (its L1/TEX data pipe also serves the scheduler's
+// tables); K4 alone on config #4 82.1 -> 73.8 M rows/s (the dependent load
+// lengthens its latency-bound chain) -- so only the sweep uses it.
+template <int kIlp, bool kS64 = false, bool kSink = false, bool kLds2 = false, class X64>
 __device__ __forceinline__ double walk_ensemble_b2(const gk_ensemble &E, const float *xf, int stride,
                                                    const X64 &x64) {
     double total = E.base_score;
     uint32_t t = 0;
     for (; t + kIlp <= E.n_trees; t += kIlp)
-        walk_b2_group<kIlp, false, kS64, kSink>(E, t, kIlp, xf, stride, x64, total);
+        walk_b2_group<kIlp, false, kS64, kSink, kLds2>(E, t, kIlp, xf, stride, x64, total);
     if (t < E.n_trees)
-        walk_b2_group<kIlp, true, kS64, kSink>(E, t, (int)(E.n_trees - t), xf, stride, x64, total);
+        walk_b2_group<kIlp, true, kS64, kSink, kLds2>(E, t, (int)(E.n_trees - t), xf, stride, x64,
+                                                     total);
     return total;
 }
 
