@@ -28,7 +28,10 @@ def _port() -> int:
 @pytest.mark.gpu
 def test_bench_torchrun_two_ranks_gloo_on_one_gpu():
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-           "--master-addr=127.0.0.1", f"--master-port={_port()}", str(ROOT / "bench.py"),
+           "--master-addr=127.0.0.1", f"--master-port={_port()}",
+           # the agent's own address: without it torchrun resolves the box's
+           # hostname, which hung the rendezvous on some GPU boxes
+           "--local-addr=127.0.0.1", str(ROOT / "bench.py"),
            "--gpus", "2", "--backend", "gloo", "--kernels", "1000", "--cycle-kernels", "1000",
            "--steps", "2", "--warmup", "3", "--trees", "24", "--depth", "8", "--no-rf",
            "--no-c4", "--cpu-seconds", "1", "--e2e-steps", "1"]
