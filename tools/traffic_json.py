@@ -36,6 +36,8 @@ def num(v):
     return float(str(v[0]).replace(",", "")) * SCALE.get(v[1], 1)
 
 
+OUT = ROOT / "profiles" / "r2" / "traffic.json"
+old = json.loads(OUT.read_text()) if OUT.exists() else {}
 out = {"_doc": "dram__bytes_read.sum + dram__bytes_write.sum per launch and the binding "
                "unit's utilisation from one `ncu --set full --clock-control none` capture "
                "(tools/profile_round.sh) of the command named; bench.py reports it as "
@@ -58,6 +60,11 @@ for f, (wl, kern, units, unit, cap) in CAPS.items():
         "warps_active_pct": num(rec.get("sm__warps_active.avg.pct_of_peak_sustained_active")),
         "l2_hit_pct": num(rec.get("lts__t_sector_hit_rate.pct")),
     }
-dst = ROOT / "profiles" / "r2" / "traffic.json"
+for wl, kerns in old.items():   # entries whose capture is not in this pass stay
+    if wl.startswith("_"):
+        continue
+    for kern, rec in kerns.items():
+        out.setdefault(wl, {}).setdefault(kern, rec)
+dst = OUT
 dst.write_text(json.dumps(out, indent=1) + "\n")
 print(dst.read_text())
