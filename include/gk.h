@@ -319,13 +319,20 @@ int gk_rf_bin(const double *X, int64_t n_rows, int32_t n_feat, int64_t ld, const
  * rows are partitioned by their split search (records moved to the other
  * buffer): their split record has pad = 1 and n_left = the left row count;
  * for the others (pad = 0) n_left is NOT filled -- gk_rf_partition_lists moves
- * their records and its cursor gives the left row count */
+ * their records and its cursor gives the left row count.  Big tasks keep
+ * their histograms in hist_ws (gk_rf_hist_bytes; interleaved {weight, sum}
+ * per bin, slot = position in big_ids); slot_cur[n_tasks] receives each
+ * task's slot (-1: not big).  Sibling subtraction (optional: prev_hist_ws /
+ * par_slot non-null, par_slot from gk_rf_next_level): of two big siblings
+ * the smaller is built, the larger = the parent's histogram (prev_hist_ws at
+ * par_slot) - the smaller's. */
 int gk_rf_split_level(const uint8_t *Xb, const int64_t *yfp, const double *y,
                       const uint32_t *counts, int64_t n_rows, int32_t n_feat,
                       const void *tasks, const int32_t *small_ids, int32_t n_small,
                       const int32_t *med_ids, int32_t n_med, const int32_t *big_ids,
                       int32_t n_big, int32_t big_max_chunks, void *recs0, void *recs1,
-                      void *hist_ws, void *split_out, void *stream);
+                      void *hist_ws, void *split_out, const void *prev_hist_ws,
+                      const int32_t *par_slot, int32_t *slot_cur, int32_t n_tasks, void *stream);
 size_t gk_rf_hist_bytes(int32_t n_big, int32_t n_feat);
 /* move each split task's records to the other buffer: left rows up from begin,
  * right rows down from end; cursor[2*i] ends as task i's left row count (n_left) */
@@ -348,11 +355,14 @@ int gk_rf_partition(const uint8_t *Xb, const int64_t *yfp, const double *y,
  * task count, the three list lengths, largest medium / big child.  scratch:
  * gk_rf_level_scratch_bytes. */
 size_t gk_rf_level_scratch_bytes(int32_t n_tasks, int32_t n_trees);
+/* slot_cur (this level's big slots from gk_rf_split_level, or NULL) and
+ * par_slot_next (2 * n_tasks, or NULL): each child's parent histogram slot */
 int gk_rf_next_level(const void *tasks, const int32_t *node, const void *split,
                      const int32_t *cursor, int32_t n_tasks, int32_t n_trees, int32_t child_depth,
                      int32_t max_depth, int32_t *next_id, int32_t *lid_out, void *tasks_next,
                      int32_t *node_next, int32_t *lists, int32_t list_cap, int32_t *stats,
-                     void *scratch, void *stream);
+                     void *scratch, const int32_t *slot_cur, int32_t *par_slot_next,
+                     void *stream);
 /* gk_rf_partition over a level's three search lists (searched tasks that stayed
  * leaves are skipped); cursor: 2 * n_tasks int32, zeroed here */
 int gk_rf_partition_lists(const uint8_t *Xb, const uint32_t *counts, int64_t n_rows,

@@ -835,16 +835,59 @@ __global__ void __launch_bounds__(kMedThreads, GK_MED_MINB) k5_split_medium(
     reduce_best(H, mine, out + ti);
 }
 
-// big tasks: CTA = (task, row chunk, feature chunk) -> global histograms
+// Sibling subtraction for big tasks: the two children of a big parent that
+// are both big -- the smaller builds its histogram, the larger takes the
+// parent's (kept from the previous level) minus the smaller's (exact integer
+// sums).  par_slot[task] = the parent's slot in the previous level's
+// histogram workspace (-1: none), slot_cur[task] = the task's slot in this
+// level's (-1: not big).  Children are adjacent (2 e, 2 e + 1: sibling = task ^ 1).
+__device__ __forceinline__ bool derives(const RfTask *__restrict__ tasks,
+                                        const int32_t *__restrict__ par_slot,
+                                        const int32_t *__restrict__ slot_cur, int ti) {
+    if (!par_slot || par_slot[ti] < 0) return false;
+    const int tj = ti ^ 1;
+    if (slot_cur[tj] < 0) return false;
+    const int mi = tasks[ti].end - tasks[ti].begin, mj = tasks[tj].end - tasks[tj].begin;
+    return mi > mj || (mi == mj && (ti & 1));
+}
+
+// the big list's slots (histogram workspace index) by task
+__global__ void k5_big_slots(const int32_t *__restrict__ task_ids, int n_big,
+                             int32_t *__restrict__ slot_cur) {
+    const int bi = blockIdx.x * blockDim.x + threadIdx.x;
+    if (bi < n_big) slot_cur[task_ids[bi]] = bi;
+}
+
+// derived histograms: parent - sibling, per (task, 256-bin feature row)
+__global__ void k5_hist_derive(const RfTask *__restrict__ tasks, const int32_t *__restrict__ task_ids,
+                               const int32_t *__restrict__ par_slot,
+                               const int32_t *__restrict__ slot_cur, int F,
+                               const uint64_t *__restrict__ prev, uint64_t *__restrict__ cur) {
+    const int bi = blockIdx.y;
+    const int ti = task_ids[bi];
+    if (!derives(tasks, par_slot, slot_cur, ti)) return;
+    const size_t row = (size_t)F * kBins * 2;  // interleaved {weight, sum} per bin
+    const uint64_t *p = prev + (size_t)par_slot[ti] * row;
+    const uint64_t *s = cur + (size_t)slot_cur[ti ^ 1] * row;
+    uint64_t *d = cur + (size_t)bi * row;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < row;
+         i += (size_t)gridDim.x * blockDim.x)
+        d[i] = p[i] - s[i];
+}
+
+// big tasks: CTA = (task, row chunk, feature chunk) -> global histograms,
+// interleaved {weight, fixed-point sum} per bin
 __global__ void __launch_bounds__(256) k5_hist_big(RfTrainData D, const RfTask *__restrict__ tasks,
                                                    const int32_t *__restrict__ task_ids,
                                                    const uint8_t *__restrict__ rows0,
                                                    const uint8_t *__restrict__ rows1,
-                                                   uint64_t *__restrict__ gcw,
-                                                   int64_t *__restrict__ gs) {
+                                                   const int32_t *__restrict__ par_slot,
+                                                   const int32_t *__restrict__ slot_cur,
+                                                   uint64_t *__restrict__ gh) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     HistSmem &H = *reinterpret_cast<HistSmem *>(smem_raw);
     const int bi = blockIdx.z;           // index among big tasks
+    if (derives(tasks, par_slot, slot_cur, task_ids[bi])) return;  // k5_hist_derive fills it
     const RfTask T = tasks[task_ids[bi]];
     const uint8_t *rows = T.parity ? rows1 : rows0;
     const int fc = blockIdx.y;
@@ -856,22 +899,20 @@ __global__ void __launch_bounds__(256) k5_hist_big(RfTrainData D, const RfTask *
     accumulate<GK_ACC_BIG>(H, D, rows, p0, p1, fc);
     __syncthreads();
     const int f0 = fc * kFC, nf = min(kFC, D.F - f0);
-    uint64_t *dcw = gcw + ((size_t)bi * D.F + f0) * kBins;
-    int64_t *ds = gs + ((size_t)bi * D.F + f0) * kBins;
+    uint64_t *dh = gh + ((size_t)bi * D.F + f0) * kBins * 2;
     for (int i = threadIdx.x; i < nf * kBins; i += blockDim.x) {
         const Bins3 hb = H.feat(i / kBins);
         const int b = i % kBins;
         const uint32_t c = hb.wgt[b];
         if (c) {
-            atomicAdd((unsigned long long *)(dcw + i), (unsigned long long)c);
-            atomicAdd((unsigned long long *)(ds + i), (unsigned long long)hb.sum(b));
+            atomicAdd((unsigned long long *)(dh + 2 * i), (unsigned long long)c);
+            atomicAdd((unsigned long long *)(dh + 2 * i + 1), (unsigned long long)hb.sum(b));
         }
     }
 }
 
 __global__ void __launch_bounds__(256) k5_eval_big(RfTrainData D, const int32_t *__restrict__ task_ids,
-                                                   const uint64_t *__restrict__ gcw,
-                                                   const int64_t *__restrict__ gs,
+                                                   const uint64_t *__restrict__ gh,
                                                    RfSplit *__restrict__ out) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     HistSmem &H = *reinterpret_cast<HistSmem *>(smem_raw);
@@ -880,11 +921,10 @@ __global__ void __launch_bounds__(256) k5_eval_big(RfTrainData D, const int32_t 
     const int n_fc = (D.F + kFC - 1) / kFC;
     for (int fc = 0; fc < n_fc; fc++) {
         const int f0 = fc * kFC, nf = min(kFC, D.F - f0);
-        const uint64_t *scw = gcw + ((size_t)bi * D.F + f0) * kBins;
-        const int64_t *ss = gs + ((size_t)bi * D.F + f0) * kBins;
+        const uint64_t *sh = gh + ((size_t)bi * D.F + f0) * kBins * 2;
         for (int i = threadIdx.x; i < kFC * kBins; i += blockDim.x)
-            H.feat(i / kBins).set(i % kBins, i < nf * kBins ? scw[i] : 0,
-                                  i < nf * kBins ? ss[i] : 0);
+            H.feat(i / kBins).set(i % kBins, i < nf * kBins ? sh[2 * i] : 0,
+                                  i < nf * kBins ? (int64_t)sh[2 * i + 1] : 0);
         __syncthreads();
         if (fc == 0) parent_proxy(H);
         eval_chunk(H, D.F, fc, mine);
@@ -1468,7 +1508,8 @@ __global__ void __launch_bounds__(kLvlThreads) k5_level_emit(
     const int32_t *__restrict__ lid_base, const int32_t *__restrict__ cursor, int child_depth,
     int max_depth, int32_t *__restrict__ lid_out, RfTask *__restrict__ tasks_next,
     int32_t *__restrict__ node_next, int32_t *__restrict__ lists, int cap,
-    int32_t *__restrict__ stats) {
+    int32_t *__restrict__ stats, const int32_t *__restrict__ slot_cur,
+    int32_t *__restrict__ par_slot_next) {
     __shared__ int32_t wsum[kLvlThreads / 32];
     const int i = blockIdx.x * kLvlThreads + threadIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1495,6 +1536,11 @@ __global__ void __launch_bounds__(kLvlThreads) k5_level_emit(
         tasks_next[2 * excl + 1] = RfTask{T.tree, mid, T.end, 1 - T.parity};
         node_next[2 * excl] = lid;
         node_next[2 * excl + 1] = lid + 1;
+        if (par_slot_next) {  // the children's parent histogram (sibling subtraction)
+            const int32_t ps = slot_cur ? slot_cur[i] : -1;
+            par_slot_next[2 * excl] = ps;
+            par_slot_next[2 * excl + 1] = ps;
+        }
         sz_l = n_left;
         sz_r = T.end - mid;
         const bool deep_ok = child_depth < max_depth;
@@ -1701,7 +1747,8 @@ int gk_rf_split_level(const uint8_t *Xb, const int64_t *yfp, const double *y,
                       const void *tasks, const int32_t *small_ids, int32_t n_small,
                       const int32_t *med_ids, int32_t n_med, const int32_t *big_ids,
                       int32_t n_big, int32_t big_max_chunks, void *recs0, void *recs1,
-                      void *hist_ws, void *split_out, void *stream) {
+                      void *hist_ws, void *split_out, const void *prev_hist_ws,
+                      const int32_t *par_slot, int32_t *slot_cur, int32_t n_tasks, void *stream) {
     const cudaStream_t st = (cudaStream_t)stream;
     gk::RfTrainData D{Xb, yfp, y, counts, n_rows, n_feat, gk::rec_stride(n_feat)};
     uint8_t *rows0 = (uint8_t *)recs0, *rows1 = (uint8_t *)recs1;
@@ -1749,15 +1796,23 @@ int gk_rf_split_level(const uint8_t *Xb, const int64_t *yfp, const double *y,
                                                                        out);
         gk::k5_split_medium<<<n_med, gk::kMedThreads, smem, st>>>(D, T, med_ids, rows0, rows1, out);
     }
+    // this level's big slots by task (-1: not big), for the sibling
+    // subtraction and the next level's parent slots
+    if (slot_cur && n_tasks > 0) cudaMemsetAsync(slot_cur, 0xFF, sizeof(int32_t) * (size_t)n_tasks, st);
     if (n_big > 0) {
-        uint64_t *gcw = (uint64_t *)hist_ws;
-        int64_t *gs = (int64_t *)(gcw + (size_t)n_big * n_feat * gk::kBins);
+        uint64_t *gh = (uint64_t *)hist_ws;
+        const int32_t *ps = (prev_hist_ws && slot_cur) ? par_slot : nullptr;
+        if (slot_cur)
+            gk::k5_big_slots<<<(n_big + 255) / 256, 256, 0, st>>>(big_ids, n_big, slot_cur);
         cudaMemsetAsync(hist_ws, 0, 2 * sizeof(uint64_t) * (size_t)n_big * n_feat * gk::kBins, st);
         // the host sizes big_max_chunks in kMedRows units; CTAs take kBigRows
         dim3 grid(big_max_chunks * (gk::kMedRows / gk::kBigRows), (n_feat + gk::kFC - 1) / gk::kFC,
                   n_big);
-        gk::k5_hist_big<<<grid, 256, smem, st>>>(D, T, big_ids, rows0, rows1, gcw, gs);
-        gk::k5_eval_big<<<n_big, 256, smem, st>>>(D, big_ids, gcw, gs, out);
+        gk::k5_hist_big<<<grid, 256, smem, st>>>(D, T, big_ids, rows0, rows1, ps, slot_cur, gh);
+        if (ps)
+            gk::k5_hist_derive<<<dim3(8, n_big), 256, 0, st>>>(T, big_ids, ps, slot_cur, n_feat,
+                                                               (const uint64_t *)prev_hist_ws, gh);
+        gk::k5_eval_big<<<n_big, 256, smem, st>>>(D, big_ids, gh, out);
     }
     return gk_check_launch("k5_split_level");
 }
@@ -1800,7 +1855,8 @@ int gk_rf_next_level(const void *tasks, const int32_t *node, const void *split,
                      const int32_t *cursor, int32_t n_tasks, int32_t n_trees, int32_t child_depth,
                      int32_t max_depth, int32_t *next_id, int32_t *lid_out, void *tasks_next,
                      int32_t *node_next, int32_t *lists, int32_t list_cap, int32_t *stats,
-                     void *scratch, void *stream) {
+                     void *scratch, const int32_t *slot_cur, int32_t *par_slot_next,
+                     void *stream) {
     if (n_tasks < 0 || n_trees < 1 || list_cap < 2 * (int64_t)n_tasks) {
         gk_set_error("gk_rf_next_level: bad sizes (n_tasks %d, n_trees %d, list_cap %d)", n_tasks,
                      n_trees, list_cap);
@@ -1821,7 +1877,7 @@ int gk_rf_next_level(const void *tasks, const int32_t *node, const void *split,
     gk::k5_level_emit<<<nb, gk::kLvlThreads, 0, st>>>(T, node, S, n_tasks, block_cnt, lid_base,
                                                        cursor, child_depth, max_depth, lid_out,
                                                        (gk::RfTask *)tasks_next, node_next, lists,
-                                                       list_cap, stats);
+                                                       list_cap, stats, slot_cur, par_slot_next);
     return gk_check_launch("k5_next_level");
 }
 

@@ -52,7 +52,7 @@ def _lib():
         L.gk_rf_record_bytes.restype = C.c_size_t
         L.gk_rf_bin.argtypes = [vp, i64, i32, i64, vp, vp, vp, vp, vp, vp]
         L.gk_rf_split_level.argtypes = [vp, vp, vp, vp, i64, i32, vp, vp, i32, vp, i32, vp, i32,
-                                        i32, vp, vp, vp, vp, vp]
+                                        i32, vp, vp, vp, vp, vp, vp, vp, i32, vp]
         L.gk_rf_hist_bytes.argtypes = [i32, i32]
         L.gk_rf_hist_bytes.restype = C.c_size_t
         L.gk_rf_partition.argtypes = [vp, vp, vp, vp, i64, i32, vp, i32, vp, vp, i32, i32, vp,
@@ -64,7 +64,7 @@ def _lib():
         L.gk_rf_level_scratch_bytes.argtypes = [i32, i32]
         L.gk_rf_level_scratch_bytes.restype = C.c_size_t
         L.gk_rf_next_level.argtypes = [vp, vp, vp, vp, i32, i32, i32, i32, vp, vp, vp, vp, vp,
-                                       i32, vp, vp, vp]
+                                       i32, vp, vp, vp, vp, vp]
         L.gk_rf_partition_lists.argtypes = [vp, vp, i64, i32, vp, i32, vp, vp, i32, vp, i32, i32,
                                             vp, i32, i32, vp, vp, vp, vp]
         L._rf_bound = True
@@ -485,10 +485,14 @@ class _LevelGrower:
         lists_d = torch.from_numpy(lists).to(dev)
         next_id_d = torch.ones(TB, dtype=i32, device=dev)
         stats_d = torch.empty(8, dtype=i32, device=dev)
-        # one histogram workspace for the batch: a big task has > MEDIUM rows
+        # two histogram workspaces for the batch (a big task has > MEDIUM rows),
+        # alternating by level: the previous level's big histograms stay for
+        # the sibling subtraction (GK_RF_SUBTRACT=0: every big task builds)
         n_big_cap = int(np.sum(m)) // (MEDIUM + 1) + 1
-        hist = torch.empty(max(int(L.gk_rf_hist_bytes(n_big_cap, F)), 8), dtype=torch.uint8,
-                           device=dev)
+        hists = [torch.empty(max(int(L.gk_rf_hist_bytes(n_big_cap, F)), 8), dtype=torch.uint8,
+                             device=dev) for _ in range(2)]
+        subtract = os.environ.get("GK_RF_SUBTRACT", "1") != "0"
+        par_slot = None
         cursor = torch.empty(0, dtype=i32, device=dev)
         records = []  # per level: (tasks, node, split, lid, n_tasks, n_split), device tensors
         depth = 0
@@ -503,6 +507,10 @@ class _LevelGrower:
             if n_b > n_big_cap:
                 raise RuntimeError("forest: big-task workspace undersized")
             big_chunks = -(-int(stats[5]) // MEDIUM) if n_b else 0
+            hist, prev_hist = hists[depth % 2], hists[(depth + 1) % 2]
+            sub_args = (_ptr(prev_hist) if subtract and par_slot is not None else None,
+                        _ptr(par_slot) if par_slot is not None else None)
+            slot_cur = torch.empty(max(nt, 1), dtype=i32, device=dev)
             if _LEVEL_LOG is not None:   # tuning aid: per-level, per-class device times
                 ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
                 ev[0].record()
@@ -513,13 +521,14 @@ class _LevelGrower:
                     _check(L.gk_rf_split_level(
                         _ptr(D["Xb"]), _ptr(D["yfp"]), _ptr(D["y"]), _ptr(counts), n, F,
                         _ptr(tasks_d), *args_, big_chunks, _ptr(rows0), _ptr(rows1), _ptr(hist),
-                        _ptr(split_d), st))
+                        _ptr(split_d), *sub_args, _ptr(slot_cur), nt, st))
                     ev[c + 1].record()
             else:
                 _check(L.gk_rf_split_level(
                     _ptr(D["Xb"]), _ptr(D["yfp"]), _ptr(D["y"]), _ptr(counts), n, F,
                     _ptr(tasks_d), lp, n_s, lp + 4 * cap, n_m, lp + 8 * cap, n_b, big_chunks,
-                    _ptr(rows0), _ptr(rows1), _ptr(hist), _ptr(split_d), st))
+                    _ptr(rows0), _ptr(rows1), _ptr(hist), _ptr(split_d), *sub_args,
+                    _ptr(slot_cur), nt, st))
             if len(cursor) < 2 * nt:
                 cursor = torch.empty(2 * nt, dtype=i32, device=dev)
             _check(L.gk_rf_partition_lists(
@@ -532,11 +541,12 @@ class _LevelGrower:
             lists_n = torch.empty(max(6 * nt, 3), dtype=i32, device=dev)
             scratch = torch.empty(int(L.gk_rf_level_scratch_bytes(nt, TB)), dtype=torch.uint8,
                                   device=dev)
+            par_next = torch.empty(max(2 * nt, 1), dtype=i32, device=dev)
             _check(L.gk_rf_next_level(
                 _ptr(tasks_d), _ptr(node_d), _ptr(split_d), _ptr(cursor), nt, TB, depth + 1,
                 max_depth,
                 _ptr(next_id_d), _ptr(lid_d), _ptr(tasks_n), _ptr(node_n), _ptr(lists_n),
-                2 * nt, _ptr(stats_d), _ptr(scratch), st))
+                2 * nt, _ptr(stats_d), _ptr(scratch), _ptr(slot_cur), _ptr(par_next), st))
             if _LEVEL_LOG is not None:
                 ev[4].record()
             prev = stats
@@ -555,6 +565,7 @@ class _LevelGrower:
             if stats[0] == 0:
                 break
             tasks_d, node_d, lists_d, cap = tasks_n, node_n, lists_n, 2 * nt
+            par_slot = par_next
 
         rd = _Read(next_id_d)
         yield rd
@@ -687,7 +698,8 @@ class _LevelGrower:
             _check(L.gk_rf_split_level(
                 _ptr(D["Xb"]), _ptr(D["yfp"]), _ptr(D["y"]), _ptr(counts), n, F, _ptr(tasks_d),
                 _ptr(ids_d["s"]), len(ids_small), _ptr(ids_d["m"]), len(ids_med), _ptr(ids_d["b"]),
-                n_big, big_chunks, _ptr(rows0), _ptr(rows1), _ptr(hist), _ptr(split_d), st))
+                n_big, big_chunks, _ptr(rows0), _ptr(rows1), _ptr(hist), _ptr(split_d), None, None,
+                None, 0, st))
             sp = split_d.cpu().numpy().view(SPLIT_DT)
             s = sp["feat"] >= 0
             # leaves of this level stay where they are
