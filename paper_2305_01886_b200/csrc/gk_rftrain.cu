@@ -1043,6 +1043,10 @@ __device__ __forceinline__ void split_sorted(const RfTrainData &D, int m, int la
     warp_finish<1>(D, best, parent, node, out_node, m, lane, out);
 }
 
+// one kernel per network size (<= 16 rows, 17..32 rows): each keeps one sort
+// network in the instruction cache (ncu, level 15: the kernel holding both
+// spent 25 % of its stall samples on instruction fetch)
+template <int N>
 __global__ void __launch_bounds__(kSmallThreads, GK_SMALL_MINB) k5_split_sorted(
     RfTrainData D, const RfTask *__restrict__ tasks, const int32_t *__restrict__ task_ids,
     int n_ids, uint8_t *__restrict__ rows0, uint8_t *__restrict__ rows1,
@@ -1054,7 +1058,7 @@ __global__ void __launch_bounds__(kSmallThreads, GK_SMALL_MINB) k5_split_sorted(
         const int ti = task_ids[wi];
         const RfTask T = tasks[ti];
         const int m = T.end - T.begin;
-        if (m > 32) continue;  // warp-uniform: k5_split_rank's node
+        if (m > N || m <= (N == 32 ? kTiny : 0)) continue;  // warp-uniform: another kernel's node
         const uint8_t *node = (T.parity ? rows1 : rows0) + (size_t)T.begin * D.rs;
         uint8_t *out_node = (T.parity ? rows0 : rows1) + (size_t)T.begin * D.rs;
         uint32_t wv = 0u;
@@ -1064,10 +1068,7 @@ __global__ void __launch_bounds__(kSmallThreads, GK_SMALL_MINB) k5_split_sorted(
             wv = h.y;
             sv = (int64_t)(((uint64_t)h.w << 32) | h.z);
         }
-        if (m <= kTiny)
-            split_sorted<16>(D, m, lane, Z[wib], wv, sv, node, out_node, out + ti);
-        else
-            split_sorted<32>(D, m, lane, Z[wib], wv, sv, node, out_node, out + ti);
+        split_sorted<N>(D, m, lane, Z[wib], wv, sv, node, out_node, out + ti);
         __syncwarp();  // Z reuse by the warp's next node
     }
 }
@@ -1781,8 +1782,10 @@ int gk_rf_split_level(const uint8_t *Xb, const int64_t *yfp, const double *y,
         const int64_t want = ((int64_t)n_small + wpb - 1) / wpb;
         const int64_t cap = (int64_t)n_sm * GK_SMALL_MINB * 4;
         const unsigned blocks = (unsigned)(want < cap ? want : cap);
-        gk::k5_split_sorted<<<blocks, gk::kSmallThreads, 0, st>>>(D, T, small_ids, n_small, rows0,
-                                                                   rows1, out);
+        gk::k5_split_sorted<16><<<blocks, gk::kSmallThreads, 0, st>>>(D, T, small_ids, n_small,
+                                                                       rows0, rows1, out);
+        gk::k5_split_sorted<32><<<blocks, gk::kSmallThreads, 0, st>>>(D, T, small_ids, n_small,
+                                                                       rows0, rows1, out);
         if (GK_SMALL_RADIX)
             gk::k5_split_radix<<<blocks, gk::kSmallThreads, 0, st>>>(D, T, small_ids, n_small,
                                                                       rows0, rows1, out);
