@@ -307,6 +307,30 @@ def test_sharded_fits_merge_to_the_unsharded_forest():
 
 
 @pytest.mark.gpu
+def test_sibling_subtraction_grows_the_same_trees(monkeypatch):
+    """Big tasks (> 32768 rows) take the parent's histogram minus the smaller
+    sibling's (exact integer sums): the forest equals the one that builds
+    every big histogram (GK_RF_SUBTRACT=0), array for array -- and the
+    gradient-boosted model, whose levels are all big at this size."""
+    from paper_2305_01886_b200.boosting import GradientBoostingRegressor
+    from paper_2305_01886_b200.forest import RandomForestRegressor
+
+    rng = np.random.default_rng(9)
+    X = rng.random((300_000, 16))
+    X[:, 12:] = np.floor(X[:, 12:] * 5)
+    y = 3 * X[:, 0] + np.sin(5 * X[:, 1]) + X[:, 12] + rng.normal(0, 0.2, 300_000)
+    fits = {}
+    for sub in ("1", "0"):
+        monkeypatch.setenv("GK_RF_SUBTRACT", sub)
+        rf = RandomForestRegressor(4, max_depth=10, random_state=2).fit(X, y)
+        gb = GradientBoostingRegressor(3, max_depth=4, random_state=0).fit(X, y)
+        fits[sub] = [e.tree_ for e in rf.estimators_] + [e[0].tree_ for e in gb.estimators_]
+    for a, b in zip(fits["1"], fits["0"]):
+        for u, v in zip(_tree_arrays(a), _tree_arrays(b)):
+            assert np.array_equal(u, v)
+
+
+@pytest.mark.gpu
 def test_device_resident_trees_predict_and_read_back(monkeypatch):
     """Fitted trees stay in HBM (TreeBatch): predict() builds the walk nodes
     on the device; reading a tree_ array copies the batch to the host through
