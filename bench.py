@@ -551,6 +551,11 @@ def main():
     ap.add_argument("--rf-cpu-trees", type=int, default=0, help="sklearn trees (default: cores)")
     ap.add_argument("--gbt-stages", type=int, default=100)
     args = ap.parse_args()
+    wd = os.environ.get("GK_BENCH_WATCHDOG")  # debugging aid: tracebacks of a stuck rank
+    if wd:
+        import faulthandler
+
+        faulthandler.dump_traceback_later(float(wd), repeat=True)
     args.warmup = max(args.warmup, 3)
 
     rank = int(os.environ.get("RANK", 0))
