@@ -1003,6 +1003,13 @@ def rf_fit_measure(args, rank, world, threads):
                         "accounting": "sum over internal nodes of n_node_samples x 73 B "
                                       "(64 B bins + 4 B row id + 4 B target + 1 B count)",
                         "traffic": None}}
+    try:  # DRAM bytes of the fit from the committed ncu launch list, per tree
+        rec = json.loads(TRAFFIC.read_text())["c3"]["k5_fit"]
+        out["roofline"]["traffic"] = rec["read_plus_write"] / rec["units"] * args.rf_trees
+        out["roofline"]["traffic_source"] = (rec["capture"] + f"; scaled from {rec['units']} "
+                                             f"to {args.rf_trees} trees")
+    except Exception:
+        pass
     del m
     if args.rf_trees != 500:
         out["fit_s_500_trees_extrapolated"] = out["fit_s"] * 500 / args.rf_trees
