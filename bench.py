@@ -1017,6 +1017,11 @@ def rf_fit_measure(args, rank, world, threads):
     # fit + predict (R^2 / RMSE / MAE, + MAPE), then the final fit on all rows
     if not args.no_train:
         names = tuple(f"f{i:02d}" for i in range(64))
+        # the reference's training module imports scikit-learn at import time;
+        # ours imports it inside train(): load it before the clock starts
+        import sklearn.metrics  # noqa: F401
+        import sklearn.model_selection  # noqa: F401
+        import sklearn.preprocessing  # noqa: F401
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()

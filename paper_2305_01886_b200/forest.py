@@ -175,12 +175,22 @@ def bin_edges(Xf: np.ndarray, n_bins: int = N_BINS, sample: int = 65_536, device
     `device` when given (sorting is exact: the same sorted columns; it was
     ~1/3 of a 50-stage boosting fit on the host)."""
     n, F = Xf.shape
-    if n > sample:
+    if is_device_tensor(Xf):   # the same rows, sorted on the tensor's device
+        import torch
+
+        S = Xf
+        if n > sample:
+            idx = np.sort(np.random.default_rng(0).choice(n, sample, replace=False))
+            S = Xf.index_select(0, torch.from_numpy(idx).to(Xf.device))
+        S = torch.sort(S.to(torch.float32), dim=0).values.cpu().numpy()
+    elif n > sample:
         idx = np.random.default_rng(0).choice(n, sample, replace=False)
         S = Xf[np.sort(idx)]
     else:
         S = Xf
-    if device is not None:
+    if is_device_tensor(Xf):
+        pass
+    elif device is not None:
         import torch
 
         S = torch.sort(torch.from_numpy(np.ascontiguousarray(S, dtype=np.float32)).to(device),
@@ -207,6 +217,12 @@ def bin_edges(Xf: np.ndarray, n_bins: int = N_BINS, sample: int = 65_536, device
         edges[f, : len(e)] = e
         n_edges[f] = len(e)
     return edges, n_edges
+
+
+def is_device_tensor(a) -> bool:
+    """A torch tensor (the trainer passes its folds as device tensors: no host
+    copies of the scaled folds, no re-upload)."""
+    return type(a).__module__.split(".")[0] == "torch"
 
 
 def check_n_bins(n_bins) -> int:
@@ -394,7 +410,8 @@ class _LevelGrower:
         L = _lib()
         dev = device()
         edges, n_edges = bin_edges(X, self.n_bins, device=dev)   # float32 sample inside
-        Xd = _dev(X, dev)               # k5_bin casts to float32 (sklearn)
+        # k5_bin casts to float32 (sklearn)
+        Xd = X.contiguous() if is_device_tensor(X) else _dev(X, dev)
         Xb = torch.empty(n * F, dtype=torch.uint8, device=dev)
         bmin = torch.empty(F * N_BINS, dtype=torch.int32, device=dev)
         bmax = torch.empty(F * N_BINS, dtype=torch.int32, device=dev)
@@ -822,6 +839,8 @@ class _LevelGrower:
 class RandomForestRegressor(_LevelGrower):
     """GPU-trained random forest with scikit-learn's constructor/fit/predict."""
 
+    _device_input = True   # fit / predict also take device tensors (trainer.train)
+
     def __init__(self, n_estimators: int = 100, *, max_depth: int | None = None,
                  random_state=None, n_bins: int = N_BINS, trees_per_batch: int | None = None,
                  shard: tuple[int, int] | None = None, concurrent: bool = True,
@@ -844,28 +863,54 @@ class RandomForestRegressor(_LevelGrower):
 
         if sample_weight is not None:
             raise NotImplementedError("sample_weight is not supported (training.py never passes it)")
-        X = np.ascontiguousarray(X, dtype=np.float64)
-        y = np.ascontiguousarray(y, dtype=np.float64).reshape(-1)
-        n, F = X.shape
+        on_dev = is_device_tensor(X)
+        if on_dev:   # device tensors (trainer.train's folds): the same values, no host copies
+            dev = device()
+            X = X.to(dev, torch.float64).contiguous()
+            yd = torch.as_tensor(y).to(dev, torch.float64).reshape(-1).contiguous()
+            n, F = X.shape
+        else:
+            X = np.ascontiguousarray(X, dtype=np.float64)
+            y = np.ascontiguousarray(y, dtype=np.float64).reshape(-1)
+            n, F = X.shape
         if n < 1 or F > 64 * 1024 or n >= 2 ** 31:
             raise ValueError("bad training table shape")
-        if len(y) != n:
+        if (len(yd) if on_dev else len(y)) != n:
             raise ValueError("X and y have different lengths")
-        check_finite(X, y)
+        if on_dev:
+            if not bool(torch.isfinite(X).all()):
+                raise ValueError("Input X contains NaN or infinity.")
+            if not bool(torch.isfinite(yd).all()):
+                raise ValueError("Input y contains NaN or infinity.")
+        else:
+            check_finite(X, y)
         check_n_bins(self.n_bins)
         self.n_features_in_ = F
-        Xb = self._prepare_bins(X)
         dev = device()
-        ymax = float(np.max(np.abs(y))) if n else 1.0
+        Xb = self._prepare_bins(X)
+        # fixed-point targets: rint(ldexp(v, shift)) (ldexp = an exact power-of-two
+        # product; round half to even like np.rint) on either side
+        if on_dev:
+            ymax = float(yd.abs().max())
+        else:
+            ymax = float(np.max(np.abs(y))) if n else 1.0
         shift = int(np.floor(62 - np.log2(max(ymax, 1e-300) * n + 1e-300)))
         shift = max(min(shift, 60), -60)
-        yfp = torch.from_numpy(np.rint(np.ldexp(y, shift)).astype(np.int64)).to(dev)
-        y2 = y * y
-        y2max = float(np.max(y2)) if n else 1.0
+        if on_dev:
+            yfp = torch.round(yd * (2.0 ** shift)).to(torch.int64)
+            y2d = yd * yd
+            y2max = float(y2d.max())
+        else:
+            yfp = torch.from_numpy(np.rint(np.ldexp(y, shift)).astype(np.int64)).to(dev)
+            y2 = y * y
+            y2max = float(np.max(y2)) if n else 1.0
         shift2 = int(np.floor(62 - np.log2(max(y2max, 1e-300) * n + 1e-300)))
         shift2 = max(min(shift2, 60), -60)
-        y2fp = torch.from_numpy(np.rint(np.ldexp(y2, shift2)).astype(np.int64)).to(dev)
-        yd = _dev(y, dev)
+        if on_dev:
+            y2fp = torch.round(y2d * (2.0 ** shift2)).to(torch.int64)
+        else:
+            y2fp = torch.from_numpy(np.rint(np.ldexp(y2, shift2)).astype(np.int64)).to(dev)
+            yd = _dev(y, dev)
         self._dev = dict(Xb=Xb, yfp=yfp, y2fp=y2fp, y=yd, n=n, F=F, shift=shift, shift2=shift2)
 
         seeds = tree_seeds(self.random_state, self.n_estimators)
@@ -1006,6 +1051,11 @@ class RandomForestRegressor(_LevelGrower):
 
         if getattr(self, "_flat", None) is None:
             self._flat = self.device_ensemble()
-        Xf = np.ascontiguousarray(np.asarray(X, dtype=np.float64).astype(np.float32), np.float64)
-        total, _ = rf_predict(self._flat, torch.from_numpy(Xf).to(device()))
+        if is_device_tensor(X):
+            Xd = X.to(device(), torch.float64).to(torch.float32).to(torch.float64).contiguous()
+        else:
+            Xf = np.ascontiguousarray(np.asarray(X, dtype=np.float64).astype(np.float32),
+                                      np.float64)
+            Xd = torch.from_numpy(Xf).to(device())
+        total, _ = rf_predict(self._flat, Xd)
         return total.cpu().numpy() / len(self.estimators_)

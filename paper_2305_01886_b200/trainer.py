@@ -122,6 +122,29 @@ def canonical_rows(X, y, manifest) -> tuple[np.ndarray, np.ndarray]:
     return X[order], y[order]
 
 
+def _minmax_on_device(Xd):
+    """A fitted sklearn MinMaxScaler for the device table Xd: the column minima
+    and maxima are reduced on the device (exact), and the scaler is fitted on
+    that 2-row summary -- data_min_ / data_max_ / scale_ / min_ come out of
+    sklearn's own code, identical to fitting on the rows."""
+    from sklearn.preprocessing import MinMaxScaler
+
+    summary = np.stack([Xd.amin(dim=0).cpu().numpy(), Xd.amax(dim=0).cpu().numpy()])
+    sc = MinMaxScaler().fit(summary)
+    sc.n_samples_seen_ = int(Xd.shape[0])
+    return sc
+
+
+def _scale_on_device(sc, Xd):
+    """MinMaxScaler.transform on the device: X * scale_, then + min_ (sklearn's
+    in-place `X *= scale_; X += min_`, the same two roundings)."""
+    import torch
+
+    scale = torch.from_numpy(np.asarray(sc.scale_, np.float64)).to(Xd.device)
+    shift = torch.from_numpy(np.asarray(sc.min_, np.float64)).to(Xd.device)
+    return torch.add(torch.mul(Xd, scale), shift)
+
+
 def train(dataset, family: str = "gradient_boosted", *, n_estimators: int = 500,
           learning_rate: float = 0.05, max_depth: int | None = None, seed: int = 0) -> TrainResult:
     """5-fold CV, then a final fit on all rows (reference ``training.py:94-160``).
@@ -146,14 +169,34 @@ def train(dataset, family: str = "gradient_boosted", *, n_estimators: int = 500,
     X, y = canonical_rows(Xraw, yraw, manifest)
     if np.ptp(y) == 0.0:
         raise TrainerError("degenerate target: every row has the same value")
-    _make_model(family, n_estimators, learning_rate, max_depth, seed)  # family check
+    probe = _make_model(family, n_estimators, learning_rate, max_depth, seed)  # family check
+    # models that take device tensors get every fold scaled on the device from
+    # one upload of the canonical table: the same float64 values as
+    # MinMaxScaler.transform (X * scale_ then + min_, two IEEE roundings), no
+    # host copies of the folds (they were ~40 % of a config #3 train())
+    dev_folds = getattr(probe, "_device_input", False)
+    if dev_folds:
+        import torch
+
+        from .runtime import device
+
+        Xd = torch.from_numpy(np.ascontiguousarray(X, dtype=np.float64)).to(device())
+        yd = torch.from_numpy(np.ascontiguousarray(y, dtype=np.float64)).to(device())
     folds, mapes = [], []
     holdout = np.empty(0, dtype=int)
     for tr, te in KFold(n_splits=N_FOLDS, shuffle=True, random_state=seed).split(X):
-        scaler = MinMaxScaler().fit(X[tr])
         model = _make_model(family, n_estimators, learning_rate, max_depth, seed)
-        model.fit(scaler.transform(X[tr]), y[tr])
-        pred = model.predict(scaler.transform(X[te]))
+        if dev_folds:
+            tr_d, te_d = (torch.from_numpy(i).to(Xd.device) for i in (tr, te))
+            Xtr = Xd.index_select(0, tr_d)
+            scaler = _minmax_on_device(Xtr)
+            model.fit(_scale_on_device(scaler, Xtr), yd.index_select(0, tr_d))
+            del Xtr
+            pred = model.predict(_scale_on_device(scaler, Xd.index_select(0, te_d)))
+        else:
+            scaler = MinMaxScaler().fit(X[tr])
+            model.fit(scaler.transform(X[tr]), y[tr])
+            pred = model.predict(scaler.transform(X[te]))
         folds.append(FoldMetrics(r2=float(r2_score(y[te], pred)),
                                  rmse=float(np.sqrt(mean_squared_error(y[te], pred))),
                                  mae=float(mean_absolute_error(y[te], pred))))
@@ -162,9 +205,14 @@ def train(dataset, family: str = "gradient_boosted", *, n_estimators: int = 500,
     mean = FoldMetrics(r2=float(np.mean([m.r2 for m in folds])),
                        rmse=float(np.mean([m.rmse for m in folds])),
                        mae=float(np.mean([m.mae for m in folds])))
-    final_scaler = MinMaxScaler().fit(X)
     final_model = _make_model(family, n_estimators, learning_rate, max_depth, seed)
-    final_model.fit(final_scaler.transform(X), y)
+    if dev_folds:
+        final_scaler = _minmax_on_device(Xd)
+        final_model.fit(_scale_on_device(final_scaler, Xd), yd)
+        del Xd, yd
+    else:
+        final_scaler = MinMaxScaler().fit(X)
+        final_model.fit(final_scaler.transform(X), y)
     return TrainResult(family=family, seed=seed,
                        hyperparameters={"n_estimators": n_estimators,
                                         "learning_rate": learning_rate, "max_depth": max_depth},

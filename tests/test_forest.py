@@ -331,6 +331,33 @@ def test_sibling_subtraction_grows_the_same_trees(monkeypatch):
 
 
 @pytest.mark.gpu
+def test_train_device_folds_equal_host_folds(monkeypatch):
+    """trainer.train scales each fold on the device for models that take
+    device tensors: fold metrics, the final scaler and every tree equal the
+    host path (sklearn MinMaxScaler.transform + numpy folds), bit for bit."""
+    from paper_2305_01886_b200 import trainer as T
+    from paper_2305_01886_b200.forest import RandomForestRegressor
+
+    rng = np.random.default_rng(21)
+    X = rng.random((40_000, 12)) * rng.uniform(0.5, 50, 12) - 3.0
+    X[:, 10:] = np.floor(X[:, 10:])
+    y = 20 + 5 * X[:, 0] + np.sin(X[:, 1]) + X[:, 10] + rng.normal(0, 0.5, 40_000)
+    names = tuple(f"f{i}" for i in range(12))
+    res = {}
+    for dev in (True, False):
+        monkeypatch.setattr(RandomForestRegressor, "_device_input", dev)
+        res[dev] = T.train((X, y, names), "random_forest", n_estimators=6, max_depth=10, seed=3)
+    a, b = res[True], res[False]
+    assert [m.r2 for m in a.fold_metrics] == [m.r2 for m in b.fold_metrics]
+    assert a.fold_mape_pct == b.fold_mape_pct
+    for k in ("data_min_", "data_max_", "scale_", "min_"):
+        assert np.array_equal(getattr(a.scaler, k), getattr(b.scaler, k))
+    for ea, eb in zip(a.model.estimators_, b.model.estimators_):
+        for u, v in zip(_tree_arrays(ea.tree_), _tree_arrays(eb.tree_)):
+            assert np.array_equal(u, v)
+
+
+@pytest.mark.gpu
 def test_device_resident_trees_predict_and_read_back(monkeypatch):
     """Fitted trees stay in HBM (TreeBatch): predict() builds the walk nodes
     on the device; reading a tree_ array copies the batch to the host through
