@@ -863,54 +863,49 @@ class RandomForestRegressor(_LevelGrower):
 
         if sample_weight is not None:
             raise NotImplementedError("sample_weight is not supported (training.py never passes it)")
-        on_dev = is_device_tensor(X)
-        if on_dev:   # device tensors (trainer.train's folds): the same values, no host copies
+        from .errors import DeviceError
+
+        if is_device_tensor(X):   # trainer.train's folds: no host copies at all
             dev = device()
             X = X.to(dev, torch.float64).contiguous()
             yd = torch.as_tensor(y).to(dev, torch.float64).reshape(-1).contiguous()
-            n, F = X.shape
         else:
             X = np.ascontiguousarray(X, dtype=np.float64)
             y = np.ascontiguousarray(y, dtype=np.float64).reshape(-1)
-            n, F = X.shape
+            if X.ndim != 2 or len(y) != len(X):
+                raise ValueError("X and y have different lengths")
+            try:
+                dev = device()
+            except DeviceError:
+                check_finite(X, y)   # sklearn's input errors first, as on a GPU box
+                raise
+            # one upload; the input checks and the fixed-point targets run on
+            # the device (np.isfinite over config #3's 64M values cost ~0.1 s)
+            X = torch.from_numpy(X).to(dev)
+            yd = torch.from_numpy(y).to(dev)
+        n, F = X.shape
         if n < 1 or F > 64 * 1024 or n >= 2 ** 31:
             raise ValueError("bad training table shape")
-        if (len(yd) if on_dev else len(y)) != n:
+        if len(yd) != n:
             raise ValueError("X and y have different lengths")
-        if on_dev:
-            if not bool(torch.isfinite(X).all()):
-                raise ValueError("Input X contains NaN or infinity.")
-            if not bool(torch.isfinite(yd).all()):
-                raise ValueError("Input y contains NaN or infinity.")
-        else:
-            check_finite(X, y)
+        if not bool(torch.isfinite(X).all()):
+            raise ValueError("Input X contains NaN or infinity.")
+        if not bool(torch.isfinite(yd).all()):
+            raise ValueError("Input y contains NaN or infinity.")
         check_n_bins(self.n_bins)
         self.n_features_in_ = F
-        dev = device()
         Xb = self._prepare_bins(X)
-        # fixed-point targets: rint(ldexp(v, shift)) (ldexp = an exact power-of-two
-        # product; round half to even like np.rint) on either side
-        if on_dev:
-            ymax = float(yd.abs().max())
-        else:
-            ymax = float(np.max(np.abs(y))) if n else 1.0
+        # fixed-point targets: rint(ldexp(v, shift)) -- ldexp is an exact
+        # power-of-two product, torch.round rounds half to even like np.rint
+        ymax = float(yd.abs().max())
         shift = int(np.floor(62 - np.log2(max(ymax, 1e-300) * n + 1e-300)))
         shift = max(min(shift, 60), -60)
-        if on_dev:
-            yfp = torch.round(yd * (2.0 ** shift)).to(torch.int64)
-            y2d = yd * yd
-            y2max = float(y2d.max())
-        else:
-            yfp = torch.from_numpy(np.rint(np.ldexp(y, shift)).astype(np.int64)).to(dev)
-            y2 = y * y
-            y2max = float(np.max(y2)) if n else 1.0
+        yfp = torch.round(yd * (2.0 ** shift)).to(torch.int64)
+        y2d = yd * yd
+        y2max = float(y2d.max())
         shift2 = int(np.floor(62 - np.log2(max(y2max, 1e-300) * n + 1e-300)))
         shift2 = max(min(shift2, 60), -60)
-        if on_dev:
-            y2fp = torch.round(y2d * (2.0 ** shift2)).to(torch.int64)
-        else:
-            y2fp = torch.from_numpy(np.rint(np.ldexp(y2, shift2)).astype(np.int64)).to(dev)
-            yd = _dev(y, dev)
+        y2fp = torch.round(y2d * (2.0 ** shift2)).to(torch.int64)
         self._dev = dict(Xb=Xb, yfp=yfp, y2fp=y2fp, y=yd, n=n, F=F, shift=shift, shift2=shift2)
 
         seeds = tree_seeds(self.random_state, self.n_estimators)
