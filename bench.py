@@ -982,12 +982,14 @@ def rf_fit_measure(args, rank, world, threads):
         return m, float(t[0])
 
     m, dt = timed_fit()
-    m2, dt2 = timed_fit()   # a second fit: wall-time variance
-    same = all(np.array_equal(a.tree_.threshold, b.tree_.threshold)
-               for a, b in zip(m.estimators_[:8], m2.estimators_[:8]))
-    del m2
+    # the second fit runs under the same conditions as the first (the warm-up
+    # forest was gone too): keep 8 trees' thresholds on the host, free the rest
+    thr8 = [e.tree_.threshold.copy() for e in m.estimators_[:8]]
     nodes = float(np.mean([e.tree_.node_count for e in m.estimators_]))
     hb = hist_pass_bytes(m)
+    del m
+    m, dt2 = timed_fit()   # a second fit: wall-time variance
+    same = all(np.array_equal(t, e.tree_.threshold) for t, e in zip(thr8, m.estimators_[:8]))
     peak, peak_kind = hbm_peak()
     out = {"workload": f"BASELINE configs[2]: {args.rf_rows} x 64 table (workloads.config3_table), "
                        f"depth 16, {args.rf_trees} trees (tree-sharded over {world} GPU)",
