@@ -27,7 +27,8 @@ import ctypes as C
 import numpy as np
 
 from .ensemble import NODE_DT, FlatEnsemble
-from .forest import TreeEstimator, _check, _LevelGrower, _lib, check_finite, check_n_bins
+from .forest import (TreeEstimator, _check, _LevelGrower, _lib, check_finite, check_n_bins,
+                     is_device_tensor)
 
 
 def _shifts(bound: float, n: int) -> tuple[int, int]:
@@ -53,6 +54,8 @@ class _Init:
 class GradientBoostingRegressor(_LevelGrower):
     """GPU-trained gradient boosting (squared error) with sklearn's face."""
 
+    _device_input = True   # fit / predict also take device tensors (trainer.train)
+
     def __init__(self, n_estimators: int = 100, *, learning_rate: float = 0.1,
                  max_depth: int | None = 3, random_state=None, n_bins: int = 256):
         self.n_estimators = n_estimators
@@ -71,14 +74,26 @@ class GradientBoostingRegressor(_LevelGrower):
             raise NotImplementedError("sample_weight is not supported (training.py never passes it)")
         if not self.learning_rate > 0.0:
             raise ValueError("learning_rate must be > 0")
-        X = np.ascontiguousarray(X, dtype=np.float64)
-        y = np.ascontiguousarray(y, dtype=np.float64).reshape(-1)
+        on_dev = is_device_tensor(X)
+        if on_dev:   # trainer.train's device folds: X stays on the device
+            X = X.to(device(), torch.float64).contiguous()
+            y = (y.detach().to("cpu", torch.float64).numpy() if is_device_tensor(y)
+                 else np.asarray(y, dtype=np.float64))
+            y = np.ascontiguousarray(y).reshape(-1)   # the init mean is numpy's (sklearn's)
+        else:
+            X = np.ascontiguousarray(X, dtype=np.float64)
+            y = np.ascontiguousarray(y, dtype=np.float64).reshape(-1)
         n, F = X.shape
         if n < 1 or F > 64 * 1024 or n >= 2 ** 31:
             raise ValueError("bad training table shape")
         if len(y) != n:
             raise ValueError("X and y have different lengths")
-        check_finite(X, y)
+        if on_dev:
+            if not bool(torch.isfinite(X).all()):
+                raise ValueError("Input X contains NaN or infinity.")
+            check_finite(np.zeros((1, 1)), y)
+        else:
+            check_finite(X, y)
         check_n_bins(self.n_bins)
         self.n_features_in_ = F
         L = _lib()
@@ -169,8 +184,13 @@ class GradientBoostingRegressor(_LevelGrower):
 
         if getattr(self, "_flat", None) is None:
             self._flat = DeviceEnsemble.upload(self.flat())
-        Xf = np.ascontiguousarray(np.asarray(X, dtype=np.float64).astype(np.float32), np.float64)
-        total, _ = rf_predict(self._flat, torch.from_numpy(Xf).to(device()))
+        if is_device_tensor(X):
+            Xd = X.to(device(), torch.float64).to(torch.float32).to(torch.float64).contiguous()
+        else:
+            Xf = np.ascontiguousarray(np.asarray(X, dtype=np.float64).astype(np.float32),
+                                      np.float64)
+            Xd = torch.from_numpy(Xf).to(device())
+        total, _ = rf_predict(self._flat, Xd)
         return total.cpu().numpy()
 
 

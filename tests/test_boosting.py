@@ -102,3 +102,26 @@ def test_gbt_follows_sklearn_when_bins_are_exact():
     assert same >= 30, same   # near-ties in the proxy may order a few splits differently
     p_ours, p_sk = ours.predict(X), sk.predict(X)
     assert np.max(np.abs(p_ours - p_sk)) < 0.05 * np.std(y)
+
+
+@pytest.mark.gpu
+def test_train_gbt_device_folds_equal_host_folds(monkeypatch):
+    """trainer.train's device folds for the boosted family: fold metrics and
+    the final model's trees equal the host-fold path bit for bit."""
+    from paper_2305_01886_b200 import trainer as T
+    from paper_2305_01886_b200.boosting import GradientBoostingRegressor
+
+    rng = np.random.default_rng(8)
+    X = rng.random((30_000, 10)) * 7.0
+    y = 10 + 3 * X[:, 0] + np.cos(X[:, 1]) + rng.normal(0, 0.3, 30_000)
+    names = tuple(f"f{i}" for i in range(10))
+    res = {}
+    for dev in (True, False):
+        monkeypatch.setattr(GradientBoostingRegressor, "_device_input", dev)
+        res[dev] = T.train((X, y, names), "gradient_boosted", n_estimators=12, max_depth=3, seed=1)
+    a, b = res[True], res[False]
+    assert [m.r2 for m in a.fold_metrics] == [m.r2 for m in b.fold_metrics]
+    assert a.model.init_.value == b.model.init_.value
+    for (ea,), (eb,) in zip(a.model.estimators_, b.model.estimators_):
+        for f in ("children_left", "feature", "threshold", "value"):
+            assert np.array_equal(getattr(ea.tree_, f), getattr(eb.tree_, f))
