@@ -1,5 +1,7 @@
 #!/bin/bash
 # fused sweep on config #5 (100k kernels) with / without the persisting-L2 window
+# (GK_SLAB_L2 lived in gk_sched.cu for this measurement only: the window
+# doubled the DRAM writes and cost 4 %, profiles/r2/fused_table_traffic_l2_persist.txt)
 # over the reservation-table slabs (GK_SLAB_L2): points/s and one launch's DRAM bytes
 for v in 1 0; do
   GK_SLAB_L2=$v timeout 600 python bench.py --kernels 100000 --steps 3 --warmup 3 --no-cpu --no-rf --no-c4 --no-c1 --e2e-steps 1 --cycle-kernels 500 2>/dev/null \
