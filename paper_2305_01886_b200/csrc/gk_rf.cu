@@ -21,7 +21,11 @@ namespace cg = cooperative_groups;
 namespace gk {
 
 constexpr int kRfThreads = 128;
-constexpr int kMaxFeat = 64;
+// feature limits: the compact layouts' feature byte (gk_block2/3: 0..254;
+// gk_node8 builders stop at 126) and the fp64 gk_node path's shared tile
+// ((n_feat + 1) x 128 doubles <= 227 KB)
+constexpr int kMaxFeatCompact = 255;
+constexpr int kMaxFeat64 = 220;
 
 struct RfArgs {
     gk_ensemble ens[4];        // up to 4 ensembles selected per row by `arch`
@@ -218,7 +222,7 @@ int gk_launch_rf(const gk_ensemble *ens, uint32_t n_ens, const double *X, int64_
             return -1;
         }
     }
-    if (nf < 1 || nf > (uint32_t)gk::kMaxFeat || ld < (int64_t)nf) {
+    if (nf < 1 || ld < (int64_t)nf) {
         gk_set_error("gk_rf_predict: n_feat=%u ld=%lld unsupported", nf, (long long)ld);
         return -1;
     }
@@ -239,6 +243,10 @@ int gk_launch_rf(const gk_ensemble *ens, uint32_t n_ens, const double *X, int64_
         all_n8 &= ens[a].nodes8 != nullptr;
     }
     if (all_b3 || all_blocks || all_n8) {
+        if (nf > (uint32_t)gk::kMaxFeatCompact) {
+            gk_set_error("gk_rf_predict: n_feat=%u > %d", nf, gk::kMaxFeatCompact);
+            return -1;
+        }
         const int mode = all_b3 ? 2 : all_blocks ? 1 : 0;
         const size_t smem8 = mode == 2 ? (size_t)nf * gk::kRfThreads * sizeof(uint16_t)
                                        : ((size_t)nf + 1) * gk::kRfThreads * sizeof(float);
@@ -284,6 +292,10 @@ int gk_launch_rf(const gk_ensemble *ens, uint32_t n_ens, const double *X, int64_
         k8<<<(unsigned)tiles, gk::kRfThreads, smem8, st>>>(R);
         return gk_check_launch(mode == 2 ? "k4_rf_predict_c<blocks3>"
                                : mode == 1 ? "k4_rf_predict_c<blocks>" : "k4_rf_predict_c<nodes8>");
+    }
+    if (nf > (uint32_t)gk::kMaxFeat64) {
+        gk_set_error("gk_rf_predict: n_feat=%u > %d (fp64 node layout)", nf, gk::kMaxFeat64);
+        return -1;
     }
     // one tile: leading +inf row + [feature][thread] (the staged raw rows are
     // transposed in place through registers)

@@ -24,6 +24,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import warnings
 from dataclasses import dataclass
 
 import numpy as np
@@ -881,8 +882,10 @@ class RandomForestRegressor(_LevelGrower):
                 raise
             # one upload; the input checks and the fixed-point targets run on
             # the device (np.isfinite over config #3's 64M values cost ~0.1 s)
-            X = torch.from_numpy(X).to(dev)
-            yd = torch.from_numpy(y).to(dev)
+            with warnings.catch_warnings():   # read-only views (pandas): only read here
+                warnings.simplefilter("ignore", UserWarning)
+                X = torch.from_numpy(X).to(dev)
+                yd = torch.from_numpy(y).to(dev)
         n, F = X.shape
         if n < 1 or F > 64 * 1024 or n >= 2 ** 31:
             raise ValueError("bad training table shape")

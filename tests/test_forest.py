@@ -411,3 +411,30 @@ def test_train_parity_config3_shape():
     assert abs(mape - ref["mean_mape_pct"]) <= 0.5, (mape, ref["mean_mape_pct"])
     for got, want in zip(res.fold_metrics, ref["folds"]):   # every fold, not just the mean
         assert abs(got.r2 - want["r2"]) <= 0.005
+
+
+@pytest.mark.gpu
+def test_wide_tables_grow_the_same_trees_as_their_informative_columns():
+    """F > 64 takes the wide record stride (16 + 112 bytes at F = 100) and the
+    medium/big kernels for nodes the <= 64-feature CTA kernel would take:
+    appending 40 constant columns (no split candidates) to a 60-column table
+    grows the 60-column forest and boosted model array for array."""
+    from paper_2305_01886_b200.boosting import GradientBoostingRegressor
+    from paper_2305_01886_b200.forest import RandomForestRegressor
+
+    rng = np.random.default_rng(23)
+    X = rng.random((70_000, 60))
+    X[:, 50:] = np.floor(X[:, 50:] * 4)
+    y = 3 * X[:, 0] + np.sin(6 * X[:, 7]) + X[:, 55] + rng.normal(0, 0.1, 70_000)
+    Xw = np.concatenate([X, np.full((70_000, 40), 0.25)], axis=1)
+    fits = []
+    for A in (X, Xw):
+        rf = RandomForestRegressor(5, max_depth=None, random_state=6).fit(A, y)
+        gb = GradientBoostingRegressor(3, max_depth=5, random_state=0).fit(A, y)
+        fits.append(([e.tree_ for e in rf.estimators_] + [e[0].tree_ for e in gb.estimators_],
+                     rf.predict(A[:3000]), gb.predict(A[:3000])))
+    (ta, pa, ga), (tb, pb, gb_) = fits
+    for a, b in zip(ta, tb):
+        for u, v in zip(_tree_arrays(a), _tree_arrays(b)):
+            assert np.array_equal(u, v)
+    assert np.array_equal(pa, pb) and np.array_equal(ga, gb_)
