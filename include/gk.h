@@ -271,7 +271,8 @@ int gk_schedule_features(const gk_corpus *corpus, const gk_grid *grid,
  * writes energy = power * time_us (power.py:171-181, fp64 product).
  * Rows whose status byte (optional) is nonzero get NaN.  n_rows = 0 is a
  * valid empty batch (buffers may then be NULL).  n_feat <= 255 for the
- * compact layouts (nodes8 / blocks / blocks3), <= 220 for the fp64 nodes. */
+ * compact layouts (nodes8 / blocks / blocks3), <= 886 for the fp64 nodes
+ * (32-row tiles above 220 features). */
 int gk_rf_predict(const gk_ensemble *ens, const double *X, int64_t ld, int64_t n_rows,
                   const uint8_t *status, const double *time_us,
                   double *out_power, double *out_energy, void *stream);

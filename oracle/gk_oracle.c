@@ -426,7 +426,7 @@ typedef struct {
 static void rf_range(void *vctx, int64_t lo, int64_t hi) {
     rf_ctx *R = (rf_ctx *)vctx;
     const gk_ensemble *E = R->E;
-    double x[256];
+    double x[1024];
     for (int64_t r = lo; r < hi; r++) {
         if (R->status && R->status[r]) {
             R->power[r] = NAN;
@@ -454,7 +454,7 @@ static void rf_range(void *vctx, int64_t lo, int64_t hi) {
 int gko_rf_predict(const gk_ensemble *E, const double *X, int64_t ld, int64_t n_rows,
                    const uint8_t *status, const double *time_us, double *power,
                    double *energy, int n_threads) {
-    if (E->n_feat > 256) return -1;
+    if (E->n_feat > 1024) return -1;
     rf_ctx R = {E, X, ld, status, time_us, power, energy};
     parallel_for(n_rows, n_threads, rf_range, &R);
     return 0;

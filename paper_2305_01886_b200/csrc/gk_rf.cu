@@ -25,7 +25,9 @@ constexpr int kRfThreads = 128;
 // gk_node8 builders stop at 126) and the fp64 gk_node path's shared tile
 // ((n_feat + 1) x 128 doubles <= 227 KB)
 constexpr int kMaxFeatCompact = 255;
-constexpr int kMaxFeat64 = 220;
+constexpr int kMaxFeat64 = 220;       // 128-row tiles
+constexpr int kWideRows = 32;
+constexpr int kMaxFeatWide = 886;     // 32-row tiles
 
 struct RfArgs {
     gk_ensemble ens[4];        // up to 4 ensembles selected per row by `arch`
@@ -51,16 +53,18 @@ __device__ __forceinline__ void bulk_g2s(void *smem_dst, const void *gsrc, uint3
 
 // kMaxF: compile-time bound on the feature count for the in-place transpose
 // through registers (16 or 32); 0 = no staging, rows read straight from global.
-template <int kMaxF>
-__global__ void __launch_bounds__(kRfThreads) k4_rf_predict(RfArgs R) {
+// kT: rows (threads) per CTA -- 128, or 32 for wide tables (the tile is
+// (n_feat + 1) x kT doubles)
+template <int kMaxF, int kT = kRfThreads>
+__global__ void __launch_bounds__(kT) k4_rf_predict(RfArgs R) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t bar;
-    const int64_t row0 = (int64_t)blockIdx.x * kRfThreads;
-    const int64_t nr = min((int64_t)kRfThreads, R.n_rows - row0);
+    const int64_t row0 = (int64_t)blockIdx.x * kT;
+    const int64_t nr = min((int64_t)kT, R.n_rows - row0);
     const uint32_t nf = R.ens[0].n_feat;
     // one tile: row -1 = +inf (leaf slot), rows 0..nf-1 = [feature][thread]; the
     // raw [thread][feature] rows are staged into rows 0.. and transposed in place
-    double *xt = reinterpret_cast<double *>(smem_raw) + kRfThreads;
+    double *xt = reinterpret_cast<double *>(smem_raw) + kT;
     double *xs = xt;
 
     // ---- stage the row tile (contiguous when ld == n_feat)
@@ -86,7 +90,7 @@ __global__ void __launch_bounds__(kRfThreads) k4_rf_predict(RfArgs R) {
             " @!p bra WAIT_%=;\n}\n" ::"r"(b)
             : "memory");
     } else {
-        for (int64_t q = threadIdx.x; q < nr * nf; q += kRfThreads) {
+        for (int64_t q = threadIdx.x; q < nr * nf; q += kT) {
             const int64_t r = q / nf, f = q % nf;
             xs[r * nf + f] = R.X[(row0 + r) * R.ld + f];
         }
@@ -98,7 +102,7 @@ __global__ void __launch_bounds__(kRfThreads) k4_rf_predict(RfArgs R) {
     const gk_ensemble &E = R.ens[ai < R.n_ens ? ai : 0];
     // scale and transpose to [feature][thread]: the per-visit reads x[f] with a
     // lane-varying f are then bank-conflict-free
-    xt[(int)threadIdx.x - kRfThreads] = __longlong_as_double(0x7ff0000000000000ll);
+    xt[(int)threadIdx.x - kT] = __longlong_as_double(0x7ff0000000000000ll);
     if (kMaxF > 0) {
         double v[kMaxF > 0 ? kMaxF : 1];
 #pragma unroll
@@ -108,10 +112,10 @@ __global__ void __launch_bounds__(kRfThreads) k4_rf_predict(RfArgs R) {
 #pragma unroll
         for (int f = 0; f < kMaxF; f++)
             if (live && f < (int)nf)
-                xt[f * kRfThreads + threadIdx.x] = scale_feature(v[f], E.scale_lo[f], E.scale_hi[f]);
+                xt[f * kT + threadIdx.x] = scale_feature(v[f], E.scale_lo[f], E.scale_hi[f]);
     } else if (live) {
         for (uint32_t f = 0; f < nf; f++)
-            xt[f * kRfThreads + threadIdx.x] =
+            xt[f * kT + threadIdx.x] =
                 scale_feature(R.X[row * R.ld + f], E.scale_lo[f], E.scale_hi[f]);
     }
     if (!live) return;
@@ -121,7 +125,7 @@ __global__ void __launch_bounds__(kRfThreads) k4_rf_predict(RfArgs R) {
         if (R.energy) R.energy[row] = NaN;
         return;
     }
-    const double total = walk_ensemble(E, xt + threadIdx.x, kRfThreads);
+    const double total = walk_ensemble(E, xt + threadIdx.x, kT);
     R.power[row] = total;
     if (R.energy) R.energy[row] = __dmul_rn(total, R.time_us[row]);
 }
@@ -293,27 +297,30 @@ int gk_launch_rf(const gk_ensemble *ens, uint32_t n_ens, const double *X, int64_
         return gk_check_launch(mode == 2 ? "k4_rf_predict_c<blocks3>"
                                : mode == 1 ? "k4_rf_predict_c<blocks>" : "k4_rf_predict_c<nodes8>");
     }
-    if (nf > (uint32_t)gk::kMaxFeat64) {
-        gk_set_error("gk_rf_predict: n_feat=%u > %d (fp64 node layout)", nf, gk::kMaxFeat64);
+    if (nf > (uint32_t)gk::kMaxFeatWide) {
+        gk_set_error("gk_rf_predict: n_feat=%u > %d (fp64 node layout)", nf, gk::kMaxFeatWide);
         return -1;
     }
+    const bool wide = nf > (uint32_t)gk::kMaxFeat64;
+    const int rows_per_cta = wide ? gk::kWideRows : gk::kRfThreads;
     // one tile: leading +inf row + [feature][thread] (the staged raw rows are
     // transposed in place through registers)
-    const size_t smem = ((size_t)nf + 1) * gk::kRfThreads * sizeof(double);
-    const auto kern = nf <= 16 ? gk::k4_rf_predict<16>
+    const size_t smem = ((size_t)nf + 1) * rows_per_cta * sizeof(double);
+    const auto kern = wide ? gk::k4_rf_predict<0, gk::kWideRows>
+                    : nf <= 16 ? gk::k4_rf_predict<16>
                     : nf <= 32 ? gk::k4_rf_predict<32> : gk::k4_rf_predict<0>;
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     // the node gathers live in L1: give shared memory only what resident CTAs need
     {
         int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, gk::kRfThreads, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, rows_per_cta, smem);
         const size_t need = (smem + 1024) * (per_sm > 0 ? per_sm : 1);
         int carve = (int)((need * 100 + 228 * 1024 - 1) / (228 * 1024));
         cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                              carve > 100 ? 100 : carve);
     }
-    const int64_t blocks = (n_rows + gk::kRfThreads - 1) / gk::kRfThreads;
-    kern<<<(unsigned)blocks, gk::kRfThreads, smem, st>>>(R);
+    const int64_t blocks = (n_rows + rows_per_cta - 1) / rows_per_cta;
+    kern<<<(unsigned)blocks, rows_per_cta, smem, st>>>(R);
     return gk_check_launch("k4_rf_predict");
 }

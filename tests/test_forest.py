@@ -438,3 +438,44 @@ def test_wide_tables_grow_the_same_trees_as_their_informative_columns():
         for u, v in zip(_tree_arrays(a), _tree_arrays(b)):
             assert np.array_equal(u, v)
     assert np.array_equal(pa, pb) and np.array_equal(ga, gb_)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["1row", "2rows", "const_y", "const_X", "duplicates"])
+def test_degenerate_tables_match_sklearn(case):
+    """Tables where binning is exact (<= 256 distinct values per column): one
+    row, two rows, a constant target, constant columns (no split: one leaf),
+    duplicated rows -- forest and boosted predictions equal scikit-learn's."""
+    from sklearn.ensemble import GradientBoostingRegressor as SkGB
+    from sklearn.ensemble import RandomForestRegressor as SkRF
+
+    from paper_2305_01886_b200.boosting import GradientBoostingRegressor
+    from paper_2305_01886_b200.forest import RandomForestRegressor
+
+    rng = np.random.default_rng(3)
+    X, y = {"1row": (rng.random((1, 3)), np.array([2.5])),
+            "2rows": (rng.random((2, 3)), np.array([1.0, 3.0])),
+            "const_y": (rng.random((500, 4)), np.full(500, 7.0)),
+            "const_X": (np.ones((500, 4)), rng.random(500)),
+            "duplicates": (np.repeat(rng.random((10, 3)), 100, axis=0),
+                           np.repeat(rng.random(10), 100))}[case]
+    for ours, sk in ((RandomForestRegressor, SkRF), (GradientBoostingRegressor, SkGB)):
+        kw = dict(n_estimators=4, random_state=0)
+        np.testing.assert_allclose(ours(**kw).fit(X, y).predict(X), sk(**kw).fit(X, y).predict(X),
+                                   rtol=0, atol=1e-12)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("F", [255, 300])
+def test_wide_forest_predicts_like_the_oracle_walk(F):
+    """Above 220 features the fp64-node walk runs on 32-row tiles: the forest's
+    device predictions equal the oracle's sequential walk of its trees."""
+    import oracle as O
+    from paper_2305_01886_b200.forest import RandomForestRegressor
+
+    rng = np.random.default_rng(F)
+    X = rng.random((4000, F))
+    y = 2 * X[:, 0] + X[:, F - 1] + rng.normal(0, 0.05, 4000)
+    m = RandomForestRegressor(4, max_depth=9, random_state=0).fit(X, y)
+    want, _ = O.rf_predict(m.flat(), X[:500].astype(np.float32).astype(np.float64))
+    np.testing.assert_allclose(m.predict(X[:500]), np.asarray(want) / 4, rtol=1e-15, atol=0)
