@@ -23,10 +23,12 @@ so F never leaves the device.  Parity bar: R^2 / MAPE (BASELINE.json).
 from __future__ import annotations
 
 import ctypes as C
+import warnings
 
 import numpy as np
 
 from .ensemble import NODE_DT, FlatEnsemble
+from .errors import DeviceError
 from .forest import (TreeEstimator, _check, _LevelGrower, _lib, check_finite, check_n_bins,
                      is_device_tensor)
 
@@ -83,17 +85,26 @@ class GradientBoostingRegressor(_LevelGrower):
         else:
             X = np.ascontiguousarray(X, dtype=np.float64)
             y = np.ascontiguousarray(y, dtype=np.float64).reshape(-1)
+            if X.ndim != 2 or len(y) != len(X):
+                raise ValueError("X and y have different lengths")
+            try:
+                dev = device()
+            except DeviceError:
+                check_finite(X, y)   # sklearn's input errors first, as on a GPU box
+                raise
+            # one upload; the finite check and the bin edges run on the device
+            # (host isfinite + edges cost ~0.1 s of a 100-stage fit at 1M x 64)
+            with warnings.catch_warnings():   # read-only views (pandas): only read here
+                warnings.simplefilter("ignore", UserWarning)
+                X = torch.from_numpy(X).to(dev)
         n, F = X.shape
         if n < 1 or F > 64 * 1024 or n >= 2 ** 31:
             raise ValueError("bad training table shape")
         if len(y) != n:
             raise ValueError("X and y have different lengths")
-        if on_dev:
-            if not bool(torch.isfinite(X).all()):
-                raise ValueError("Input X contains NaN or infinity.")
-            check_finite(np.zeros((1, 1)), y)
-        else:
-            check_finite(X, y)
+        if not bool(torch.isfinite(X).all()):
+            raise ValueError("Input X contains NaN or infinity.")
+        check_finite(np.zeros((1, 1)), y)
         check_n_bins(self.n_bins)
         self.n_features_in_ = F
         L = _lib()

@@ -1698,7 +1698,15 @@ __global__ void __launch_bounds__(256) k5_gb_step(const RfTask *__restrict__ lea
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(GK_FULL, m, o));
-    if ((threadIdx.x & 31) == 0) atomicMax(absmax, (unsigned long long)__double_as_longlong(m));
+    // one atomic per CTA (m >= 0: the bit patterns order like the values)
+    __shared__ unsigned long long wmax[8];
+    if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = (unsigned long long)__double_as_longlong(m);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long b = wmax[0];
+        for (int w = 1; w < (int)(blockDim.x >> 5); w++) b = b > wmax[w] ? b : wmax[w];
+        if (b) atomicMax(absmax, b);
+    }
 }
 
 }  // namespace gk
@@ -1929,12 +1937,15 @@ int gk_rf_leaf_stats(const uint32_t *counts, int64_t n_rows, int32_t n_feat, con
     gk::RfTrainData D{nullptr, yfp, nullptr, counts, n_rows, n_feat, gk::rec_stride(n_feat)};
     const uint8_t *rows0 = (const uint8_t *)recs0, *rows1 = (const uint8_t *)recs1;
     cudaMemsetAsync(out, 0, sizeof(int64_t) * 4 * (size_t)n_leaves, st);
-    // chunks sized by the largest leaf (one 32-lane warp per 2048 rows, <= 64)
+    // chunks sized by the largest leaf: one 32-lane warp per 256 rows, at most
+    // 1024 per leaf and ~2^18 warps per launch (few large leaves -- a boosting
+    // stage's 8 -- fill the GPU; a forest batch's ~1M tiny ones take one each)
     int max_rows = 0;
     if (max_leaf_rows > 0) max_rows = max_leaf_rows;
-    int chunks = (max_rows + 2047) / 2048;
+    int64_t chunks = ((int64_t)max_rows + 255) / 256;
+    const int64_t cap = std::max<int64_t>(1, std::min<int64_t>(1024, (1 << 18) / n_leaves));
+    if (chunks > cap) chunks = cap;
     if (chunks < 1) chunks = 1;
-    if (chunks > 64) chunks = 64;
     gk::k5_leaf_stats<<<dim3((unsigned)n_leaves, (unsigned)chunks), 32, 0, st>>>(
         D, y2fp, (const gk::RfTask *)leaves, n_leaves, rows0, rows1, out);
     return gk_check_launch("k5_leaf_stats");

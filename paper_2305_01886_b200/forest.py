@@ -23,6 +23,7 @@ from sklearn's exact search; the parity bar is R^2 / MAPE (BASELINE.json).
 from __future__ import annotations
 
 import ctypes as C
+import functools
 import os
 import warnings
 from dataclasses import dataclass
@@ -169,6 +170,16 @@ def tree_seeds(random_state, n_estimators: int) -> np.ndarray:
                     dtype=np.int64)
 
 
+@functools.lru_cache(maxsize=8)
+def _sample_rows(n: int, sample: int) -> np.ndarray:
+    """The deterministic edge sample: sorted row ids of default_rng(0).choice
+    (n, sample, replace=False), cached per table height (folds and repeated
+    fits of one table reuse it; the draw costs ~10-30 ms at 1M rows)."""
+    idx = np.sort(np.random.default_rng(0).choice(n, sample, replace=False))
+    idx.setflags(write=False)
+    return idx
+
+
 def bin_edges(Xf: np.ndarray, n_bins: int = N_BINS, sample: int = 65_536, device=None):
     """Per-feature bin edges on float32 data: one bin per distinct value when a
     feature has <= n_bins of them, else quantile edges of a deterministic
@@ -176,17 +187,17 @@ def bin_edges(Xf: np.ndarray, n_bins: int = N_BINS, sample: int = 65_536, device
     `device` when given (sorting is exact: the same sorted columns; it was
     ~1/3 of a 50-stage boosting fit on the host)."""
     n, F = Xf.shape
+    # the sorted sample is kept transposed ([feature][row], each column
+    # contiguous) for the per-feature scan below
     if is_device_tensor(Xf):   # the same rows, sorted on the tensor's device
         import torch
 
         S = Xf
         if n > sample:
-            idx = np.sort(np.random.default_rng(0).choice(n, sample, replace=False))
-            S = Xf.index_select(0, torch.from_numpy(idx).to(Xf.device))
-        S = torch.sort(S.to(torch.float32), dim=0).values.cpu().numpy()
+            S = Xf.index_select(0, torch.from_numpy(_sample_rows(n, sample).copy()).to(Xf.device))
+        S = torch.sort(S.to(torch.float32), dim=0).values.t().contiguous().cpu().numpy()
     elif n > sample:
-        idx = np.random.default_rng(0).choice(n, sample, replace=False)
-        S = Xf[np.sort(idx)]
+        S = Xf[_sample_rows(n, sample)]
     else:
         S = Xf
     if is_device_tensor(Xf):
@@ -195,17 +206,17 @@ def bin_edges(Xf: np.ndarray, n_bins: int = N_BINS, sample: int = 65_536, device
         import torch
 
         S = torch.sort(torch.from_numpy(np.ascontiguousarray(S, dtype=np.float32)).to(device),
-                       dim=0).values.cpu().numpy()
+                       dim=0).values.t().contiguous().cpu().numpy()
     else:
-        S = np.sort(S.astype(np.float32), axis=0)
-    m = S.shape[0]
+        S = np.ascontiguousarray(np.sort(S.astype(np.float32), axis=0).T)
+    m = S.shape[1]
     # k5_bin reads a fixed (N_BINS - 1)-wide edge row per feature; fewer bins
     # use a prefix of it (n_edges[f] <= n_bins - 1)
     edges = np.zeros((F, N_BINS - 1), np.float32)
     n_edges = np.zeros(F, np.int32)
     qpos = (np.linspace(0.0, 1.0, n_bins + 1)[1:-1] * (m - 1)).astype(np.int64)  # "lower"
     for f in range(F):
-        col = S[:, f]
+        col = S[f]
         new = np.empty(m, bool)
         new[0] = True
         np.not_equal(col[1:], col[:-1], out=new[1:])
@@ -632,10 +643,12 @@ class _LevelGrower:
         lv_d = tk[li].contiguous()
         gl = nb_d[lv_d[:, 0].long()] + nd[li].long()
         nl = int(lv_d.shape[0])
-        rd = _Read((lv_d[:, 2] - lv_d[:, 1]).max() if nl else torch.zeros((), dtype=torch.int32,
-                                                                              device=dev))
-        yield rd
-        max_leaf = int(rd.get())
+        if nl <= 256:   # few leaves (boosting stages): n bounds them, no read
+            max_leaf = n
+        else:
+            rd = _Read((lv_d[:, 2] - lv_d[:, 1]).max())
+            yield rd
+            max_leaf = int(rd.get())
         stats_d = torch.empty(4 * max(nl, 1), dtype=i64, device=dev)
         _check(L.gk_rf_leaf_stats(_ptr(counts), n, D["F"], _ptr(D["yfp"]), _ptr(D["y2fp"]), _ptr(lv_d),
                                   nl, _ptr(rows0), _ptr(rows1), _ptr(stats_d), max_leaf, st))
