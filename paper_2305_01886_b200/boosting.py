@@ -23,7 +23,6 @@ so F never leaves the device.  Parity bar: R^2 / MAPE (BASELINE.json).
 from __future__ import annotations
 
 import ctypes as C
-import warnings
 
 import numpy as np
 
@@ -70,7 +69,7 @@ class GradientBoostingRegressor(_LevelGrower):
     def fit(self, X, y, sample_weight=None):
         import torch
 
-        from .runtime import _dev, _ptr, device
+        from .runtime import _dev, _ptr, device, upload
 
         if sample_weight is not None:
             raise NotImplementedError("sample_weight is not supported (training.py never passes it)")
@@ -94,9 +93,7 @@ class GradientBoostingRegressor(_LevelGrower):
                 raise
             # one upload; the finite check and the bin edges run on the device
             # (host isfinite + edges cost ~0.1 s of a 100-stage fit at 1M x 64)
-            with warnings.catch_warnings():   # read-only views (pandas): only read here
-                warnings.simplefilter("ignore", UserWarning)
-                X = torch.from_numpy(X).to(dev)
+            X = upload(X, dev)   # pinned staging ring (runtime.upload)
         n, F = X.shape
         if n < 1 or F > 64 * 1024 or n >= 2 ** 31:
             raise ValueError("bad training table shape")
@@ -191,7 +188,7 @@ class GradientBoostingRegressor(_LevelGrower):
         (sklearn's predict_stages order)."""
         import torch
 
-        from .runtime import DeviceEnsemble, device, rf_predict
+        from .runtime import DeviceEnsemble, device, rf_predict, upload
 
         if getattr(self, "_flat", None) is None:
             self._flat = DeviceEnsemble.upload(self.flat())
@@ -200,7 +197,7 @@ class GradientBoostingRegressor(_LevelGrower):
         else:
             Xf = np.ascontiguousarray(np.asarray(X, dtype=np.float64).astype(np.float32),
                                       np.float64)
-            Xd = torch.from_numpy(Xf).to(device())
+            Xd = upload(Xf, device())
         total, _ = rf_predict(self._flat, Xd)
         return total.cpu().numpy()
 

@@ -25,7 +25,6 @@ from __future__ import annotations
 import ctypes as C
 import functools
 import os
-import warnings
 from dataclasses import dataclass
 
 import numpy as np
@@ -873,7 +872,7 @@ class RandomForestRegressor(_LevelGrower):
     def fit(self, X, y, sample_weight=None):
         import torch
 
-        from .runtime import _dev, _ptr, device
+        from .runtime import _dev, _ptr, device, upload
 
         if sample_weight is not None:
             raise NotImplementedError("sample_weight is not supported (training.py never passes it)")
@@ -895,10 +894,8 @@ class RandomForestRegressor(_LevelGrower):
                 raise
             # one upload; the input checks and the fixed-point targets run on
             # the device (np.isfinite over config #3's 64M values cost ~0.1 s)
-            with warnings.catch_warnings():   # read-only views (pandas): only read here
-                warnings.simplefilter("ignore", UserWarning)
-                X = torch.from_numpy(X).to(dev)
-                yd = torch.from_numpy(y).to(dev)
+            X = upload(X, dev)   # pinned staging ring (runtime.upload)
+            yd = upload(y, dev)
         n, F = X.shape
         if n < 1 or F > 64 * 1024 or n >= 2 ** 31:
             raise ValueError("bad training table shape")
@@ -1058,7 +1055,7 @@ class RandomForestRegressor(_LevelGrower):
         walked on the device."""
         import torch
 
-        from .runtime import device, rf_predict
+        from .runtime import device, rf_predict, upload
 
         if getattr(self, "_flat", None) is None:
             self._flat = self.device_ensemble()
@@ -1067,6 +1064,6 @@ class RandomForestRegressor(_LevelGrower):
         else:
             Xf = np.ascontiguousarray(np.asarray(X, dtype=np.float64).astype(np.float32),
                                       np.float64)
-            Xd = torch.from_numpy(Xf).to(device())
+            Xd = upload(Xf, device())
         total, _ = rf_predict(self._flat, Xd)
         return total.cpu().numpy() / len(self.estimators_)

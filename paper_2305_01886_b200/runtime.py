@@ -10,6 +10,7 @@ fallback: if the library or a CUDA device is missing, every entry point raises
 from __future__ import annotations
 
 import ctypes as C
+import threading
 from dataclasses import dataclass, field
 from pathlib import Path
 
@@ -82,13 +83,61 @@ def _stream(stream=None) -> int:
 
 
 def _dev(a: np.ndarray, dev=None):
-    """numpy -> device tensor of raw bytes (structured dtypes go as uint8)."""
+    """numpy -> device tensor of raw bytes (structured dtypes go as uint8).
+    Large arrays go through the pinned staging ring (upload())."""
     t = _torch()
     a = np.ascontiguousarray(a)
+    if a.nbytes >= _STAGE_MIN:
+        return upload(a.view(np.uint8).reshape(-1) if a.dtype.fields else a, dev)
     if not a.flags.writeable:      # torch.from_numpy wants a writable buffer
         a = a.copy()
     host = t.from_numpy(a.view(np.uint8).reshape(-1) if a.dtype.fields else a)
     return host.to(dev or device(), non_blocking=False)
+
+
+_STAGE_CHUNK = 8 << 20     # bytes per pinned staging buffer
+_STAGE_N = 4               # buffers in the ring
+_STAGE_MIN = 4 * _STAGE_CHUNK
+_stage = {"bufs": None, "events": None}
+_stage_lock = threading.Lock()
+
+
+def upload(a: np.ndarray, dev=None):
+    """Pageable host array -> new device tensor, staged through a ring of
+    pinned buffers: torch's multi-threaded CPU copy fills one buffer while
+    the DMA of the previous ones runs (B200 box, 512 MB fp64 table: 10 ms /
+    52 GB/s vs 46 ms / 11 GB/s for a pageable .to(), tools/upload_probe.py).
+    The copies run on the current stream; the result is ready for work
+    queued after them."""
+    import warnings
+
+    t = _torch()
+    a = np.ascontiguousarray(a)
+    dev = dev or device()
+    with warnings.catch_warnings():   # read-only arrays: only read here
+        warnings.simplefilter("ignore", UserWarning)
+        src = t.from_numpy(a)
+    if a.nbytes < _STAGE_MIN:
+        return src.to(dev)
+    flat = src.reshape(-1).view(t.uint8)
+    out = t.empty(a.nbytes, dtype=t.uint8, device=dev)
+    st = t.cuda.current_stream(dev)
+    with _stage_lock:
+        if _stage["bufs"] is None:
+            _stage["bufs"] = [t.empty(_STAGE_CHUNK, dtype=t.uint8, pin_memory=True)
+                              for _ in range(_STAGE_N)]
+            _stage["events"] = [None] * _STAGE_N
+        bufs, evs = _stage["bufs"], _stage["events"]
+        for i, o in enumerate(range(0, a.nbytes, _STAGE_CHUNK)):
+            k = i % _STAGE_N
+            if evs[k] is not None:
+                evs[k].synchronize()          # the buffer's previous DMA is done
+            c = min(_STAGE_CHUNK, a.nbytes - o)
+            bufs[k][:c].copy_(flat[o:o + c])
+            out[o:o + c].copy_(bufs[k][:c], non_blocking=True)
+            evs[k] = t.cuda.Event()
+            evs[k].record(st)
+    return out.view(src.dtype).view(src.shape)
 
 
 def _ptr(t) -> int | None:

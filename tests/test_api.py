@@ -191,3 +191,31 @@ def test_predict_launches_matches_scalar_faces():
         pw = gk.predict_power(ens, vec.as_dict())
         assert row["power_w"] == pw
         assert row["energy_uj"] == gk.predict_energy(pw, row["time_us"])
+
+
+@pytest.mark.gpu
+def test_staged_upload_equals_the_host_array():
+    """runtime.upload (pinned staging ring): sizes below / at / above the
+    staging threshold, a tail shorter than a chunk, read-only and structured
+    arrays (through _dev), back-to-back calls reusing the ring."""
+    import torch
+
+    import numpy as np
+
+    from paper_2305_01886_b200 import runtime as R
+
+    rng = np.random.default_rng(0)
+    ch = R._STAGE_CHUNK
+    for nbytes in (8, R._STAGE_MIN - 8, R._STAGE_MIN, 5 * ch + 24, 13 * ch + 8):
+        a = rng.random(nbytes // 8)
+        d = R.upload(a)
+        assert d.dtype == torch.float64 and d.shape == a.shape
+        assert np.array_equal(d.cpu().numpy(), a)
+    b = rng.integers(0, 255, (3 * ch, 3), dtype=np.uint8)
+    b.setflags(write=False)
+    assert np.array_equal(R.upload(b).cpu().numpy(), b)
+    s = np.zeros(R._STAGE_MIN // 16 + 3, dtype=[("v", "<f8"), ("f", "<i4"), ("l", "<i4")])
+    s["v"] = rng.random(len(s))
+    s["f"] = np.arange(len(s))
+    got = R._dev(s).cpu().numpy()
+    assert np.array_equal(got, s.view(np.uint8).reshape(-1))
