@@ -347,10 +347,10 @@ def predict_power_batch(ensemble: TreeEnsemble, X, *, time_us=None, status=None)
     """Rows X [n, n_features] (manifest order, raw) -> power [n] (and energy)."""
     import torch
 
-    from .runtime import device, rf_predict
+    from .runtime import device, rf_predict, upload
 
     de = _device_ensemble(ensemble)
-    Xt = torch.as_tensor(np.ascontiguousarray(X, dtype=np.float64)).to(device())
+    Xt = upload(np.ascontiguousarray(X, dtype=np.float64), device())
     if Xt.dim() != 2 or Xt.shape[1] != ensemble.n_features:
         raise EnsembleError(f"expected {ensemble.n_features} feature values per row")
     tu = None if time_us is None else torch.as_tensor(np.asarray(time_us, np.float64)).to(device())

@@ -162,6 +162,7 @@ def broadcast_flat(flat, src: int = 0, group=None, device=None):
     import torch.distributed as dist
 
     from .ensemble import NODE_DT, FlatEnsemble
+    from .runtime import upload
 
     rank = dist.get_rank(group)
     dev = device or collective_device(group)
@@ -173,7 +174,7 @@ def broadcast_flat(flat, src: int = 0, group=None, device=None):
     dist.broadcast_object_list(meta, src=src, group=group)
     m = meta[0]
     if rank == src:
-        nodes = torch.from_numpy(flat.nodes.view(np.uint8).copy()).to(dev)
+        nodes = upload(flat.nodes.view(np.uint8).reshape(-1), dev)
         off = torch.from_numpy(flat.tree_off.copy()).to(dev)
         dep = torch.from_numpy(np.asarray(flat.tree_depth, np.int32).copy()).to(dev)
         sc = torch.from_numpy(np.stack([flat.scale_lo, flat.scale_hi])).to(dev)

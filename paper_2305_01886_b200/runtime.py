@@ -111,12 +111,15 @@ def upload(a: np.ndarray, dev=None):
     queued after them."""
     import warnings
 
-    t = _torch()
+    import torch as t   # (not _torch(): a gloo group's CPU device needs no GPU)
+
     a = np.ascontiguousarray(a)
-    dev = dev or device()
+    dev = dev if dev is not None else device()
     with warnings.catch_warnings():   # read-only arrays: only read here
         warnings.simplefilter("ignore", UserWarning)
         src = t.from_numpy(a)
+    if t.device(dev).type != "cuda":   # e.g. a gloo group's CPU tensors
+        return src.to(dev, copy=True)
     if a.nbytes < _STAGE_MIN:
         return src.to(dev)
     flat = src.reshape(-1).view(t.uint8)

@@ -178,10 +178,10 @@ def train(dataset, family: str = "gradient_boosted", *, n_estimators: int = 500,
     if dev_folds:
         import torch
 
-        from .runtime import device
+        from .runtime import device, upload
 
-        Xd = torch.from_numpy(np.ascontiguousarray(X, dtype=np.float64)).to(device())
-        yd = torch.from_numpy(np.ascontiguousarray(y, dtype=np.float64)).to(device())
+        Xd = upload(np.ascontiguousarray(X, dtype=np.float64), device())
+        yd = upload(np.ascontiguousarray(y, dtype=np.float64), device())
     folds, mapes = [], []
     holdout = np.empty(0, dtype=int)
     for tr, te in KFold(n_splits=N_FOLDS, shuffle=True, random_state=seed).split(X):
@@ -331,7 +331,7 @@ def export_ensemble(result: TrainResult, out_dir, *, n_vectors: int = 20) -> tup
     import torch
 
     from .ensemble import flatten, load_ensemble
-    from .runtime import DeviceEnsemble, device, rf_predict
+    from .runtime import DeviceEnsemble, device, rf_predict, upload
 
     if n_vectors < 1:
         raise TrainerError("need at least one test vector")
@@ -342,7 +342,7 @@ def export_ensemble(result: TrainResult, out_dir, *, n_vectors: int = 20) -> tup
     picked = _sample_rows(result, n_vectors)
     rows = np.ascontiguousarray(np.asarray(result.X, np.float64)[picked])
     de = DeviceEnsemble.upload(flatten(load_ensemble(ensemble_path)))
-    power, _ = rf_predict(de, torch.from_numpy(rows).to(device()))
+    power, _ = rf_predict(de, upload(rows, device()))
     pred = power.cpu().numpy()
     vectors = [{"inputs": {name: float(v) for name, v in zip(result.manifest, row)},
                 "prediction": float(p)} for row, p in zip(rows, pred)]
