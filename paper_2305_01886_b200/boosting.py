@@ -28,8 +28,8 @@ import numpy as np
 
 from .ensemble import NODE_DT, FlatEnsemble
 from .errors import DeviceError
-from .forest import (TreeEstimator, _check, _LevelGrower, _lib, check_finite, check_n_bins,
-                     is_device_tensor)
+from .forest import (Tree, TreeBatch, TreeEstimator, _check, _LevelGrower, _lib, check_finite,
+                     check_n_bins, is_device_tensor)
 
 
 def _shifts(bound: float, n: int) -> tuple[int, int]:
@@ -135,25 +135,59 @@ class GradientBoostingRegressor(_LevelGrower):
         base, m = np.zeros(1, np.int64), np.array([n], np.int64)
         seeds = np.random.RandomState(self.random_state).randint(np.iinfo(np.int32).max,
                                                                    size=self.n_estimators)
-        self.estimators_ = []
-        for k in range(self.n_estimators):
-            _check(L.gk_rf_compact(_ptr(counts), 1, n, _ptr(Xb), F, _ptr(yfp), _ptr(base_d),
-                                   _ptr(rows0), _ptr(fill), st))
-            trees, (lv, lv_d, leaf_value) = self._grow(counts, base, m, rows0, rows1, 1)
-            self.estimators_.append([TreeEstimator(tree_=trees[0], random_state=int(seeds[k]))])
-            if k + 1 == self.n_estimators:
-                break
-            # next stage's fixed point: |y - F_new| <= (1 + lr) max |y - F| (leaf means
-            # are averages of the current residuals)
-            shift, shift2 = _shifts(rmax * (1.0 + self.learning_rate) * (1.0 + 1e-9) + 1e-300, n)
-            lvals = torch.from_numpy(self.learning_rate * leaf_value).to(dev)
-            absmax.zero_()
-            size = lv["end"] - lv["begin"]
-            _check(L.gk_gb_step(_ptr(lv_d), len(lv), _ptr(lvals), _ptr(rows0), _ptr(rows1), F,
-                                _ptr(yd), _ptr(Fd), _ptr(yfp), _ptr(y2fp), shift, shift2,
-                                _ptr(absmax), int(size.max()), st))
-            rmax = float(absmax.cpu().numpy().view(np.float64)[0])
-            self._dev["shift"], self._dev["shift2"] = shift, shift2
+        # a stage reads only its three level sizes: the tree stays on the device
+        # (depths read once after the loop), the leaf values feed the residual
+        # update on the device, and max |y - F| comes back asynchronously --
+        # the next stage's levels run before it is needed
+        absmax_h = torch.zeros(1, dtype=torch.int64, pin_memory=True)
+        absmax_ev = None
+        pending = []
+        self._defer_reads = True
+        try:
+            for k in range(self.n_estimators):
+                _check(L.gk_rf_compact(_ptr(counts), 1, n, _ptr(Xb), F, _ptr(yfp), _ptr(base_d),
+                                       _ptr(rows0), _ptr(fill), st))
+                tree_d, leaves = self._grow(counts, base, m, rows0, rows1, 1)
+                if isinstance(tree_d, list):   # GK_RF_HOST_LEVELS=1: host trees, host leaves
+                    lv, lv_d, leaf_value = leaves
+                    nl, leaf_val_d = len(lv), torch.from_numpy(leaf_value).to(dev)
+                else:
+                    nl, lv_d, leaf_val_d = leaves
+                pending.append(tree_d)
+                if k + 1 == self.n_estimators:
+                    break
+                if absmax_ev is not None:   # max |y - F| after the previous stage
+                    absmax_ev.synchronize()
+                    rmax = float(absmax_h.numpy().view(np.float64)[0])
+                # next stage's fixed point: |y - F_new| <= (1 + lr) max |y - F| (leaf
+                # means are averages of the current residuals)
+                shift, shift2 = _shifts(rmax * (1.0 + self.learning_rate) * (1.0 + 1e-9)
+                                        + 1e-300, n)
+                lvals = leaf_val_d * self.learning_rate   # the fp64 product numpy formed
+                absmax.zero_()
+                _check(L.gk_gb_step(_ptr(lv_d), nl, _ptr(lvals), _ptr(rows0), _ptr(rows1), F,
+                                    _ptr(yd), _ptr(Fd), _ptr(yfp), _ptr(y2fp), shift, shift2,
+                                    _ptr(absmax), n, st))
+                absmax_h.copy_(absmax, non_blocking=True)
+                absmax_ev = torch.cuda.Event()
+                absmax_ev.record()
+                self._dev["shift"], self._dev["shift2"] = shift, shift2
+        finally:
+            self._defer_reads = False
+        dev_trees = [p for p in pending if not isinstance(p, list)]
+        depths = (torch.cat([p[4] for p in dev_trees]).cpu().numpy() if dev_trees
+                  else np.zeros(0, np.int64))
+        self.estimators_, j = [], 0
+        for k, p in enumerate(pending):
+            if isinstance(p, list):
+                tree = p[0]
+            else:
+                fl, it, node_base, next_id, _ = p
+                batch = TreeBatch(fl, it, node_base, next_id, depths[j: j + 1])
+                tree = Tree(node_count=int(next_id[0]), max_depth=int(depths[j]), batch=batch,
+                            start=0)
+                j += 1
+            self.estimators_.append([TreeEstimator(tree_=tree, random_state=int(seeds[k]))])
         self.n_estimators_ = len(self.estimators_)
         self._flat = None
         del self._dev, self._dev_thr

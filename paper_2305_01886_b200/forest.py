@@ -606,10 +606,13 @@ class _LevelGrower:
             tasks_d, node_d, lists_d, cap = tasks_n, node_n, lists_n, 2 * nt
             par_slot = par_next
 
-        rd = _Read(next_id_d)
-        yield rd
-        return (yield from self._assemble_dev(counts, rows0, rows1, TB, records,
-                                              rd.get().astype(np.int64)))
+        if TB == 1:   # one tree: every node is a task of exactly one level
+            next_id = np.array([sum(r[4] for r in records)], np.int64)
+        else:
+            rd = _Read(next_id_d)
+            yield rd
+            next_id = rd.get().astype(np.int64)
+        return (yield from self._assemble_dev(counts, rows0, rows1, TB, records, next_id))
 
     def _assemble_dev(self, counts, rows0, rows1, TB, records, next_id):
         """_assemble on the device: node arrays by scatter from the level records,
@@ -678,6 +681,10 @@ class _LevelGrower:
                                       _ptr(self._dev_thr), D["shift"], D["shift2"], _ptr(fl),
                                       _ptr(it), st))
         leaf_val_d = fl[1][gl]
+        if TB == 1 and getattr(self, "_defer_reads", False):
+            # boosting stages: nothing read here; the caller keeps the tree's
+            # device arrays and reads every stage's depth once, after the loop
+            return (fl, it, node_base, next_id, depth_d), (nl, lv_d, leaf_val_d)
         reads = [_Read(leaf_val_d), _Read(depth_d), _Read(lv_d)]
         yield reads[-1]
         leaf_value, tree_depth, lv = (r.get() for r in reads)
