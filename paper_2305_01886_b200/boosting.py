@@ -165,6 +165,8 @@ class GradientBoostingRegressor(_LevelGrower):
                                         + 1e-300, n)
                 lvals = leaf_val_d * self.learning_rate   # the fp64 product numpy formed
                 absmax.zero_()
+                # n bounds the leaf sizes (the launcher caps CTAs per leaf by the
+                # leaf count, so deep unbounded stages stay small grids)
                 _check(L.gk_gb_step(_ptr(lv_d), nl, _ptr(lvals), _ptr(rows0), _ptr(rows1), F,
                                     _ptr(yd), _ptr(Fd), _ptr(yfp), _ptr(y2fp), shift, shift2,
                                     _ptr(absmax), n, st))

@@ -1990,8 +1990,12 @@ int gk_gb_step(const void *leaves, int32_t n_leaves, const double *leaf_val,
         return -1;
     }
     const cudaStream_t st = (cudaStream_t)stream;
+    // 256 rows per CTA of the largest leaf, at most 1024 CTAs per leaf and
+    // ~2^18 CTAs per launch (max_leaf_rows may be a bound: n for a stage of
+    // few leaves, whose sizes are not read back)
     int64_t chunks = ((int64_t)max_leaf_rows + 255) / 256;
-    if (chunks > 1024) chunks = 1024;
+    const int64_t cap = std::max<int64_t>(1, std::min<int64_t>(1024, (1 << 18) / n_leaves));
+    if (chunks > cap) chunks = cap;
     if (chunks < 1) chunks = 1;
     dim3 grid((unsigned)n_leaves, (unsigned)chunks);
     gk::k5_gb_step<<<grid, 256, 0, st>>>((const gk::RfTask *)leaves, leaf_val,

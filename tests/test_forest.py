@@ -209,15 +209,20 @@ def test_device_level_bookkeeping_equals_host_form(monkeypatch, rows, depth, tre
 
 
 @pytest.mark.gpu
-def test_device_level_bookkeeping_equals_host_form_gbt(monkeypatch):
+@pytest.mark.parametrize("rows,depth,stages", [(50_000, 4, 12), (20_000, None, 4)])
+def test_device_level_bookkeeping_equals_host_form_gbt(monkeypatch, rows, depth, stages):
+    """Boosting stages on the device path (no per-stage tree reads, leaf values
+    scaled on the device, grids from bounds) equal the host level loop: a
+    depth-4 model and an unbounded one (~10^4 leaves per stage)."""
     from paper_2305_01886_b200.boosting import GradientBoostingRegressor
 
     rng = np.random.default_rng(8)
-    X = rng.random((50_000, 10))
-    y = 5 * X[:, 0] - 2 * X[:, 3] ** 2 + rng.normal(0, 0.05, 50_000)
-    got = GradientBoostingRegressor(12, learning_rate=0.1, max_depth=4, random_state=0).fit(X, y)
+    X = rng.random((rows, 10))
+    y = 5 * X[:, 0] - 2 * X[:, 3] ** 2 + rng.normal(0, 0.05, rows)
+    kw = dict(learning_rate=0.1, max_depth=depth, random_state=0)
+    got = GradientBoostingRegressor(stages, **kw).fit(X, y)
     monkeypatch.setenv("GK_RF_HOST_LEVELS", "1")
-    want = GradientBoostingRegressor(12, learning_rate=0.1, max_depth=4, random_state=0).fit(X, y)
+    want = GradientBoostingRegressor(stages, **kw).fit(X, y)
     for (a,), (b,) in zip(got.estimators_, want.estimators_):
         for u, v in zip(_tree_arrays(a.tree_), _tree_arrays(b.tree_)):
             assert np.array_equal(u, v)
