@@ -246,8 +246,11 @@ def check_n_bins(n_bins) -> int:
 
 
 def check_finite(X: np.ndarray, y: np.ndarray) -> None:
-    """scikit-learn rejects NaN / inf in X and y (check_X_y, force_all_finite):
-    same error class here, before anything reaches the device."""
+    """NaN / inf in X or y raise ValueError before anything reaches the device.
+    scikit-learn raises the same for inf, and for NaN in boosting; its forest
+    (>= 1.4) would route NaN as a missing value, which K5 does not implement --
+    the reference never passes NaN (its Dataset rejects missing values before
+    any fit, dataset.py:57-58)."""
     if not np.isfinite(X).all():
         raise ValueError("Input X contains NaN or infinity.")
     if not np.isfinite(y).all():
