@@ -59,3 +59,20 @@ for e in ev:
 print("top host self time:")
 for n, v in sorted(tot.items(), key=lambda kv: -kv[1])[:12]:
     print(f"  {n[:60]:60s} {v / 1e3:8.1f} ms")
+# GPU idle gaps and the host ops running in them (summed by op name)
+cpu = [e for e in ev if e.device_type == torch.autograd.DeviceType.CPU]
+gaps, ce = [], None
+for s_, e_ in iv:
+    if ce is not None and s_ > ce:
+        gaps.append((ce, s_))
+    ce = e_ if ce is None else max(ce, e_)
+print(f"idle gaps: {len(gaps)}, total {sum(b - a for a, b in gaps) / 1e3:.1f} ms")
+inside = {}
+for e in cpu:
+    for a, b in gaps:
+        ov = min(b, e.time_range.end) - max(a, e.time_range.start)
+        if ov > 0:
+            inside[e.name] = inside.get(e.name, 0) + ov
+print("host ops overlapping the gaps (us, summed):")
+for n_, v in sorted(inside.items(), key=lambda kv: -kv[1])[:16]:
+    print(f"  {n_[:60]:60s} {v / 1e3:8.2f} ms")
